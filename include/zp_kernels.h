@@ -1,0 +1,47 @@
+/*
+ * zp_kernels.h — C ABI of the individual sm_100a kernels of the heterogeneous-ZeRO step.
+ *
+ * These entry points are what the step driver (zp_runtime.h) launches; they are exported
+ * separately so parity tests can drive each kernel on device buffers. All pointers are
+ * device pointers; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Every function returns 0 on success or a ZP_E* code (zp_host.h) and never throws.
+ *
+ * Reference counterpart: none of these exist in the reference, which models the whole
+ * device step as the closed form `compute_fixed + compute_per_batch * b`
+ * (proj/core/src/hardware.cpp:160-167) and `optimizer_time` (hardware.cpp:168).
+ */
+#ifndef ZP_KERNELS_H_
+#define ZP_KERNELS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GEMM: C[z][m,n] = epilogue(alpha * sum_k A[z][m,k] * B[z][n,k]), bf16 in, fp32 accumulate.
+ * major: 0 = K-major (elem (r,k) at ptr[r*ld+k]), 1 = MN-major (elem (r,k) at ptr[k*ld+r]).
+ * epilogue: 0 store bf16, 1 store f32, 2 accumulate f32, 3 +bias bf16, 4 +bias+residual bf16,
+ *           5 +bias then GELU (pre-activation to aux_out) bf16, 6 times GELU'(aux) bf16.
+ * causal:   0 none, 1 skip tiles above the diagonal, 2 k <= tile last row, 3 k >= tile first row.
+ */
+typedef struct zp_gemm_desc {
+  int32_t M, N, K, nb1, nb2;
+  const void* a; int32_t a_major; int64_t lda, a_bs1, a_bs2;
+  const void* b; int32_t b_major; int64_t ldb, b_bs1, b_bs2;
+  void* c; int64_t ldc, c_bs1, c_bs2;
+  float alpha;
+  int32_t epilogue;
+  int32_t causal;
+  const void* bias;
+  const void* aux;
+  void* aux_out;
+  int32_t max_ctas;
+} zp_gemm_desc;
+
+int zp_gemm(const zp_gemm_desc* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZP_KERNELS_H_ */

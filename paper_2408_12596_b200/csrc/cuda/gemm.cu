@@ -1,0 +1,470 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+// One CTA per SM (grid capped by the rank's SM budget). Warp roles:
+//   warp 0      : TMA producer (one elected thread), SWIZZLE_128B tiles into an S-stage ring
+//   warp 1      : MMA issuer (one thread), tcgen05.mma 128xBNx16 into a double-buffered TMEM
+//                 accumulator (2*BN columns)
+//   warp 2      : TMEM allocator
+//   warps 4..7  : epilogue, tcgen05.ld 32x32b -> registers -> fused epilogue -> global
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA) and TMEM full/empty mbarriers
+// (MMA <-> epilogue), so the epilogue of tile i overlaps the mainloop of tile i+1.
+#include <cstdio>
+#include <mutex>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace zp {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128-byte swizzle span of bf16
+constexpr int kThreads = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kATileBytes = kBM * kBK * 2;
+  static constexpr int kBTileBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kATileBytes + kBTileBytes;
+  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+struct TileInfo {
+  int z1, z2, m0, n0, kb0, kb1;
+  bool skip;
+};
+
+struct Sched {
+  int m_tiles, n_tiles, nb1, total;
+  int M, N, K, BN, causal;
+  __device__ TileInfo tile(int t) const {
+    TileInfo ti;
+    const int per_batch = m_tiles * n_tiles;
+    const int z = t / per_batch;
+    const int r = t - z * per_batch;
+    const int mb = r / n_tiles;
+    const int nb = r - mb * n_tiles;
+    ti.z1 = z % nb1;
+    ti.z2 = z / nb1;
+    ti.m0 = mb * kBM;
+    ti.n0 = nb * BN;
+    int kb0 = 0, kb1 = (K + kBK - 1) / kBK;
+    ti.skip = false;
+    if (causal == kCausalSkipUpper) {
+      ti.skip = ti.n0 > ti.m0 + kBM - 1;
+    } else if (causal == kCausalKUpper) {
+      const int kend = min(K, ti.m0 + kBM);
+      kb1 = (kend + kBK - 1) / kBK;
+    } else if (causal == kCausalKLower) {
+      kb0 = ti.m0 / kBK;
+    }
+    ti.kb0 = kb0;
+    ti.kb1 = kb1;
+    if (kb1 <= kb0) ti.skip = true;
+    return ti;
+  }
+};
+
+struct EpiParams {
+  void* c;
+  int64_t ldc, cs1, cs2;
+  float alpha;
+  int epilogue;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* aux;
+  __nv_bfloat16* aux_out;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * x * (1.0f + t);
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+}
+
+// Writes 32 consecutive columns [n, n+32) of one row.
+__device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32_t (&acc)[32],
+                                               int64_t off, int n, int N) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]);
+  const bool full = (n + 32 <= N);
+  const int e = ep.epilogue;
+  if (e == kEpiStoreF32 || e == kEpiAccumF32) {
+    float* c = static_cast<float*>(ep.c) + off;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 o = make_float4(ep.alpha * v[i], ep.alpha * v[i + 1], ep.alpha * v[i + 2],
+                               ep.alpha * v[i + 3]);
+        if (e == kEpiAccumF32) {
+          const float4 p = *reinterpret_cast<const float4*>(c + i);
+          o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+        }
+        *reinterpret_cast<float4*>(c + i) = o;
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i) {
+        const float o = ep.alpha * v[i];
+        c[i] = (e == kEpiAccumF32) ? c[i] + o : o;
+      }
+    }
+    return;
+  }
+  // bf16 outputs
+  if (e == kEpiStoreBf16) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+  } else if (e == kEpiBiasBf16 || e == kEpiBiasResidBf16 || e == kEpiBiasGeluBf16) {
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        const uint4 braw = *reinterpret_cast<const uint4*>(ep.bias + n + i);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 bf = __bfloat1622float2(b2[j]);
+          v[i + 2 * j] += bf.x;
+          v[i + 2 * j + 1] += bf.y;
+        }
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i) v[i] += __bfloat162float(ep.bias[n + i]);
+    }
+    if (e == kEpiBiasResidBf16) {
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 rraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rraw);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 rf = __bfloat1622float2(r2[j]);
+            v[i + 2 * j] += rf.x;
+            v[i + 2 * j + 1] += rf.y;
+          }
+        }
+      } else {
+        for (int i = 0; i < 32 && n + i < N; ++i) v[i] += __bfloat162float(ep.aux[off + i]);
+      }
+    } else if (e == kEpiBiasGeluBf16) {
+      __nv_bfloat16* u = ep.aux_out + off;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 o;
+          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+          *reinterpret_cast<uint4*>(u + i) = o;
+        }
+      } else {
+        for (int i = 0; i < 32 && n + i < N; ++i) u[i] = __float2bfloat16_rn(v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+    }
+  } else if (e == kEpiGeluBwdBf16) {
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        const uint4 uraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
+        const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uraw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 uf = __bfloat1622float2(u2[j]);
+          v[i + 2 * j] *= gelu_tanh_grad(uf.x);
+          v[i + 2 * j + 1] *= gelu_tanh_grad(uf.y);
+        }
+      }
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i)
+        v[i] *= gelu_tanh_grad(__bfloat162float(ep.aux[off + i]));
+    }
+  }
+  __nv_bfloat16* c = static_cast<__nv_bfloat16*>(ep.c) + off;
+  if (full) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+      *reinterpret_cast<uint4*>(c + i) = o;
+    }
+  } else {
+    for (int i = 0; i < 32 && n + i < N; ++i) c[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b, Sched sched, EpiParams ep) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::kStages * C::kATileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::kStages;
+  uint64_t* tfull = bars + 2 * C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = ptx::warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_a);
+    ptx::tma_prefetch_desc(&map_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 128);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+        const TileInfo ti = sched.tile(t);
+        if (ti.skip) continue;
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* sa = smem_a + stage * C::kATileBytes;
+          uint8_t* sb = smem_b + stage * C::kBTileBytes;
+          const int k0 = kb * kBK;
+          if (A_MN) {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              ptx::tma_load_4d(sa + j * 64 * kBK * 2, &map_a, &full[stage], ti.m0 + 64 * j, k0,
+                               ti.z1, ti.z2);
+          } else {
+            ptx::tma_load_4d(sa, &map_a, &full[stage], k0, ti.m0, ti.z1, ti.z2);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              ptx::tma_load_4d(sb + j * 64 * kBK * 2, &map_b, &full[stage], ti.n0 + 64 * j, k0,
+                               ti.z1, ti.z2);
+          } else {
+            ptx::tma_load_4d(sb, &map_b, &full[stage], k0, ti.n0, ti.z1, ti.z2);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+        const TileInfo ti = sched.tile(t);
+        if (ti.skip) continue;
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem_a + stage * C::kATileBytes);
+          const uint32_t sb = ptx::smem_u32(smem_b + stage * C::kBTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // K-major: advance 16 elements (32 B) inside the 128 B swizzle row.
+            // MN-major: advance 16 K-rows (2 x 1024 B swizzle atoms); LBO = 64-wide MN chunk.
+            const uint64_t da = A_MN ? ptx::smem_desc_sw128(sa + kk * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 64 * kBK * 2, 1024)
+                                     : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
+            ptx::umma_bf16(d_tmem, da, db, idesc, (kb > ti.kb0 || kk > 0) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);
+        ++local;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;  // TMEM lane quarter
+    int local = 0;
+    for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+      const TileInfo ti = sched.tile(t);
+      if (ti.skip) continue;
+      const int acc = local & 1;
+      ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ptx::tc_fence_after();
+      const int row = ti.m0 + q * 32 + lane;
+      const int64_t row_off = ti.z1 * ep.cs1 + ti.z2 * ep.cs2 + int64_t(row) * ep.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + c + (uint32_t(q * 32) << 16), r);
+        ptx::tmem_ld_wait();
+        const int n = ti.n0 + c;
+        if (row < sched.M && n < sched.N) epilogue_row32(ep, r, row_off + n, n, sched.N);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      ++local;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// rows x inner matrix (inner contiguous), plus two batch dims; box = {64, box_rows}.
+bool make_map(CUtensorMap* map, const GemmOperand& op, int64_t inner, int64_t rows, int nb1,
+              int nb2, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(nb1), cuuint64_t(nb2)};
+  // Strides for dims 1..3 in bytes; batch strides of size-1 dims must still be valid.
+  const int64_t row_bytes = op.ld * 2;
+  const int64_t s1 = (nb1 > 1 ? op.bs1 : rows * op.ld) * 2;
+  const int64_t s2 = (nb2 > 1 ? op.bs2 : s1 * nb1 / 2) * 2;
+  cuuint64_t strides[3] = {cuuint64_t(row_bytes), cuuint64_t(s1), cuuint64_t(s2)};
+  cuuint32_t box[4] = {64, cuuint32_t(box_rows), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(op.ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, int A_MN, int B_MN>
+cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  const bool ok_a = A_MN ? make_map(&ma, a.a, a.M, a.K, a.nb1, a.nb2, 64)
+                         : make_map(&ma, a.a, a.K, a.M, a.nb1, a.nb2, kBM);
+  const bool ok_b = B_MN ? make_map(&mb, a.b, a.N, a.K, a.nb1, a.nb2, 64)
+                         : make_map(&mb, a.b, a.K, a.N, a.nb1, a.nb2, BN);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  Sched s;
+  s.m_tiles = (a.M + kBM - 1) / kBM;
+  s.n_tiles = (a.N + BN - 1) / BN;
+  s.nb1 = a.nb1;
+  s.total = s.m_tiles * s.n_tiles * a.nb1 * a.nb2;
+  s.M = a.M;
+  s.N = a.N;
+  s.K = a.K;
+  s.BN = BN;
+  s.causal = a.causal;
+  EpiParams ep;
+  ep.c = a.c;
+  ep.ldc = a.ldc;
+  ep.cs1 = a.cs1;
+  ep.cs2 = a.cs2;
+  ep.alpha = a.alpha;
+  ep.epilogue = a.epilogue;
+  ep.bias = static_cast<const __nv_bfloat16*>(a.bias);
+  ep.aux = static_cast<const __nv_bfloat16*>(a.aux);
+  ep.aux_out = static_cast<__nv_bfloat16*>(a.aux_out);
+  int grid = num_sms();
+  if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
+  if (s.total < grid) grid = s.total;
+  if (grid < 1) return cudaSuccess;
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, s, ep);
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_major(const GemmArgs& a, cudaStream_t s) {
+  if (a.a.major == kKMajor && a.b.major == kKMajor) return launch<BN, 0, 0>(a, s);
+  if (a.a.major == kKMajor && a.b.major == kMNMajor) return launch<BN, 0, 1>(a, s);
+  if (a.a.major == kMNMajor && a.b.major == kKMajor) return launch<BN, 1, 0>(a, s);
+  return launch<BN, 1, 1>(a, s);
+}
+
+}  // namespace
+
+cudaError_t gemm(const GemmArgs& a, cudaStream_t stream) {
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.nb1 <= 0 || a.nb2 <= 0) return cudaErrorInvalidValue;
+  if ((a.a.ld % 8) || (a.b.ld % 8) || (a.ldc % 8)) return cudaErrorInvalidValue;
+  if (a.N <= 64) return dispatch_major<64>(a, stream);
+  if (a.N <= 128) return dispatch_major<128>(a, stream);
+  return dispatch_major<256>(a, stream);
+}
+
+}  // namespace zp

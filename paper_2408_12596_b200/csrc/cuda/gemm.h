@@ -1,0 +1,62 @@
+// Dense bf16 GEMM on sm_100a tensor cores (tcgen05 + TMEM + TMA), host-side interface.
+//
+//   C[z][m, n] = epilogue( alpha * sum_k A[z][m, k] * B[z][n, k] )
+//
+// A is logically [M, K], B is logically [N, K] (i.e. the product is A * B^T).
+// Each operand is stored either K-major (element (r, k) at ptr[r*ld + k]) or
+// MN-major (element (r, k) at ptr[k*ld + r]); this covers the forward
+// (X W^T), data-gradient (dY W) and weight-gradient (dY^T X) products of a
+// linear layer without any transpose pass. A batch index z = z1 + nb1*z2 maps
+// to element offsets z1*bs1 + z2*bs2, so per-(sample, head) attention GEMMs
+// read head slices of the fused QKV activation in place.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zp {
+
+enum GemmMajor : int { kKMajor = 0, kMNMajor = 1 };
+
+enum GemmEpilogue : int {
+  kEpiStoreBf16 = 0,      // C(bf16) = alpha*acc
+  kEpiStoreF32 = 1,       // C(f32)  = alpha*acc
+  kEpiAccumF32 = 2,       // C(f32) += alpha*acc
+  kEpiBiasBf16 = 3,       // C(bf16) = acc + bias[n]
+  kEpiBiasResidBf16 = 4,  // C(bf16) = acc + bias[n] + R[m, n]   (R may alias C)
+  kEpiBiasGeluBf16 = 5,   // U(bf16) = acc + bias[n];  C(bf16) = gelu(U)
+  kEpiGeluBwdBf16 = 6,    // C(bf16) = acc * gelu'(U[m, n])
+};
+
+enum GemmCausal : int {
+  kCausalNone = 0,
+  kCausalSkipUpper = 1,  // skip tiles whose first column is past the tile's last row
+  kCausalKUpper = 2,     // reduce only over k <= last row of the tile (A is lower-triangular)
+  kCausalKLower = 3,     // reduce only over k >= first row of the tile (A is upper-triangular)
+};
+
+struct GemmOperand {
+  const void* ptr = nullptr;  // bf16
+  int major = kKMajor;
+  int64_t ld = 0;             // elements between stored rows
+  int64_t bs1 = 0, bs2 = 0;   // batch strides in elements
+};
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0;
+  int nb1 = 1, nb2 = 1;
+  GemmOperand a, b;
+  void* c = nullptr;
+  int64_t ldc = 0, cs1 = 0, cs2 = 0;  // C row stride / batch strides (elements)
+  float alpha = 1.0f;
+  int epilogue = kEpiStoreBf16;
+  int causal = kCausalNone;
+  const void* bias = nullptr;  // bf16 [N]
+  const void* aux = nullptr;   // bf16, same layout as C (residual R or pre-activation U)
+  void* aux_out = nullptr;     // bf16, same layout as C (U written by kEpiBiasGeluBf16)
+  int max_ctas = 0;            // SM budget cap (0 = all SMs)
+};
+
+// Returns cudaSuccess or the launch/encode error.
+cudaError_t gemm(const GemmArgs& args, cudaStream_t stream);
+
+}  // namespace zp

@@ -1,0 +1,196 @@
+"""tcgen05 GEMM parity against a plain PyTorch fp32 reference of the same product.
+
+Tolerance: inputs are exact bf16, accumulation is fp32 on both sides, so the only
+difference is summation order (and the bf16 rounding of the output when the
+epilogue emits bf16): rel-Frobenius error <= 1e-5 (f32 out) / 8e-3 (bf16 out).
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2408_12596_b200 import _lib
+    return _lib
+
+
+def run_gemm(A_store, a_major, B_store, b_major, M, N, K, out_dtype=torch.float32, epilogue=None,
+             alpha=1.0, causal=0, nb=(1, 1), a_bs=(0, 0), b_bs=(0, 0), c=None, ldc=None, c_bs=(0, 0),
+             bias=None, aux=None, aux_out=None, lda=None, ldb=None, max_ctas=0, sync=True):
+    L = _lib()
+    if c is None:
+        c = torch.zeros(nb[1] * nb[0] * M * N, dtype=out_dtype, device=A_store.device)
+        ldc = N
+        c_bs = (M * N, M * N * nb[0])
+    if epilogue is None:
+        epilogue = 1 if out_dtype == torch.float32 else 0
+    d = L.GemmDesc()
+    d.M, d.N, d.K, d.nb1, d.nb2 = M, N, K, nb[0], nb[1]
+    d.a, d.a_major = A_store.data_ptr(), a_major
+    d.lda = lda if lda is not None else (K if a_major == 0 else M)
+    d.a_bs1, d.a_bs2 = a_bs
+    d.b, d.b_major = B_store.data_ptr(), b_major
+    d.ldb = ldb if ldb is not None else (K if b_major == 0 else N)
+    d.b_bs1, d.b_bs2 = b_bs
+    d.c, d.ldc, d.c_bs1, d.c_bs2 = c.data_ptr(), ldc, c_bs[0], c_bs[1]
+    d.alpha = alpha
+    d.epilogue = epilogue
+    d.causal = causal
+    d.bias = bias.data_ptr() if bias is not None else None
+    d.aux = aux.data_ptr() if aux is not None else None
+    d.aux_out = aux_out.data_ptr() if aux_out is not None else None
+    d.max_ctas = max_ctas
+    rc = L.lib.zp_gemm(d, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    if sync:
+        torch.cuda.synchronize()
+    return c
+
+
+def relerr(x, ref):
+    return ((x.float() - ref.float()).norm() / ref.float().norm().clamp_min(1e-30)).item()
+
+
+SHAPES = [(128, 64, 64), (256, 256, 128), (384, 320, 200), (1024, 2304, 768), (200, 130, 70),
+          (512, 768, 3072)]
+
+
+@pytest.mark.parametrize("a_major", [0, 1])
+@pytest.mark.parametrize("b_major", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_majors(cuda, a_major, b_major, shape):
+    M, N, K = shape
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(M, K, generator=g).to(torch.bfloat16).to(cuda)
+    B = torch.randn(N, K, generator=g).to(torch.bfloat16).to(cuda)
+    if (a_major == 1 and M % 8) or (b_major == 1 and N % 8) or (a_major == 0 and K % 8) or (b_major == 0 and K % 8):
+        pytest.skip("row stride must be a multiple of 8 elements")
+    A_store = A.contiguous() if a_major == 0 else A.t().contiguous()
+    B_store = B.contiguous() if b_major == 0 else B.t().contiguous()
+    C = run_gemm(A_store, a_major, B_store, b_major, M, N, K).view(M, N)
+    ref = A.float() @ B.float().t()
+    assert relerr(C, ref) < 1e-5
+
+
+def test_gemm_bf16_out_alpha(cuda):
+    M, N, K = 512, 384, 256
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = torch.randn(N, K, device=cuda).to(torch.bfloat16)
+    C = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, alpha=0.125).view(M, N)
+    ref = 0.125 * (A.float() @ B.float().t())
+    assert relerr(C, ref) < 8e-3
+
+
+def test_gemm_accumulate(cuda):
+    M, N, K = 256, 512, 128
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = torch.randn(N, K, device=cuda).to(torch.bfloat16)
+    C0 = torch.randn(M * N, device=cuda)
+    C = C0.clone()
+    run_gemm(A, 0, B, 0, M, N, K, epilogue=2, alpha=0.5, c=C, ldc=N)
+    ref = C0.view(M, N) + 0.5 * (A.float() @ B.float().t())
+    assert relerr(C.view(M, N), ref) < 1e-5
+
+
+def test_gemm_bias_resid_gelu(cuda):
+    M, N, K = 256, 768, 256
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = (0.1 * torch.randn(N, K, device=cuda)).to(torch.bfloat16)
+    bias = torch.randn(N, device=cuda).to(torch.bfloat16)
+    R = torch.randn(M, N, device=cuda).to(torch.bfloat16)
+    acc = A.float() @ B.float().t()
+    C = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, epilogue=3, bias=bias).view(M, N)
+    assert relerr(C, acc + bias.float()) < 8e-3
+    C = R.clone()
+    run_gemm(A, 0, B, 0, M, N, K, epilogue=4, bias=bias, aux=C, c=C, ldc=N)
+    assert relerr(C, acc + bias.float() + R.float()) < 8e-3
+    U = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    C = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, epilogue=5, bias=bias, aux_out=U).view(M, N)
+    u = acc + bias.float()
+    assert relerr(U, u) < 8e-3
+    assert relerr(C, torch.nn.functional.gelu(u, approximate="tanh")) < 1e-2
+    D = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, epilogue=6, aux=U).view(M, N)
+    uu = U.float().requires_grad_(True)
+    y = torch.nn.functional.gelu(uu, approximate="tanh")
+    (gp,) = torch.autograd.grad(y.sum(), uu)
+    assert relerr(D, acc * gp) < 1e-2
+
+
+def test_gemm_attention_batched_heads(cuda):
+    # S[z=(head, sample)] = Q_h K_h^T read in place from a fused [b*s, 3h] QKV activation.
+    b, s, H, d = 2, 256, 4, 64
+    h = H * d
+    qkv = torch.randn(b * s, 3 * h, device=cuda).to(torch.bfloat16)
+    q = qkv[:, :h].view(b, s, H, d).permute(0, 2, 1, 3)
+    k = qkv[:, h:2 * h].view(b, s, H, d).permute(0, 2, 1, 3)
+    v = qkv[:, 2 * h:].view(b, s, H, d).permute(0, 2, 1, 3)
+    S = torch.zeros(b * H * s * s, device=cuda)
+    base = qkv.data_ptr()
+    esz = 2
+    Q_store = qkv  # pointer adjusted below through a view
+    run_gemm(qkv[:, :], 0, qkv[:, h:], 0, s, s, d, nb=(H, b), a_bs=(d, s * 3 * h), b_bs=(d, s * 3 * h),
+             lda=3 * h, ldb=3 * h, c=S, ldc=s, c_bs=(s * s, H * s * s), alpha=0.125)
+    ref = 0.125 * (q.float() @ k.float().transpose(-1, -2))
+    assert relerr(S.view(b, H, s, s), ref) < 1e-5
+    # O = P V with V MN-major (d contiguous), written into [b*s, h] at head offsets.
+    P = torch.softmax(ref, -1).to(torch.bfloat16)
+    O = torch.zeros(b * s, h, device=cuda, dtype=torch.bfloat16)
+    run_gemm(P, 0, qkv[:, 2 * h:], 1, s, d, s, nb=(H, b), a_bs=(s * s, H * s * s), b_bs=(d, s * 3 * h),
+             lda=s, ldb=3 * h, c=O, ldc=h, c_bs=(d, s * h), out_dtype=torch.bfloat16, epilogue=0)
+    refO = (P.float() @ v.float()).permute(0, 2, 1, 3).reshape(b * s, h)
+    assert relerr(O, refO) < 8e-3
+
+
+def test_gemm_causal_modes(cuda):
+    s, d = 512, 64
+    Q = torch.randn(s, d, device=cuda).to(torch.bfloat16)
+    Kt = torch.randn(s, d, device=cuda).to(torch.bfloat16)
+    S = torch.full((s * s,), 7.0, device=cuda)
+    run_gemm(Q, 0, Kt, 0, s, s, d, c=S, ldc=s, causal=1)
+    ref = Q.float() @ Kt.float().t()
+    S = S.view(s, s)
+    for mb in range(s // 128):
+        for nb in range(s // 256):
+            blk = S[mb * 128:(mb + 1) * 128, nb * 256:(nb + 1) * 256]
+            if nb * 256 > mb * 128 + 127:
+                assert torch.all(blk == 7.0)
+            else:
+                assert relerr(blk, ref[mb * 128:(mb + 1) * 128, nb * 256:(nb + 1) * 256]) < 1e-5
+    # K-upper: A lower triangular (P), reduce only up to the tile's last row.
+    P = torch.tril(torch.randn(s, s, device=cuda)).to(torch.bfloat16)
+    V = torch.randn(s, d, device=cuda).to(torch.bfloat16)
+    O = run_gemm(P, 0, V, 1, s, d, s, causal=2).view(s, d)
+    assert relerr(O, P.float() @ V.float()) < 1e-5
+    # K-lower: A = P^T is upper triangular; A MN-major view of P.
+    G = torch.randn(s, d, device=cuda).to(torch.bfloat16)
+    dV = run_gemm(P, 1, G, 1, s, d, s, causal=3).view(s, d)
+    assert relerr(dV, P.float().t() @ G.float()) < 1e-5
+
+
+def test_gemm_sm_budget(cuda):
+    M, N, K = 1024, 1024, 512
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = torch.randn(N, K, device=cuda).to(torch.bfloat16)
+    C = run_gemm(A, 0, B, 0, M, N, K, max_ctas=7).view(M, N)
+    assert relerr(C, A.float() @ B.float().t()) < 1e-5
+
+
+def test_gemm_perf_smoke(cuda):
+    """Not a gate: prints achieved TFLOP/s of a large K-major GEMM."""
+    M, N, K = 8192, 8192, 8192
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = torch.randn(N, K, device=cuda).to(torch.bfloat16)
+    C = torch.empty(M * N, device=cuda, dtype=torch.bfloat16)
+    for _ in range(3):
+        run_gemm(A, 0, B, 0, M, N, K, c=C, ldc=N, epilogue=0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        run_gemm(A, 0, B, 0, M, N, K, c=C, ldc=N, epilogue=0, sync=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"\n[gemm 8192^3 bf16] {ms:.3f} ms  {2 * M * N * K / ms / 1e9:.1f} TFLOP/s")
