@@ -22,7 +22,7 @@ def _load():
         raise ZpLibraryMissing(
             f"{LIB_PATH} not found: the CUDA extension is not built "
             "(run `python paper_2408_12596_b200/build.py`)")
-    return C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    return C.CDLL(LIB_PATH)
 
 
 lib = _load()

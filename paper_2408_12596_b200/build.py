@@ -81,7 +81,7 @@ def build(verbose: bool = False) -> str:
     if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
             "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart", "-lnccl",
-            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
+            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64"), "-Xlinker", "-Bsymbolic"]
         _compile(cmd)
     return LIB
 
