@@ -1,0 +1,602 @@
+// HBM-bound kernels: embedding, LayerNorm, causal softmax, cross-entropy, reductions,
+// and the ZeRO accumulate / AdamW update. 16-byte vector accesses, warp-shuffle
+// reductions, grid-stride loops capped at the rank's CTA budget.
+#include <cmath>
+
+#include "kernels.h"
+
+namespace zp {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+int grid_for(int64_t work_items, int per_block, int ctas, int per_sm = 4) {
+  int64_t g = (work_items + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(ctas) * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+// ------------------------------------------------------------------ init / data
+
+__global__ void init_normal_k(float* p32, bf16* p16, int64_t n, float stdv, uint64_t seed,
+                              uint64_t offset) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t h1 = mix64(seed ^ mix64(offset + uint64_t(i)));
+    const uint64_t h2 = mix64(h1 ^ 0x5851f42d4c957f2dull);
+    const float u1 = (float((h1 >> 40) + 1) * (1.0f / 16777217.0f));
+    const float u2 = float(h2 >> 40) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+    const float v = __bfloat162float(__float2bfloat16_rn(stdv * z));  // bf16-representable master
+    if (p32) p32[i] = v;
+    if (p16) p16[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void init_const_k(float* p32, bf16* p16, int64_t n, float value) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (p32) p32[i] = value;
+    if (p16) p16[i] = __float2bfloat16_rn(value);
+  }
+}
+
+__global__ void synth_tokens_k(int32_t* tok, int64_t first, int64_t count, int sp1, int vocab,
+                               uint64_t seed, uint64_t it) {
+  const int64_t total = count * sp1;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = first + i / sp1;
+    const int64_t t = i % sp1;
+    const uint64_t h = mix64(mix64(mix64(seed ^ 0x7f4a7c15ull) ^ it) ^ (uint64_t(j) << 20 | uint64_t(t)));
+    tok[i] = int32_t(h % uint64_t(vocab));
+  }
+}
+
+// ------------------------------------------------------------------ embedding
+
+// x[r] = wte[tok[r]] + wpe[r % seq]; tokens are [samples, seq+1] (inputs are columns 0..seq-1).
+__global__ void embed_fwd_k(const int32_t* tok, int seq, const bf16* wte, const bf16* wpe, bf16* x,
+                            int64_t rows, int h) {
+  const int vec = h / 8;
+  const int64_t total = rows * vec;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vec;
+    const int c = int(i % vec) * 8;
+    const int64_t smp = r / seq;
+    const int pos = int(r % seq);
+    const int32_t t = tok[smp * (seq + 1) + pos];
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(wte + int64_t(t) * h + c), a);
+    unpack8(*reinterpret_cast<const uint4*>(wpe + int64_t(pos) * h + c), b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += b[k];
+    *reinterpret_cast<uint4*>(x + r * h + c) = pack8(a);
+  }
+}
+
+__global__ void embed_bwd_k(const int32_t* tok, int seq, const bf16* dx, float* dwte, float* dwpe,
+                            int64_t rows, int h) {
+  const int vec = h / 8;
+  const int64_t total = rows * vec;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / vec;
+    const int c = int(i % vec) * 8;
+    const int64_t smp = r / seq;
+    const int pos = int(r % seq);
+    const int32_t t = tok[smp * (seq + 1) + pos];
+    float d[8];
+    unpack8(*reinterpret_cast<const uint4*>(dx + r * h + c), d);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      atomicAdd(dwte + int64_t(t) * h + c + k, d[k]);
+      atomicAdd(dwpe + int64_t(pos) * h + c + k, d[k]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ LayerNorm (one warp per row)
+
+template <int NC>  // h = NC * 256
+__global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
+                                                     const bf16* __restrict__ g,
+                                                     const bf16* __restrict__ b, bf16* y,
+                                                     float* mean, float* rstd, int64_t rows) {
+  constexpr int h = NC * 256;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    float v[NC][8];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      unpack8(*reinterpret_cast<const uint4*>(x + r * h + (c * 32 + lane) * 8), v[c]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[c][k];
+    }
+    const float mu = warp_sum(s) * (1.0f / h);
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float d = v[c][k] - mu;
+        q += d * d;
+      }
+    const float rs = rsqrtf(warp_sum(q) * (1.0f / h) + 1e-5f);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      float gg[8], bb[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+      unpack8(*reinterpret_cast<const uint4*>(b + col), bb);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = (v[c][k] - mu) * rs * gg[k] + bb[k];
+      *reinterpret_cast<uint4*>(y + r * h + col) = pack8(o);
+    }
+    if (lane == 0) {
+      mean[r] = mu;
+      rstd[r] = rs;
+    }
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy,
+                                                     const bf16* __restrict__ x,
+                                                     const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd,
+                                                     const bf16* __restrict__ g,
+                                                     const bf16* dres, bf16* dx, float* part,
+                                                     int64_t rows) {
+  constexpr int h = NC * 256;
+  __shared__ float sg[h], sb[h];
+  for (int i = threadIdx.x; i < h; i += kThreads) sg[i] = sb[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  float accg[NC][8], accb[NC][8];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) accg[c][k] = accb[c][k] = 0.f;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const float mu = mean[r], rs = rstd[r];
+    float xh[NC][8], gd[NC][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      float xv[8], dv[8], gg[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + r * h + col), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dy + r * h + col), dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        xh[c][k] = (xv[k] - mu) * rs;
+        gd[c][k] = gg[k] * dv[k];
+        s1 += gd[c][k];
+        s2 += gd[c][k] * xh[c][k];
+        accg[c][k] += dv[k] * xh[c][k];
+        accb[c][k] += dv[k];
+      }
+    }
+    const float m1 = warp_sum(s1) * (1.0f / h);
+    const float m2 = warp_sum(s2) * (1.0f / h);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      float o[8], rr[8];
+      if (dres) {
+        unpack8(*reinterpret_cast<const uint4*>(dres + r * h + col), rr);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rr[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o[k] = rr[k] + rs * (gd[c][k] - m1 - xh[c][k] * m2);
+      *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int col = (c * 32 + lane) * 8 + k;
+      atomicAdd(&sg[col], accg[c][k]);
+      atomicAdd(&sb[col], accb[c][k]);
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < h; i += kThreads) {
+    part[int64_t(blockIdx.x) * h + i] = sg[i];
+    part[int64_t(gridDim.x + blockIdx.x) * h + i] = sb[i];
+  }
+}
+
+// ------------------------------------------------------------------ causal softmax
+
+// Row r of S (fp32, row length seq) is query q = r % seq; keys 0..q are valid. P gets zeros in
+// (q, kend) with kend = the end of q's 128-row tile, the K range the P*V GEMM reduces over.
+__global__ void softmax_fwd_k(const float* S, bf16* P, int64_t rows, int seq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const int q = int(r % seq);
+    const float* s = S + r * seq;
+    bf16* p = P + r * seq;
+    const int nvalid = q + 1;
+    const int kend = min(seq, (q / 128 + 1) * 128);
+    float mx = -INFINITY;
+    for (int k = lane; k < nvalid; k += 32) mx = fmaxf(mx, s[k]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int k = lane; k < nvalid; k += 32) sum += __expf(s[k] - mx);
+    const float inv = 1.0f / warp_sum(sum);
+    for (int k = lane; k < kend; k += 32)
+      p[k] = __float2bfloat16_rn(k < nvalid ? __expf(s[k] - mx) * inv : 0.f);
+  }
+}
+
+__global__ void softmax_bwd_k(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows,
+                              int seq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const int q = int(r % seq);
+    const bf16* p = P + r * seq;
+    const float* dp = dP + r * seq;
+    bf16* ds = dS + r * seq;
+    const int nvalid = q + 1;
+    const int kend = min(seq, (q / 128 + 1) * 128);
+    float dot = 0.f;
+    for (int k = lane; k < nvalid; k += 32) dot += __bfloat162float(p[k]) * dp[k];
+    dot = warp_sum(dot);
+    for (int k = lane; k < kend; k += 32) {
+      const float v = k < nvalid ? scale * __bfloat162float(p[k]) * (dp[k] - dot) : 0.f;
+      ds[k] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ cross-entropy
+
+__device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  v = is_max ? warp_max(v) : warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float t = (threadIdx.x < kThreads / 32) ? sh[threadIdx.x] : (is_max ? -INFINITY : 0.f);
+  if (w == 0) t = is_max ? warp_max(t) : warp_sum(t);
+  if (threadIdx.x == 0) sh[0] = t;
+  __syncthreads();
+  return sh[0];
+}
+
+__global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* tok, int seq,
+                                                 int64_t rows, int vocab, int ldv, float gscale,
+                                                 float* row_loss) {
+  __shared__ float sh[32];
+  const int nvec = ldv / 8;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    bf16* lg = logits + r * ldv;
+    const int64_t smp = r / seq;
+    const int pos = int(r % seq);
+    const int target = tok[smp * (seq + 1) + pos + 1];
+    float mx = -INFINITY;
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i * 8 + k < vocab) mx = fmaxf(mx, f[k]);
+    }
+    mx = block_reduce(mx, sh, true);
+    float sum = 0.f;
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i * 8 + k < vocab) sum += __expf(f[k] - mx);
+    }
+    sum = block_reduce(sum, sh, false);
+    const float lse = mx + logf(sum);
+    const float tl = __bfloat162float(lg[target]);
+    __syncthreads();  // everyone has read lg[target] before it is overwritten
+    const float inv = 1.0f / sum;
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int col = i * 8 + k;
+        float gv = 0.f;
+        if (col < vocab) gv = (__expf(f[k] - mx) * inv - (col == target ? 1.f : 0.f)) * gscale;
+        f[k] = gv;
+      }
+      *reinterpret_cast<uint4*>(lg + i * 8) = pack8(f);
+    }
+    if (threadIdx.x == 0) row_loss[r] = lse - tl;
+  }
+}
+
+// ------------------------------------------------------------------ reductions
+
+// Partial column sums: block (32, 8) covers 64 columns (2 per thread) x one row chunk.
+__global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_t chunk,
+                              float* work) {
+  __shared__ float sh[8][64];
+  const int c = blockIdx.x * 64 + threadIdx.x * 2;
+  const int64_t r0 = blockIdx.y * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  float a = 0.f, b = 0.f;
+  if (c < N) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(X + r * ld + c));
+      a += v.x;
+      b += v.y;
+    }
+  }
+  sh[threadIdx.y][threadIdx.x * 2] = a;
+  sh[threadIdx.y][threadIdx.x * 2 + 1] = b;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < N) {
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      s0 += sh[k][threadIdx.x * 2];
+      s1 += sh[k][threadIdx.x * 2 + 1];
+    }
+    work[int64_t(blockIdx.y) * N + c] = s0;
+    if (c + 1 < N) work[int64_t(blockIdx.y) * N + c + 1] = s1;
+  }
+}
+
+__global__ void sum_partials_k(const float* part, int nparts, int N, bf16* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float s = 0.f;
+  for (int k = 0; k < nparts; ++k) s += part[int64_t(k) * N + c];
+  out[c] = __float2bfloat16_rn(s);
+}
+
+__global__ void cast_k(const float* in, bf16* out, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+__global__ void reduce_sum_k(const float* x, int64_t n, float* out) {
+  __shared__ float sh[32];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) s += x[i];
+  s = block_reduce(s, sh, false);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------------ ZeRO: accumulate / AdamW
+
+__global__ void add_f32_k(float* dst, const float* src, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+__global__ void accumulate_k(float* acc, const bf16* src, int64_t n, bool overwrite) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint2 raw = reinterpret_cast<const uint2*>(src)[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+    float4 o = make_float4(a.x, a.y, b.x, b.y);
+    if (!overwrite) {
+      const float4 p = reinterpret_cast<const float4*>(acc)[i];
+      o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+    }
+    reinterpret_cast<float4*>(acc)[i] = o;
+  }
+}
+
+// 4 elements per thread-iteration: 16 B of p32, m, v (+acc) and 8 B of bf16 grad / params.
+__global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, float* __restrict__ m,
+                                                   float* __restrict__ v, bf16* __restrict__ p16,
+                                                   const float* __restrict__ acc,
+                                                   const bf16* __restrict__ g16,
+                                                   const float* __restrict__ g32, int64_t n,
+                                                   AdamParams ap) {
+  const int64_t n4 = n / 4;
+  const float inv_bc1 = 1.0f / ap.bc1;
+  const float inv_sqrt_bc2 = rsqrtf(ap.bc2);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    if (acc) {
+      const float4 a = reinterpret_cast<const float4*>(acc)[i];
+      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w;
+    }
+    if (g16) {
+      const uint2 raw = reinterpret_cast<const uint2*>(g16)[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+      g[0] += a.x; g[1] += a.y; g[2] += b.x; g[3] += b.y;
+    }
+    if (g32) {
+      const float4 a = reinterpret_cast<const float4*>(g32)[i];
+      g[0] += a.x; g[1] += a.y; g[2] += a.z; g[3] += a.w;
+    }
+    float4 pp = reinterpret_cast<float4*>(p32)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float* P = &pp.x;
+    float* M = &mm.x;
+    float* V = &vv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      M[k] = ap.beta1 * M[k] + (1.f - ap.beta1) * g[k];
+      V[k] = ap.beta2 * V[k] + (1.f - ap.beta2) * g[k] * g[k];
+      const float denom = sqrtf(V[k]) * inv_sqrt_bc2 + ap.eps;
+      P[k] -= ap.lr * ((M[k] * inv_bc1) / denom + ap.weight_decay * P[k]);
+    }
+    reinterpret_cast<float4*>(p32)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    uint2 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+    oh[0] = __floats2bfloat162_rn(pp.x, pp.y);
+    oh[1] = __floats2bfloat162_rn(pp.z, pp.w);
+    reinterpret_cast<uint2*>(p16)[i] = o;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+
+void init_normal(float* p32, bf16* p16, int64_t n, float stdv, uint64_t seed, uint64_t offset,
+                 int ctas, cudaStream_t s) {
+  init_normal_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, stdv, seed, offset);
+}
+void init_const(float* p32, bf16* p16, int64_t n, float value, int ctas, cudaStream_t s) {
+  init_const_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, value);
+}
+void synth_tokens(int32_t* tokens, int64_t first, int64_t count, int sp1, int vocab, uint64_t seed,
+                  uint64_t it, int ctas, cudaStream_t s) {
+  if (count <= 0) return;
+  synth_tokens_k<<<grid_for(count * sp1, kThreads, ctas), kThreads, 0, s>>>(tokens, first, count,
+                                                                          sp1, vocab, seed, it);
+}
+void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe, bf16* x,
+               int64_t rows, int h, int ctas, cudaStream_t s) {
+  embed_fwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, wte, wpe, x,
+                                                                          rows, h);
+}
+void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
+               int64_t rows, int h, int ctas, cudaStream_t s) {
+  embed_bwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, dx, dwte32,
+                                                                          dwpe32, rows, h);
+}
+
+#define ZP_LN_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(12) X(16)
+
+cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean,
+                          float* rstd, int64_t rows, int h, int ctas, cudaStream_t s) {
+  const int grid = grid_for(rows, kThreads / 32, ctas, 8);
+  switch (h / 256) {
+#define X(NC)                                                                     \
+  case NC:                                                                        \
+    if (h % 256) return cudaErrorInvalidValue;                                    \
+    ln_fwd_k<NC><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows);         \
+    return cudaGetLastError();
+    ZP_LN_CASES(X)
+#undef X
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
+                          const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
+                          int64_t rows, int h, int ctas, cudaStream_t s) {
+  const int grid = grid_for(rows, kThreads / 32, ctas, 2);
+  *nblk = grid;
+  switch (h / 256) {
+#define X(NC)                                                                              \
+  case NC:                                                                                 \
+    if (h % 256) return cudaErrorInvalidValue;                                             \
+    ln_bwd_k<NC><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows);    \
+    return cudaGetLastError();
+    ZP_LN_CASES(X)
+#undef X
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+void softmax_causal_fwd(const float* S, bf16* P, int64_t rows, int seq, int ctas, cudaStream_t s) {
+  softmax_fwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(S, P, rows, seq);
+}
+void softmax_causal_bwd(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows, int seq,
+                        int ctas, cudaStream_t s) {
+  softmax_bwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(P, dP, dS, scale, rows,
+                                                                            seq);
+}
+void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
+                           int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s) {
+  ce_k<<<grid_for(rows, 1, ctas, 8), kThreads, 0, s>>>(logits, tokens, seq, rows, vocab, ldv,
+                                                      grad_scale, row_loss);
+}
+
+void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* out, int ctas,
+                 cudaStream_t s) {
+  const int col_blocks = (N + 63) / 64;
+  int chunks = (ctas * 4 + col_blocks - 1) / col_blocks;
+  if (chunks < 1) chunks = 1;
+  if (chunks > 256) chunks = 256;
+  const int64_t chunk = (rows + chunks - 1) / chunks;
+  chunks = int((rows + chunk - 1) / chunk);
+  colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work);
+  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, out);
+}
+void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s) {
+  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(part, nparts, N, out);
+}
+void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
+  cast_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(in, out, n);
+}
+void reduce_sum_f32(const float* x, int64_t n, float* out, cudaStream_t s) {
+  reduce_sum_k<<<1, kThreads, 0, s>>>(x, n, out);
+}
+void add_f32(float* dst, const float* src, int64_t n, int ctas, cudaStream_t s) {
+  add_f32_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(dst, src, n);
+}
+void accumulate_bf16(float* acc, const bf16* src, int64_t n, bool overwrite, int ctas,
+                     cudaStream_t s) {
+  accumulate_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(acc, src, n, overwrite);
+}
+void adam_update(float* p32, float* m, float* v, bf16* p16, const float* acc, const bf16* g16,
+                 const float* g32, int64_t n, const AdamParams& ap, int ctas, cudaStream_t s) {
+  adam_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(p32, m, v, p16, acc, g16, g32, n, ap);
+}
+
+}  // namespace zp

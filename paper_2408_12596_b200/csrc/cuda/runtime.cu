@@ -1,0 +1,1032 @@
+// B200 device back end of the heterogeneous-ZeRO step (include/zp_runtime.h).
+//
+// One runtime per rank (one process per GPU). Everything the rank holds lives in one
+// capped arena (the emulated HBM capacity): flat bf16 parameters, the bf16 gradient of the
+// current micro-step, the stage's fp32 master / Adam state / accumulators, fixed workspaces,
+// and — per step — the activations of the local micro-batch. OOM is the arena refusing the
+// activation reservation, which is exactly the reference's `resident + act*b > total` rule
+// (proj/core/src/hardware.cpp:152-158) realised by an allocator.
+//
+// Per micro-step: GPT forward/backward on sm_100a kernels (gemm.cu, kernels.cu); the local
+// gradient is pre-weighted by b_i/B through the loss scale 1/(B*seq). Collectives per stage
+// (proj/core/include/zeroplan/comm.hpp:25-37): Z0 all-reduce of the fp32 gradient at sync;
+// Z1 reduce-scatter + all-gather at sync; Z2 bf16 reduce-scatter every micro-step + all-gather
+// of updated parameters at sync; Z3 adds the forward/backward parameter all-gathers. The
+// optimizer is AdamW on the rank's shard, fused with the shard's gradient accumulation.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../../include/zp_runtime.h"
+#include "profiler_search.hpp"
+#include "gemm.h"
+#include "kernels.h"
+
+namespace zp {
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ::zp::g_err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;          \
+      throw ::zp::Fail{ZP_ECUDA};                                                           \
+    }                                                                                 \
+  } while (0)
+#define NK(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess) {                                                          \
+      ::zp::g_err = std::string("NCCL: ") + ncclGetErrorString(r_) + " at " #call;         \
+      throw ::zp::Fail{ZP_ENCCL};                                                           \
+    }                                                                                 \
+  } while (0)
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_err = msg;
+  throw Fail{code};
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------ arena
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, used = 0, high = 0;
+  void* take(size_t bytes) {
+    const size_t off = (used + 255) & ~size_t(255);
+    if (off + bytes > cap) return nullptr;
+    used = off + bytes;
+    if (used > high) high = used;
+    return base + off;
+  }
+  template <class T>
+  T* take_n(int64_t n) {
+    return static_cast<T*>(take(size_t(n) * sizeof(T)));
+  }
+};
+
+// ------------------------------------------------------------------ parameter layout
+struct Tensor {
+  int64_t off = 0, rows = 0, cols = 0;
+  int64_t numel() const { return rows * cols; }
+};
+struct LayerP {
+  Tensor ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc, b_fc, w_proj, b_proj;
+};
+struct Layout {
+  Tensor wte, wpe, lnf_g, lnf_b;
+  std::vector<LayerP> layers;
+  std::map<std::string, Tensor> by_name;
+  int64_t logical = 0, total = 0;
+};
+
+Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
+  Layout L;
+  int64_t cur = 0;
+  auto add = [&](const std::string& name, int64_t r, int64_t k, int64_t logical_rows) {
+    Tensor t;
+    t.off = cur;
+    t.rows = r;
+    t.cols = k;
+    cur = round_up(cur + r * k, 64);
+    L.logical += logical_rows * k;
+    L.by_name[name] = t;
+    return t;
+  };
+  const int h = c.d_model, f = c.d_ff;
+  L.wte = add("wte", vocab_pad, h, c.vocab);
+  L.wpe = add("wpe", c.seq_len, h, c.seq_len);
+  for (int i = 0; i < c.n_layer; ++i) {
+    const std::string p = "h" + std::to_string(i) + ".";
+    LayerP l;
+    l.ln1_g = add(p + "ln1_g", 1, h, 1);
+    l.ln1_b = add(p + "ln1_b", 1, h, 1);
+    l.w_qkv = add(p + "w_qkv", 3 * h, h, 3 * h);
+    l.b_qkv = add(p + "b_qkv", 1, 3 * h, 1);
+    l.w_o = add(p + "w_o", h, h, h);
+    l.b_o = add(p + "b_o", 1, h, 1);
+    l.ln2_g = add(p + "ln2_g", 1, h, 1);
+    l.ln2_b = add(p + "ln2_b", 1, h, 1);
+    l.w_fc = add(p + "w_fc", f, h, f);
+    l.b_fc = add(p + "b_fc", 1, f, 1);
+    l.w_proj = add(p + "w_proj", h, f, h);
+    l.b_proj = add(p + "b_proj", 1, h, 1);
+    L.layers.push_back(l);
+  }
+  L.lnf_g = add("lnf_g", 1, h, 1);
+  L.lnf_b = add("lnf_b", 1, h, 1);
+  L.total = round_up(cur, int64_t(world) * 256);
+  return L;
+}
+
+// ------------------------------------------------------------------ activations of one micro-step
+struct LayerActs {
+  bf16 *x_in, *ln1, *qkv, *P, *attn, *x_mid, *ln2, *u, *g;
+  float *mu1, *rs1, *mu2, *rs2;
+};
+struct Acts {
+  int64_t b = 0;
+  std::vector<LayerActs> l;
+  bf16 *x_final, *lnf, *logits;
+  float *muf, *rsf, *row_loss;
+  float* S;  // [b, H, s, s] fp32: attention scores, reused for dP
+  bf16* dS;  // [b, H, s, s]
+  bf16 *dx, *dx2, *dln, *dO, *dqkv, *du;
+};
+
+// ------------------------------------------------------------------ event timing
+enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4 };
+struct Span {
+  int kind, start, end;
+};
+struct Timer {
+  std::vector<cudaEvent_t> ev;
+  std::vector<Span> spans;
+  int next = 0;
+  void init(int n) {
+    ev.resize(n);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+  }
+  void destroy() {
+    for (auto& e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+  void reset() {
+    next = 0;
+    spans.clear();
+  }
+  int mark(cudaStream_t s) {
+    if (next >= int(ev.size())) fail(ZP_EINTERNAL, "event pool exhausted");
+    CK(cudaEventRecord(ev[next], s));
+    return next++;
+  }
+  void close(int kind, int start, cudaStream_t s) { spans.push_back({kind, start, mark(s)}); }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ runtime
+struct Runtime {
+  zp_runtime_desc d{};
+  zp_gpt_config c{};
+  int vocab_pad = 0;
+  int n = 1, rank = 0;
+  int ctas = 148;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  Layout lay;
+  Arena arena;
+  int stage = -1;
+  size_t resident_mark = 0;
+  int64_t adam_t = 0;
+  bool keep_grads = false;
+
+  // persistent state (per configured stage)
+  bf16* p16 = nullptr;   // [total] full bf16 parameters
+  bf16* g16 = nullptr;   // [total] bf16 gradient of the current micro-step
+  float* p32 = nullptr;  // master (full at Z0, shard otherwise)
+  float* m32 = nullptr;
+  float* v32 = nullptr;
+  float* acc = nullptr;   // Z0/1: [total] fp32 local accumulation; Z2: [shard] accumulation
+  float* r32 = nullptr;   // Z1: [shard] reduce-scatter output
+  bf16* r16 = nullptr;    // Z2: [shard] reduce-scatter output
+  float* gkeep = nullptr; // summed gradient of the last iteration (parity)
+  float* dwte32 = nullptr;
+  float* dwpe32 = nullptr;
+  float* ln_part = nullptr;
+  float* col_work = nullptr;
+  float* loss_steps = nullptr;  // [kMaxSteps]
+  int32_t* tokens = nullptr;
+  int64_t tokens_cap = 0, tokens_count = 0;
+  float last_gscale = 0.f;
+  cudaEvent_t marks[8] = {};
+  Timer tm;
+  static constexpr int kMaxSteps = 4096;
+
+  int64_t shard() const { return lay.total / n; }
+  int64_t shard_begin() const { return stage == 0 ? 0 : shard() * rank; }
+  int64_t state_len() const { return stage == 0 ? lay.total : shard(); }
+
+  // ---------------------------------------------------------------- GEMM helpers
+  void mm(int M, int N, int K, const bf16* A, int amaj, int64_t lda, const bf16* B, int bmaj,
+          int64_t ldb, void* C, int64_t ldc, int epi, float alpha = 1.f, const bf16* bias = nullptr,
+          const bf16* aux = nullptr, bf16* aux_out = nullptr) {
+    GemmArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.a.ptr = A; g.a.major = amaj; g.a.ld = lda;
+    g.b.ptr = B; g.b.major = bmaj; g.b.ld = ldb;
+    g.c = C; g.ldc = ldc;
+    g.alpha = alpha; g.epilogue = epi; g.bias = bias; g.aux = aux; g.aux_out = aux_out;
+    g.max_ctas = ctas;
+    CK(gemm(g, st));
+  }
+  // Per-(head, sample) attention GEMM over s x s / s x 64 blocks.
+  void mm_heads(int M, int N, int K, int64_t b, const bf16* A, int amaj, int64_t lda, int64_t a1,
+                int64_t a2, const bf16* B, int bmaj, int64_t ldb, int64_t b1, int64_t b2, void* C,
+                int64_t ldc, int64_t c1, int64_t c2, int epi, float alpha, int causal) {
+    GemmArgs g;
+    g.M = M; g.N = N; g.K = K; g.nb1 = c.n_head; g.nb2 = int(b);
+    g.a.ptr = A; g.a.major = amaj; g.a.ld = lda; g.a.bs1 = a1; g.a.bs2 = a2;
+    g.b.ptr = B; g.b.major = bmaj; g.b.ld = ldb; g.b.bs1 = b1; g.b.bs2 = b2;
+    g.c = C; g.ldc = ldc; g.cs1 = c1; g.cs2 = c2;
+    g.alpha = alpha; g.epilogue = epi; g.causal = causal;
+    g.max_ctas = ctas;
+    CK(gemm(g, st));
+  }
+
+  // ---------------------------------------------------------------- activation plan
+  // Carves one micro-step's activations from `ar` (or only counts bytes when ar == nullptr).
+  size_t plan_acts(int64_t b, Acts* a, Arena* ar) {
+    const int64_t s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
+    size_t bytes = 0;
+    auto take = [&](int64_t nbytes) -> void* {
+      bytes = ((bytes + 255) & ~size_t(255)) + size_t(nbytes);
+      if (!ar) return nullptr;
+      void* p = ar->take(size_t(nbytes));
+      if (!p) fail(ZP_OOM, "activation reservation exceeds the HBM cap");
+      return p;
+    };
+    auto B16 = [&](int64_t nel) { return static_cast<bf16*>(take(nel * 2)); };
+    auto F32 = [&](int64_t nel) { return static_cast<float*>(take(nel * 4)); };
+    Acts tmp;
+    Acts& A = a ? *a : tmp;
+    A.b = b;
+    A.l.resize(c.n_layer);
+    for (int i = 0; i < c.n_layer; ++i) {
+      LayerActs& L = A.l[i];
+      L.x_in = B16(T * h);
+      L.ln1 = B16(T * h);
+      L.qkv = B16(T * 3 * h);
+      L.P = B16(b * H * s * s);
+      L.attn = B16(T * h);
+      L.x_mid = B16(T * h);
+      L.ln2 = B16(T * h);
+      L.u = B16(T * f);
+      L.g = B16(T * f);
+      L.mu1 = F32(T);
+      L.rs1 = F32(T);
+      L.mu2 = F32(T);
+      L.rs2 = F32(T);
+    }
+    A.x_final = B16(T * h);
+    A.lnf = B16(T * h);
+    A.muf = F32(T);
+    A.rsf = F32(T);
+    A.logits = B16(T * vocab_pad);
+    A.row_loss = F32(T);
+    A.S = F32(b * H * s * s);
+    A.dS = B16(b * H * s * s);
+    A.dx = B16(T * h);
+    A.dx2 = B16(T * h);
+    A.dln = B16(T * h);
+    A.dO = B16(T * h);
+    A.dqkv = B16(T * 3 * h);
+    A.du = B16(T * f);
+    return bytes;
+  }
+
+  // ---------------------------------------------------------------- stage configuration
+  void configure(int new_stage) {
+    if (new_stage == stage) return;
+    if (new_stage < 0 || new_stage > 2) fail(ZP_EINVAL, "stage must be 0, 1 or 2 on this build");
+    arena.used = 0;
+    arena.high = 0;
+    stage = -1;
+    const int64_t T = lay.total, S = shard();
+    auto must = [&](void* p, const char* what) {
+      if (!p) fail(ZP_OOM, std::string("resident state does not fit the HBM cap: ") + what);
+      return p;
+    };
+    p16 = static_cast<bf16*>(must(arena.take_n<bf16>(T), "bf16 params"));
+    g16 = static_cast<bf16*>(must(arena.take_n<bf16>(T), "bf16 grads"));
+    const int64_t SL = new_stage == 0 ? T : S;
+    p32 = static_cast<float*>(must(arena.take_n<float>(SL), "master params"));
+    m32 = static_cast<float*>(must(arena.take_n<float>(SL), "adam m"));
+    v32 = static_cast<float*>(must(arena.take_n<float>(SL), "adam v"));
+    acc = r32 = nullptr;
+    r16 = nullptr;
+    if (new_stage <= 1) acc = static_cast<float*>(must(arena.take_n<float>(T), "grad accumulator"));
+    if (new_stage == 1) r32 = static_cast<float*>(must(arena.take_n<float>(S), "rs shard"));
+    if (new_stage == 2) {
+      acc = static_cast<float*>(must(arena.take_n<float>(S), "grad accumulator shard"));
+      r16 = static_cast<bf16*>(must(arena.take_n<bf16>(S), "rs shard"));
+    }
+    gkeep = keep_grads ? static_cast<float*>(must(arena.take_n<float>(SL), "kept grads")) : nullptr;
+    const int64_t h = c.d_model;
+    dwte32 = static_cast<float*>(must(arena.take_n<float>(int64_t(vocab_pad) * h), "dwte"));
+    dwpe32 = static_cast<float*>(must(arena.take_n<float>(int64_t(c.seq_len) * h), "dwpe"));
+    ln_part = static_cast<float*>(must(arena.take_n<float>(int64_t(2) * 2 * 148 * h), "ln partials"));
+    const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
+    col_work = static_cast<float*>(must(arena.take_n<float>(256 * maxN), "colsum work"));
+    loss_steps = static_cast<float*>(must(arena.take_n<float>(kMaxSteps), "loss"));
+    stage = new_stage;
+    resident_mark = arena.used;
+    CK(cudaMemsetAsync(g16, 0, size_t(T) * 2, st));
+    CK(cudaMemsetAsync(m32, 0, size_t(SL) * 4, st));
+    CK(cudaMemsetAsync(v32, 0, size_t(SL) * 4, st));
+    init_params();
+    adam_t = 0;
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // GPT-2 initialisation, a pure function of (seed, flat index): identical on every rank for
+  // every sharding. Residual projections use std 0.02/sqrt(2L).
+  void init_params() {
+    const int64_t lo = shard_begin(), hi = lo + state_len();
+    auto init = [&](const Tensor& t, int kind, float stdv) {
+      // full bf16 copy
+      if (kind == 0)
+        init_normal(nullptr, p16 + t.off, t.numel(), stdv, d.seed, uint64_t(t.off), ctas, st);
+      else
+        init_const(nullptr, p16 + t.off, t.numel(), kind == 1 ? 1.f : 0.f, ctas, st);
+      // master shard overlap
+      const int64_t a = std::max(lo, t.off), e = std::min(hi, t.off + t.numel());
+      if (a < e) {
+        if (kind == 0)
+          init_normal(p32 + (a - lo), nullptr, e - a, stdv, d.seed, uint64_t(a), ctas, st);
+        else
+          init_const(p32 + (a - lo), nullptr, e - a, kind == 1 ? 1.f : 0.f, ctas, st);
+      }
+    };
+    const float sp = 0.02f / std::sqrt(2.0f * c.n_layer);
+    // padding between tensors stays zero
+    CK(cudaMemsetAsync(p16, 0, size_t(lay.total) * 2, st));
+    CK(cudaMemsetAsync(p32, 0, size_t(state_len()) * 4, st));
+    Tensor wte_real = lay.wte;
+    wte_real.rows = c.vocab;  // padded vocabulary rows stay zero
+    init(wte_real, 0, 0.02f);
+    init(lay.wpe, 0, 0.01f);
+    for (const LayerP& l : lay.layers) {
+      init(l.ln1_g, 1, 0); init(l.ln1_b, 2, 0);
+      init(l.w_qkv, 0, 0.02f); init(l.b_qkv, 2, 0);
+      init(l.w_o, 0, sp); init(l.b_o, 2, 0);
+      init(l.ln2_g, 1, 0); init(l.ln2_b, 2, 0);
+      init(l.w_fc, 0, 0.02f); init(l.b_fc, 2, 0);
+      init(l.w_proj, 0, sp); init(l.b_proj, 2, 0);
+    }
+    init(lay.lnf_g, 1, 0);
+    init(lay.lnf_b, 2, 0);
+  }
+
+  // ---------------------------------------------------------------- forward / backward
+  void forward(Acts& A, const int32_t* tok, bool with_loss, float grad_scale) {
+    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
+    const float scale = 1.0f / std::sqrt(float(h / H));
+    bf16* W = p16;
+    embed_fwd(tok, int(s), W + lay.wte.off, W + lay.wpe.off, A.l[0].x_in, T, int(h), ctas, st);
+    for (int i = 0; i < c.n_layer; ++i) {
+      const LayerP& P = lay.layers[i];
+      LayerActs& L = A.l[i];
+      bf16* x_out = (i + 1 < c.n_layer) ? A.l[i + 1].x_in : A.x_final;
+      CK(layernorm_fwd(L.x_in, W + P.ln1_g.off, W + P.ln1_b.off, L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
+      mm(T, 3 * h, h, L.ln1, kKMajor, h, W + P.w_qkv.off, kKMajor, h, L.qkv, 3 * h, kEpiBiasBf16, 1.f,
+         W + P.b_qkv.off);
+      mm_heads(s, s, h / H, b, L.qkv, kKMajor, 3 * h, h / H, s * 3 * h, L.qkv + h, kKMajor, 3 * h, h / H,
+               s * 3 * h, A.S, s, s * s, H * s * s, kEpiStoreF32, scale, kCausalSkipUpper);
+      softmax_causal_fwd(A.S, L.P, b * H * s, int(s), ctas, st);
+      mm_heads(s, h / H, s, b, L.P, kKMajor, s, s * s, H * s * s, L.qkv + 2 * h, kMNMajor, 3 * h, h / H,
+               s * 3 * h, L.attn, h, h / H, s * h, kEpiStoreBf16, 1.f, kCausalKUpper);
+      mm(T, h, h, L.attn, kKMajor, h, W + P.w_o.off, kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f,
+         W + P.b_o.off, L.x_in);
+      CK(layernorm_fwd(L.x_mid, W + P.ln2_g.off, W + P.ln2_b.off, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
+      mm(T, f, h, L.ln2, kKMajor, h, W + P.w_fc.off, kKMajor, h, L.g, f, kEpiBiasGeluBf16, 1.f,
+         W + P.b_fc.off, nullptr, L.u);
+      mm(T, h, f, L.g, kKMajor, f, W + P.w_proj.off, kKMajor, f, x_out, h, kEpiBiasResidBf16, 1.f,
+         W + P.b_proj.off, L.x_mid);
+    }
+    CK(layernorm_fwd(A.x_final, W + lay.lnf_g.off, W + lay.lnf_b.off, A.lnf, A.muf, A.rsf, T, int(h), ctas,
+                     st));
+    mm(T, vocab_pad, h, A.lnf, kKMajor, h, W + lay.wte.off, kKMajor, h, A.logits, vocab_pad, kEpiStoreBf16);
+    if (with_loss)
+      cross_entropy_fwd_bwd(A.logits, tok, int(s), T, c.vocab, vocab_pad, grad_scale, A.row_loss, ctas, st);
+  }
+
+  void ln_grads(const Tensor& g, const Tensor& b, int nblk) {
+    const int h = c.d_model;
+    sum_partials(ln_part, nblk, h, g16 + g.off, st);
+    sum_partials(ln_part + int64_t(nblk) * h, nblk, h, g16 + b.off, st);
+  }
+
+  void backward(Acts& A, const int32_t* tok) {
+    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s, dh = h / H;
+    const float scale = 1.0f / std::sqrt(float(dh));
+    bf16* W = p16;
+    bf16* G = g16;
+    int nblk = 0;
+    // LM head (tied with wte): dlnf = dlogits * wte ; dwte = dlogits^T * lnf
+    mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, W + lay.wte.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
+    mm(vocab_pad, h, T, A.logits, kMNMajor, vocab_pad, A.lnf, kMNMajor, h, dwte32, h, kEpiStoreF32);
+    CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, W + lay.lnf_g.off, nullptr, A.dx, ln_part, &nblk, T,
+                     int(h), ctas, st));
+    ln_grads(lay.lnf_g, lay.lnf_b, nblk);
+    for (int i = c.n_layer - 1; i >= 0; --i) {
+      const LayerP& P = lay.layers[i];
+      LayerActs& L = A.l[i];
+      // MLP
+      colsum_bf16(A.dx, T, int(h), int(h), col_work, G + P.b_proj.off, ctas, st);
+      mm(h, f, T, A.dx, kMNMajor, h, L.g, kMNMajor, f, G + P.w_proj.off, f, kEpiStoreBf16);
+      mm(T, f, h, A.dx, kKMajor, h, W + P.w_proj.off, kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
+      colsum_bf16(A.du, T, int(f), int(f), col_work, G + P.b_fc.off, ctas, st);
+      mm(f, h, T, A.du, kMNMajor, f, L.ln2, kMNMajor, h, G + P.w_fc.off, h, kEpiStoreBf16);
+      mm(T, h, f, A.du, kKMajor, f, W + P.w_fc.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, W + P.ln2_g.off, A.dx, A.dx2, ln_part, &nblk, T, int(h),
+                       ctas, st));
+      ln_grads(P.ln2_g, P.ln2_b, nblk);
+      // attention output projection
+      colsum_bf16(A.dx2, T, int(h), int(h), col_work, G + P.b_o.off, ctas, st);
+      mm(h, h, T, A.dx2, kMNMajor, h, L.attn, kMNMajor, h, G + P.w_o.off, h, kEpiStoreBf16);
+      mm(T, h, h, A.dx2, kKMajor, h, W + P.w_o.off, kMNMajor, h, A.dO, h, kEpiStoreBf16);
+      // attention core, per (head, sample)
+      mm_heads(s, s, dh, b, A.dO, kKMajor, h, dh, s * h, L.qkv + 2 * h, kKMajor, 3 * h, dh, s * 3 * h, A.S, s,
+               s * s, H * s * s, kEpiStoreF32, 1.f, kCausalSkipUpper);
+      softmax_causal_bwd(L.P, A.S, A.dS, scale, b * H * s, int(s), ctas, st);
+      mm_heads(s, dh, s, b, L.P, kMNMajor, s, s * s, H * s * s, A.dO, kMNMajor, h, dh, s * h, A.dqkv + 2 * h,
+               3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
+      mm_heads(s, dh, s, b, A.dS, kKMajor, s, s * s, H * s * s, L.qkv + h, kMNMajor, 3 * h, dh, s * 3 * h,
+               A.dqkv, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKUpper);
+      mm_heads(s, dh, s, b, A.dS, kMNMajor, s, s * s, H * s * s, L.qkv, kMNMajor, 3 * h, dh, s * 3 * h,
+               A.dqkv + h, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
+      // QKV projection
+      colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, G + P.b_qkv.off, ctas, st);
+      mm(3 * h, h, T, A.dqkv, kMNMajor, 3 * h, L.ln1, kMNMajor, h, G + P.w_qkv.off, h, kEpiStoreBf16);
+      mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, W + P.w_qkv.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, W + P.ln1_g.off, A.dx2, A.dx, ln_part, &nblk, T, int(h),
+                       ctas, st));
+      ln_grads(P.ln1_g, P.ln1_b, nblk);
+    }
+    CK(cudaMemsetAsync(dwpe32, 0, size_t(c.seq_len) * h * 4, st));
+    embed_bwd(tok, int(s), A.dx, dwte32, dwpe32, T, int(h), ctas, st);
+    cast_f32_bf16(dwte32, G + lay.wte.off, int64_t(vocab_pad) * h, ctas, st);
+    cast_f32_bf16(dwpe32, G + lay.wpe.off, int64_t(c.seq_len) * h, ctas, st);
+  }
+
+  // ---------------------------------------------------------------- collectives
+  void reduce_scatter_bf16(const bf16* in, bf16* out) {
+    if (n == 1) return;
+    const int s0 = tm.mark(st);
+    NK(ncclReduceScatter(in, out, size_t(shard()), ncclBfloat16, ncclSum, comm, st));
+    tm.close(kComm, s0, st);
+  }
+  void reduce_scatter_f32(const float* in, float* out) {
+    const int s0 = tm.mark(st);
+    NK(ncclReduceScatter(in, out, size_t(shard()), ncclFloat, ncclSum, comm, st));
+    tm.close(kComm, s0, st);
+  }
+  void all_reduce_f32(float* buf, int64_t count) {
+    const int s0 = tm.mark(st);
+    NK(ncclAllReduce(buf, buf, size_t(count), ncclFloat, ncclSum, comm, st));
+    tm.close(kComm, s0, st);
+  }
+  void all_gather_params() {
+    if (n == 1) return;
+    const int s0 = tm.mark(st);
+    NK(ncclAllGather(p16 + shard() * rank, p16, size_t(shard()), ncclBfloat16, comm, st));
+    tm.close(kComm, s0, st);
+  }
+
+  AdamParams adam_params() {
+    ++adam_t;
+    AdamParams a;
+    a.lr = d.lr;
+    a.beta1 = d.beta1;
+    a.beta2 = d.beta2;
+    a.eps = d.eps;
+    a.weight_decay = d.weight_decay;
+    a.bc1 = 1.f - std::pow(d.beta1, float(adam_t));
+    a.bc2 = 1.f - std::pow(d.beta2, float(adam_t));
+    return a;
+  }
+
+  // ---------------------------------------------------------------- one iteration
+  // steps[k] = local batch of micro-step k (0 = sit out). Z2: every rank must pass the same
+  // number of steps (gas). Returns the micro-step count with batch > 0.
+  int64_t iterate(const std::vector<int64_t>& steps, int64_t global_batch, int* oom_step) {
+    const int64_t total = lay.total, sh = shard();
+    const float gscale = 1.0f / float(double(global_batch) * c.seq_len);
+    tm.reset();
+    const int t0 = tm.mark(st);
+    int64_t sample = 0, active = 0;
+    bool any_local = false;
+    CK(cudaMemsetAsync(loss_steps, 0, sizeof(float) * steps.size(), st));
+    for (size_t k = 0; k < steps.size(); ++k) {
+      int64_t b = steps[k];
+      if (b > 0 && sample + b > tokens_count) fail(ZP_EINVAL, "token pool has fewer samples than the plan needs");
+      Acts A;
+      if (b > 0) {
+        arena.used = resident_mark;
+        try {
+          plan_acts(b, &A, &arena);
+        } catch (const Fail& f) {
+          if (f.code != ZP_OOM || !oom_step) throw;
+          *oom_step = int(k);
+          b = 0;
+        }
+      }
+      const bool last = (k + 1 == steps.size());
+      if (b > 0) {
+        const int32_t* tok = tokens + sample * (c.seq_len + 1);
+        const int f0 = tm.mark(st);
+        forward(A, tok, true, gscale);
+        tm.close(kFwd, f0, st);
+        const int b0 = tm.mark(st);
+        backward(A, tok);
+        tm.close(kBwd, b0, st);
+        reduce_sum_f32(A.row_loss, b * c.seq_len, loss_steps + k, st);
+        sample += b;
+        ++active;
+      } else if (stage == 2) {
+        CK(cudaMemsetAsync(g16, 0, size_t(total) * 2, st));  // joins the collective with zeros
+      }
+      if (stage <= 1) {
+        if (b > 0) {
+          accumulate_bf16(acc, g16, total, !any_local, ctas, st);
+          any_local = true;
+        }
+      } else {  // Z2: reduce-scatter every micro-step
+        bf16* src = (n == 1) ? g16 : r16;
+        reduce_scatter_bf16(g16, r16);
+        if (!last) accumulate_bf16(acc, src, sh, k == 0, ctas, st);
+      }
+    }
+    if (stage <= 1 && !any_local) CK(cudaMemsetAsync(acc, 0, size_t(total) * 4, st));
+
+    // ---- synchronisation point + optimizer
+    const AdamParams ap = adam_params();
+    const int64_t L = state_len();
+    if (stage == 0) {
+      if (n > 1) all_reduce_f32(acc, total);
+      if (gkeep) CK(cudaMemcpyAsync(gkeep, acc, size_t(total) * 4, cudaMemcpyDeviceToDevice, st));
+      const int o0 = tm.mark(st);
+      adam_update(p32, m32, v32, p16, nullptr, nullptr, acc, total, ap, ctas, st);
+      tm.close(kOpt, o0, st);
+    } else if (stage == 1) {
+      const float* g = acc;
+      if (n > 1) {
+        reduce_scatter_f32(acc, r32);
+        g = r32;
+      }
+      if (gkeep) CK(cudaMemcpyAsync(gkeep, g, size_t(L) * 4, cudaMemcpyDeviceToDevice, st));
+      const int o0 = tm.mark(st);
+      adam_update(p32, m32, v32, p16 + shard_begin(), nullptr, nullptr, g, L, ap, ctas, st);
+      tm.close(kOpt, o0, st);
+      all_gather_params();
+    } else {
+      const bf16* g = (n == 1) ? g16 : r16;
+      const float* a = steps.size() > 1 ? acc : nullptr;
+      if (gkeep) {
+        accumulate_bf16(gkeep, g, L, true, ctas, st);
+        if (a) add_f32(gkeep, a, L, ctas, st);
+      }
+      const int o0 = tm.mark(st);
+      adam_update(p32, m32, v32, p16 + shard_begin(), a, g, nullptr, L, ap, ctas, st);
+      tm.close(kOpt, o0, st);
+      all_gather_params();
+    }
+    tm.close(kWall, t0, st);
+    last_gscale = gscale;
+    return active;
+  }
+
+  // ---------------------------------------------------------------- device seam
+  void ensure_tokens(int64_t count) {
+    if (count > tokens_cap) {
+      if (tokens) CK(cudaFree(tokens));
+      tokens = nullptr;
+      CK(cudaMalloc(&tokens, size_t(count) * (c.seq_len + 1) * sizeof(int32_t)));
+      tokens_cap = count;
+    }
+  }
+  void load_tokens(const int32_t* host, int64_t first, int64_t count, uint64_t it, bool from_host) {
+    ensure_tokens(count);
+    if (from_host) {
+      CK(cudaMemcpyAsync(tokens, host, size_t(count) * (c.seq_len + 1) * sizeof(int32_t),
+                         cudaMemcpyHostToDevice, st));
+    } else {
+      synth_tokens(tokens, first, count, c.seq_len + 1, c.vocab, d.seed, it, ctas, st);
+    }
+    tokens_count = count;
+  }
+
+  zp_probe memory_probe(int stg) {
+    configure(stg);
+    if (tokens_count < 1) load_tokens(nullptr, 0, 1, 0, false);
+    zp_probe p;
+    p.before_forward = double(resident_mark);
+    arena.high = arena.used = resident_mark;
+    Acts A;
+    plan_acts(1, &A, &arena);  // throws ZP_OOM when batch 1 does not fit
+    forward(A, tokens, false, 0.f);
+    CK(cudaStreamSynchronize(st));
+    p.after_forward = double(arena.high);
+    p.total = double(arena.cap);
+    arena.used = resident_mark;
+    return p;
+  }
+
+  int run_step(int64_t b, int stg, int64_t global_batch, zp_step_trace* out) {
+    configure(stg);
+    if (b > tokens_count) load_tokens(nullptr, 0, b, uint64_t(adam_t), false);
+    int oom = -1;
+    const int64_t active = iterate({b}, global_batch > 0 ? global_batch : std::max<int64_t>(b, 1), &oom);
+    zp_rank_timing t;
+    collect(&t, active, 1);
+    std::memset(out, 0, sizeof(*out));
+    out->forward_compute = t.forward;
+    out->backward_compute = t.backward;
+    out->optimizer_step = t.optimizer;
+    if (stg <= 1) {
+      out->allreduce = t.comm;
+    } else {
+      out->reduce_scatter = t.n_collectives > 0 ? t.coll_times[0] : 0.0;
+      out->allreduce = t.n_collectives > 1 ? t.coll_times[1] : 0.0;
+    }
+    return oom >= 0 ? ZP_OOM : ZP_OK;
+  }
+
+  void execute(const zp_allocation_plan* plan, int stg, zp_rank_timing* timing) {
+    if (plan->stage != stg) fail(ZP_EINVAL, "plan stage does not match the requested stage");
+    if (plan->n != n) fail(ZP_EINVAL, "plan does not match the world size");
+    configure(stg);
+    const zp_device_alloc& dv = plan->devices[rank];
+    std::vector<int64_t> steps;
+    if (stg >= 2) {
+      for (int64_t k = 0; k < plan->gas; ++k) steps.push_back(k + 1 < plan->gas ? dv.b : dv.lbs);
+    } else if (dv.gmbs > 0) {
+      const int64_t g = (dv.gmbs + dv.b - 1) / dv.b;
+      for (int64_t k = 0; k < g; ++k) steps.push_back(k + 1 < g ? dv.b : dv.lbs);
+    }
+    if (int64_t(steps.size()) > kMaxSteps) fail(ZP_EINVAL, "too many micro-steps");
+    if (dv.gmbs > tokens_count) fail(ZP_EINVAL, "token pool holds fewer samples than the plan assigns");
+    int oom = -1;
+    const int64_t active = iterate(steps, plan->gbs, &oom);
+    if (oom >= 0) {
+      CK(cudaStreamSynchronize(st));
+      fail(ZP_EINTERNAL, "plan exceeds device capacity: rank " + std::to_string(rank) +
+                             " OOMs at micro-step " + std::to_string(oom));
+    }
+    zp_rank_timing t;
+    collect(timing ? timing : &t, active, steps.size());
+  }
+
+  // ---------------------------------------------------------------- lockstep profiler (Alg. 1)
+  int* dscratch = nullptr;  // small device buffer for rank-agreement collectives
+  int64_t agree(int64_t v, ncclRedOp_t op) {
+    if (n == 1) return v;
+    if (!dscratch) CK(cudaMalloc(&dscratch, 4096));
+    long long hv = v;
+    CK(cudaMemcpyAsync(dscratch, &hv, 8, cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(dscratch, dscratch, 1, ncclInt64, op, comm, st));
+    CK(cudaMemcpyAsync(&hv, dscratch, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return hv;
+  }
+
+  // Every rank runs reference search_mbs's probe sequence (profiler.cpp:62-127) on its own
+  // device; ranks step together (one collective step per probe, finished ranks at batch 0), so
+  // ZeRO-2 reduce-scatters always have all ranks. Stage escalation needs every rank to fit batch 1
+  // (profiler.cpp:135-147). The per-rank results are all-gathered into one ProfileResult.
+  int profile(int stage_request, zp_profile* out) {
+    for (int s = stage_request < 0 ? 0 : stage_request; s <= 2; ++s) {
+      zp_probe pr{};
+      bool fits = true;
+      try {
+        pr = memory_probe(s);
+      } catch (const Fail& f) {
+        if (f.code != ZP_OOM) throw;
+        fits = false;
+      }
+      if (agree(fits ? 1 : 0, ncclMin) == 0) continue;
+      zeroplan::MemoryProbe mp{pr.before_forward, pr.after_forward, pr.total};
+      zeroplan::MbsSearch search(*zeroplan::mbs_from_probe(mp));
+      while (true) {
+        const bool active = !search.done();
+        if (agree(active ? 1 : 0, ncclMax) == 0) break;
+        const int64_t b = active ? search.next_batch() : 0;
+        if (b > tokens_count) load_tokens(nullptr, 0, b, uint64_t(adam_t), false);
+        const int64_t gb = agree(b, ncclSum);
+        zp_step_trace tr{};
+        const int rc = run_step(b, s, gb, &tr);
+        if (!active) continue;
+        if (rc == ZP_OOM) {
+          search.record(b, std::nullopt, 0.0);
+        } else {
+          zeroplan::StepTrace t;
+          t.forward_compute = tr.forward_compute;
+          t.backward_compute = tr.backward_compute;
+          t.reduce_scatter = tr.reduce_scatter;
+          t.allreduce = tr.allreduce;
+          t.optimizer_step = tr.optimizer_step;
+          search.record(b, zeroplan::time_consumed_during_step(t, zeroplan::stage_from_index(s)),
+                        t.optimizer_step);
+        }
+      }
+      const zeroplan::SearchResult r = search.result();
+      zp_device_profile mine{};
+      mine.device_id = rank;
+      mine.mbs = r.mbs;
+      mine.probes_used = r.probes_used;
+      mine.optimizer_time = r.optimizer_time;
+      mine.n_samples = int32_t(std::min<size_t>(r.samples.size(), ZP_MAX_SAMPLES));
+      for (int k = 0; k < mine.n_samples; ++k) mine.samples[k] = {r.samples[k].batch, r.samples[k].time};
+      std::memset(out, 0, sizeof(*out));
+      out->effective_stage = s;
+      out->n = n;
+      if (n == 1) {
+        out->devices[0] = mine;
+      } else {
+        void* dbuf = nullptr;
+        CK(cudaMalloc(&dbuf, sizeof(zp_device_profile) * (n + 1)));
+        CK(cudaMemcpyAsync(static_cast<char*>(dbuf) + sizeof(zp_device_profile) * n, &mine, sizeof(mine),
+                           cudaMemcpyHostToDevice, st));
+        NK(ncclAllGather(static_cast<char*>(dbuf) + sizeof(zp_device_profile) * n, dbuf, sizeof(mine),
+                         ncclUint8, comm, st));
+        CK(cudaMemcpyAsync(out->devices, dbuf, sizeof(zp_device_profile) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaFree(dbuf));
+      }
+      return ZP_OK;
+    }
+    fail(ZP_EINFEASIBLE, "model too large: a single batch does not fit on every rank");
+  }
+
+  void collect(zp_rank_timing* t, int64_t active, size_t nsteps) {
+    CK(cudaStreamSynchronize(st));
+    std::memset(t, 0, sizeof(*t));
+    for (const Span& sp : tm.spans) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, tm.ev[sp.start], tm.ev[sp.end]));
+      const double sec = double(ms) * 1e-3;
+      switch (sp.kind) {
+        case kFwd: t->forward += sec; break;
+        case kBwd: t->backward += sec; break;
+        case kComm:
+          t->comm += sec;
+          if (t->n_collectives < 512) t->coll_times[t->n_collectives++] = sec;
+          break;
+        case kOpt: t->optimizer += sec; break;
+        case kWall: t->wall = sec; break;
+      }
+    }
+    t->compute = t->forward + t->backward;
+    std::vector<float> ls(nsteps, 0.f);
+    if (nsteps) CK(cudaMemcpy(ls.data(), loss_steps, nsteps * 4, cudaMemcpyDeviceToHost));
+    double sum = 0;
+    for (size_t k = 0; k < nsteps; ++k) sum += double(ls[k]);
+    t->loss_sum = sum * double(last_gscale);
+    t->micro_steps = active;
+  }
+};
+
+// ====================================================================== C ABI
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ZP_EINTERNAL;
+  }
+}
+
+}  // namespace
+}  // namespace zp
+
+struct zp_runtime {
+  zp::Runtime rt;
+};
+
+using zp::g_err;
+using zp::guarded;
+
+extern "C" {
+
+const char* zp_runtime_last_error(void) { return g_err.c_str(); }
+
+int zp_nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) {
+    g_err = "ncclGetUniqueId failed";
+    return ZP_ENCCL;
+  }
+  std::memcpy(out, id.internal, 128);
+  return ZP_OK;
+}
+
+int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto* h = new zp_runtime();
+    zp::Runtime& R = h->rt;
+    try {
+      R.d = *desc;
+      R.c = desc->model;
+      R.n = desc->world_size < 1 ? 1 : desc->world_size;
+      R.rank = desc->rank;
+      const zp_gpt_config& c = R.c;
+      if (c.d_model % 256 || c.d_model / c.n_head != 64 || c.d_model % c.n_head || c.seq_len % 128 ||
+          c.d_ff % 64 || c.vocab < 2 || c.n_layer < 1)
+        zp::fail(ZP_EINVAL, "unsupported model shape (need d_model % 256 == 0, head_dim 64, seq % 128 == 0)");
+      CK(cudaSetDevice(desc->device));
+      int sms = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc->device));
+      R.ctas = (desc->sm_budget > 0 && desc->sm_budget < sms) ? desc->sm_budget : sms;
+      CK(cudaStreamCreateWithFlags(&R.st, cudaStreamNonBlocking));
+      R.vocab_pad = int(zp::round_up(c.vocab, 128));
+      R.lay = zp::make_layout(c, R.vocab_pad, R.n);
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      const size_t margin = size_t(4) << 30;
+      size_t cap = desc->hbm_cap_bytes > 0 ? size_t(desc->hbm_cap_bytes) : (fr > margin ? fr - margin : fr / 2);
+      if (cap + (size_t(1) << 30) > fr) zp::fail(ZP_EINVAL, "hbm_cap_bytes exceeds free device memory");
+      CK(cudaMalloc(&R.arena.base, cap));
+      R.arena.cap = cap;
+      if (R.n > 1) {
+        ncclUniqueId id;
+        std::memcpy(id.internal, desc->nccl_id, 128);
+        NK(ncclCommInitRank(&R.comm, R.n, id, R.rank));
+      }
+      R.tm.init(8192);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_destroy(zp_runtime* h) {
+  if (!h) return ZP_OK;
+  zp::Runtime& R = h->rt;
+  cudaStreamSynchronize(R.st);
+  if (R.comm) ncclCommDestroy(R.comm);
+  R.tm.destroy();
+  if (R.tokens) cudaFree(R.tokens);
+  if (R.dscratch) cudaFree(R.dscratch);
+  for (auto& e : R.marks)
+    if (e) cudaEventDestroy(e);
+  if (R.arena.base) cudaFree(R.arena.base);
+  if (R.st) cudaStreamDestroy(R.st);
+  delete h;
+  return ZP_OK;
+}
+
+int zp_runtime_param_count(zp_runtime* h, int64_t* padded, int64_t* logical) {
+  *padded = h->rt.lay.total;
+  *logical = h->rt.lay.logical;
+  return ZP_OK;
+}
+
+int zp_runtime_activation_bytes(zp_runtime* h, int64_t batch, int64_t* out) {
+  return guarded([&] {
+    *out = int64_t(h->rt.plan_acts(batch, nullptr, nullptr));
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_resident_bytes(zp_runtime* h, int32_t stage, int64_t* out) {
+  return guarded([&] {
+    h->rt.configure(stage);
+    *out = int64_t(h->rt.resident_mark);
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_memory_probe(zp_runtime* h, int32_t stage, zp_probe* out) {
+  return guarded([&] {
+    *out = h->rt.memory_probe(stage);
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_load_tokens(zp_runtime* h, const int32_t* host, int64_t first, int64_t count,
+                           uint64_t iteration, int32_t from_host) {
+  return guarded([&] {
+    h->rt.load_tokens(host, first, count, iteration, from_host != 0);
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_run_step(zp_runtime* h, int64_t batch, int32_t stage, int64_t global_batch,
+                        zp_step_trace* out) {
+  return guarded([&] {
+    if (batch < 0) zp::fail(ZP_EINVAL, "batch_size must be >= 0");
+    return h->rt.run_step(batch, stage, global_batch, out);
+  });
+}
+
+int zp_runtime_execute_iteration(zp_runtime* h, const zp_allocation_plan* plan, int32_t stage,
+                                 zp_rank_timing* timing) {
+  return guarded([&] {
+    h->rt.execute(plan, stage, timing);
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_get_state(zp_runtime* h, int32_t kind, float* out, int64_t* begin, int64_t* end) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
+    const float* src = kind == 0 ? R.p32 : kind == 1 ? R.m32 : kind == 2 ? R.v32 : R.gkeep;
+    if (!src) zp::fail(ZP_EINVAL, "state not available (enable zp_runtime_keep_grads)");
+    CK(cudaStreamSynchronize(R.st));
+    CK(cudaMemcpy(out, src, size_t(R.state_len()) * 4, cudaMemcpyDeviceToHost));
+    *begin = R.shard_begin();
+    *end = R.shard_begin() + R.state_len();
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_get_params_bf16(zp_runtime* h, uint16_t* out) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
+    CK(cudaStreamSynchronize(R.st));
+    CK(cudaMemcpy(out, R.p16, size_t(R.lay.total) * 2, cudaMemcpyDeviceToHost));
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_set_params(zp_runtime* h, const float* full) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
+    float* tmp = nullptr;
+    CK(cudaMalloc(&tmp, size_t(R.lay.total) * 4));
+    CK(cudaMemcpyAsync(tmp, full, size_t(R.lay.total) * 4, cudaMemcpyHostToDevice, R.st));
+    zp::cast_f32_bf16(tmp, R.p16, R.lay.total, R.ctas, R.st);
+    CK(cudaMemcpyAsync(R.p32, tmp + R.shard_begin(), size_t(R.state_len()) * 4, cudaMemcpyDeviceToDevice,
+                       R.st));
+    CK(cudaStreamSynchronize(R.st));
+    CK(cudaFree(tmp));
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_keep_grads(zp_runtime* h, int32_t on) {
+  h->rt.keep_grads = on != 0;
+  h->rt.stage = -1;  // re-carve the arena on the next call
+  return ZP_OK;
+}
+
+int zp_runtime_tensor_info(zp_runtime* h, const char* name, int64_t* offset, int64_t* rows, int64_t* cols) {
+  auto it = h->rt.lay.by_name.find(name);
+  if (it == h->rt.lay.by_name.end()) {
+    g_err = std::string("unknown tensor ") + name;
+    return ZP_EINVAL;
+  }
+  *offset = it->second.off;
+  *rows = it->second.rows;
+  *cols = it->second.cols;
+  return ZP_OK;
+}
+
+int zp_runtime_profile(zp_runtime* h, int32_t stage_request, zp_profile* out) {
+  return guarded([&] { return h->rt.profile(stage_request, out); });
+}
+
+int zp_runtime_mark(zp_runtime* h, int32_t slot) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (slot < 0 || slot >= 8) zp::fail(ZP_EINVAL, "slot must be in [0, 8)");
+    if (!R.marks[slot]) CK(cudaEventCreate(&R.marks[slot]));
+    CK(cudaEventRecord(R.marks[slot], R.st));
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_elapsed(zp_runtime* h, int32_t a, int32_t b, double* seconds) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    CK(cudaEventSynchronize(R.marks[b]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, R.marks[a], R.marks[b]));
+    *seconds = double(ms) * 1e-3;
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_sync(zp_runtime* h) {
+  return guarded([&] {
+    CK(cudaStreamSynchronize(h->rt.st));
+    return ZP_OK;
+  });
+}
+
+}  // extern "C"
