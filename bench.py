@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Heterogeneous-ZeRO (Poplar) training step on B200s — benchmark contract.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c2]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
+
+Workload (BASELINE.json configs[1], "C2"): GPT-2 small (124M params, s=1024, V=50257),
+ZeRO-2, ranks with unequal SM budgets alternating 132 / 66 SMs (rank 0 = 132), global batch
+512*N samples (weak scaling). Per run: Poplar Alg. 1 profiling on the devices (lockstep probes),
+Alg. 2 plan from the bit-exact zeroplan planner, W warm-up iterations, then K timed iterations
+bracketed by barrier + device sync, timed with CUDA events on the runtime stream, max over ranks.
+`value` = K * gbs / T (samples/s, whole job). Inputs (tokens) are resident in HBM for `value`;
+`e2e` re-times the same iterations through the C ABI with the tokens copied from pinned host
+memory and the loss read back every step.
+
+--impl reference times the reference's CPU implementation of the path on the host cores:
+the reference has no tensor step (its device step is a closed-form latent model), so the CPU
+path in the metric's unit is the float64 oracle port of the step (oracle/step.py), all threads;
+its planner (compiled from the reference sources, oracle/_ref) is timed beside it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec (8×B200, emulated hetero) at 1/2/4/8 GPUs; sync idle %"
+UNIT = "samples/s"
+
+CONFIGS = {
+    # name: model, ZeRO stage, SM tiers (cycled over ranks), HBM caps (GiB, cycled; 0 = full),
+    # global batch per GPU (samples)
+    "c1": dict(model="gpt-tiny", stage=1, tiers=[148, 74], caps=[0], gbs_per_gpu=32,
+               label="C1: GPT-tiny L4 h256 V8192 s256, ZeRO-1, SM 148 vs 74"),
+    "c2": dict(model="gpt2-small", stage=2, tiers=[132, 66], caps=[0], gbs_per_gpu=512,
+               label="C2: GPT-2 small (124M) s1024, ZeRO-2, SM budgets 132 vs 66"),
+    "c3": dict(model="gpt2-medium", stage=2, tiers=[148, 74], caps=[0, 80], gbs_per_gpu=256,
+               label="C3-shape: GPT-2 medium (355M) s1024, ZeRO-2, 2 SM tiers x HBM caps 180/80 GB"),
+}
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+class ClockSampler:
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.out = os.path.join(ROOT, "gpurun_out", f".clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.out), exist_ok=True)
+        try:
+            self.f = open(self.out, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            for line in open(self.out):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx = max(mx, float(parts[1]))
+                except ValueError:
+                    continue
+                for nme, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nme)
+            os.remove(self.out)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_step_sample(model_name: str, seconds_cap: float = 60.0):
+    """Times the float64 oracle step (forward + backward + AdamW) on one sample of the workload
+    on all host cores. Returns (samples/s, cores, seconds)."""
+    import numpy as np
+    from oracle import step as so
+    from paper_2408_12596_b200.runtime import MODELS
+    m = MODELS[model_name]
+    rng = np.random.default_rng(0)
+    h, f = m.d_model, m.d_ff
+    P = {"wte": rng.normal(0, 0.02, (m.vocab, h)), "wpe": rng.normal(0, 0.01, (m.seq_len, h)),
+         "lnf_g": np.ones((1, h)), "lnf_b": np.zeros((1, h))}
+    for i in range(m.n_layer):
+        P.update({f"h{i}.ln1_g": np.ones((1, h)), f"h{i}.ln1_b": np.zeros((1, h)),
+                  f"h{i}.w_qkv": rng.normal(0, 0.02, (3 * h, h)), f"h{i}.b_qkv": np.zeros((1, 3 * h)),
+                  f"h{i}.w_o": rng.normal(0, 0.02, (h, h)), f"h{i}.b_o": np.zeros((1, h)),
+                  f"h{i}.ln2_g": np.ones((1, h)), f"h{i}.ln2_b": np.zeros((1, h)),
+                  f"h{i}.w_fc": rng.normal(0, 0.02, (f, h)), f"h{i}.b_fc": np.zeros((1, f)),
+                  f"h{i}.w_proj": rng.normal(0, 0.02, (h, f)), f"h{i}.b_proj": np.zeros((1, h))})
+    tok = rng.integers(0, m.vocab, (1, m.seq_len + 1))
+    t0 = time.perf_counter()
+    _, G = so.gpt_loss_and_grads(P, tok, m.n_layer, m.n_head, m.vocab, 1)
+    for k in P:
+        so.adamw(P[k], 0.0, 0.0, G[k], 1, 1e-4, 0.9, 0.95, 1e-8, 0.0)
+    dt = time.perf_counter() - t0
+    return 1.0 / dt, os.cpu_count() or 1, dt
+
+
+def reference_planner_ms():
+    """The reference's own profile + plan (compiled from /root/reference sources, oracle/_ref) on
+    a 2-device cluster fitted to C2's shape; single-threaded as written. None if not built."""
+    try:
+        import oracle
+        from paper_2408_12596_b200.host import ClusterSpec, Device, ModelSpec
+        if not oracle.available():
+            return None
+        ref = oracle.reference()
+        cl = ClusterSpec([Device(180e9, 0.8e9, 0.01, 0.0015), Device(180e9, 0.8e9, 0.01, 0.003)],
+                         [770e9] * 2, 25e-6)
+        m = ModelSpec(124.4e6, 768, 12)
+        t0 = time.perf_counter()
+        n = 0
+        while time.perf_counter() - t0 < 0.5:
+            p = ref.profile_cluster(cl, m, 2)
+            ref.plan(1024, p, 2, m, cl)
+            n += 1
+        return 1e3 * (time.perf_counter() - t0) / n
+    except Exception:
+        return None
+
+
+def run_reference(args, cfg):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    samples, secs = 0, 0.0
+    cores = os.cpu_count() or 1
+    deadline = time.perf_counter() + 150.0
+    for k in range(max(1, args.steps)):
+        sps, cores, dt = cpu_step_sample(cfg["model"])
+        samples += 1
+        secs += dt
+        if time.perf_counter() > deadline:
+            break
+    value = samples / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": samples, "warmup": 0, "ms_per_step": 1e3 * secs / samples, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["label"], "model": cfg["model"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{samples} step(s) of 1 sample x {cfg['model']} fwd+bwd+AdamW in "
+                                       "float64 numpy (oracle/step.py); the reference has no tensor step",
+                             "reference_planner_ms": reference_planner_ms()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def rank_micro_steps(plan, r, stage):
+    d = plan["devices"][r]
+    if stage >= 2:
+        return plan["gas"]
+    return 0 if d["gmbs"] == 0 else -(-d["gmbs"] // d["b"])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--gbs", type=int, default=0, help="override global batch (samples)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # plumbing only: rendezvous, barrier, max-over-ranks
+        dist.init_process_group("gloo")
+    from paper_2408_12596_b200 import _lib
+    from paper_2408_12596_b200.runtime import Runtime, MODELS, nccl_unique_id
+    from paper_2408_12596_b200 import poplar
+
+    def allgather(obj):
+        if dist is None:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    nid = nccl_unique_id() if rank == 0 and world > 1 else None
+    nid = allgather(nid)[0] if world > 1 else None
+    model = MODELS[cfg["model"]]
+    tier = cfg["tiers"][rank % len(cfg["tiers"])]
+    cap_gib = cfg["caps"][rank % len(cfg["caps"])]
+    stage = cfg["stage"]
+    gbs = args.gbs or cfg["gbs_per_gpu"] * world
+    rt = Runtime(model, rank=rank, world_size=world, device=local, nccl_id=nid, sm_budget=tier,
+                 hbm_cap_bytes=int(cap_gib * (1 << 30)), seed=0, lr=1e-4)
+
+    # Poplar: Alg. 1 on the devices, Alg. 2 on the host (bit-exact planner)
+    t0 = time.perf_counter()
+    profile = rt.profile(stage)
+    t_profile = time.perf_counter() - t0
+    stage = profile["effective_stage"]
+    plan = poplar.poplar_plan(rt, profile, gbs, stage, world)
+    uniform = poplar.poplar_plan(rt, profile, gbs, stage, world, uniform=True)
+    first, count = poplar.rank_slice(plan, rank)
+    rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
+
+    def timed(k, plan_d, host_tokens=None):
+        from paper_2408_12596_b200.host import plan_from_py
+        from paper_2408_12596_b200.runtime import RankTiming
+        cplan = plan_from_py(plan_d)
+        tm = RankTiming()
+        last = []
+        barrier()
+        rt.sync()
+        rt.mark(0)
+        for _ in range(k):
+            if host_tokens is not None:
+                rt.load_tokens_ptr(host_tokens[0], host_tokens[1])
+            rt.execute_iteration_c(cplan, stage, tm)
+        rt.mark(1)
+        local_t = rt.elapsed(0, 1)
+        rt.sync()
+        barrier()
+        last.append(tm.to_py())
+        return max(allgather(local_t)), last[-1]
+
+    for _ in range(args.warmup):
+        rt.execute_iteration(plan, stage)
+    launches0 = _lib.lib.zp_launch_count()
+    with ClockSampler(local) as clk:
+        T, last_timing = timed(args.steps, plan)
+    launches = _lib.lib.zp_launch_count() - launches0
+    clocks = clk.summary()
+    value = args.steps * gbs / T
+    report = poplar.iteration_report(allgather(last_timing), gbs)
+
+    # e2e: tokens from pinned host memory every step, loss read back every step
+    e2e = None
+    if not args.no_e2e:
+        import numpy as np
+        import torch
+        s1 = model.seq_len + 1
+        host = torch.randint(0, model.vocab, (max(count, 1), s1), dtype=torch.int32).pin_memory()
+        T_e2e, _ = timed(args.steps, plan, host_tokens=(host.data_ptr(), max(count, 1)))
+        rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
+        h2d = sum(allgather(count * s1 * 4))
+        d2h = 4 * sum(rank_micro_steps(plan, r, stage) for r in range(world))  # per-step loss read-back
+        e2e = {"value": args.steps * gbs / T_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    # Heterogeneity-blind baseline (equal split) on the same devices
+    rt.load_tokens(first_sample=poplar.rank_slice(uniform, rank)[0],
+                   count=max(poplar.rank_slice(uniform, rank)[1], 1), iteration=0)
+    ku = max(2, args.steps // 3)
+    rt.execute_iteration(uniform, stage)
+    T_u, _ = timed(ku, uniform)
+    uniform_value = ku * gbs / T_u
+
+    # Roofline: per-launch event timing of the dense GEMMs over one more iteration
+    rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
+    rt.gemm_timing(1)
+    rt.execute_iteration(plan, stage)
+    gflops, gsec, glaunch = rt.gemm_timing(2)
+    rt.gemm_timing(0)
+    g_all = allgather((gflops, gsec, glaunch, tier))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sps, cores, dt = cpu_step_sample(cfg["model"])
+        cpu = {"value": sps, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"1 sample x {cfg['model']} fwd+bwd+AdamW, float64 numpy oracle port "
+                         f"(oracle/step.py), {dt:.1f} s; the reference has no tensor step",
+               "reference_planner_ms": reference_planner_ms()}
+
+    if rank == 0:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        fl, sec, nl, tr = g_all[0]
+        achieved = fl / sec / 1e12 if sec > 0 else 0.0
+        peak = peaks["bf16_tflops"] * tr / 148.0
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["label"], "model": cfg["model"], "params": rt.param_count,
+                       "seq_len": model.seq_len, "global_batch": gbs, "stage": stage,
+                       "sm_budgets": [cfg["tiers"][r % len(cfg["tiers"])] for r in range(world)],
+                       "plan": {"b": [d["b"] for d in plan["devices"]], "lbs": [d["lbs"] for d in plan["devices"]],
+                                "gmbs": [d["gmbs"] for d in plan["devices"]], "gas": plan["gas"]},
+                       "mbs": [d["mbs"] for d in profile["devices"]],
+                       "profile_seconds": t_profile, "parallelism": f"zero{stage}-dp{world}",
+                       "l2": "inputs larger than L2 (per-step activations are tens of GB)"},
+            "sync_idle_pct": report["sync_idle_pct"],
+            "uniform_split": {"value": uniform_value, "poplar_speedup": value / uniform_value,
+                              "plan_b": [d["b"] for d in uniform["devices"]], "gas": uniform["gas"]},
+            "roofline": {"kernel": "tcgen05 GEMM (dense linear layers, rank 0)", "bound": "tensor",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "peak_note": f"MEASURED_PEAKS bf16 {peaks['bf16_tflops']} x {tr}/148 SM budget",
+                         "launches": nl},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    rt.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

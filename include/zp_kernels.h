@@ -22,7 +22,8 @@ extern "C" {
 /* GEMM: C[z][m,n] = epilogue(alpha * sum_k A[z][m,k] * B[z][n,k]), bf16 in, fp32 accumulate.
  * major: 0 = K-major (elem (r,k) at ptr[r*ld+k]), 1 = MN-major (elem (r,k) at ptr[k*ld+r]).
  * epilogue: 0 store bf16, 1 store f32, 2 accumulate f32, 3 +bias bf16, 4 +bias+residual bf16,
- *           5 +bias then GELU (pre-activation to aux_out) bf16, 6 times GELU'(aux) bf16.
+ *           5 +bias then GELU (pre-activation to aux_out) bf16, 6 times GELU'(aux) bf16,
+ *           7 fp32 atomic add (split-K partial sums).
  * causal:   0 none, 1 skip tiles above the diagonal, 2 k <= tile last row, 3 k >= tile first row.
  */
 typedef struct zp_gemm_desc {
@@ -37,9 +38,13 @@ typedef struct zp_gemm_desc {
   const void* aux;
   void* aux_out;
   int32_t max_ctas;
+  int32_t split_k;  /* > 1 splits the K range across CTAs; needs epilogue 7 (fp32 atomic add) */
 } zp_gemm_desc;
 
 int zp_gemm(const zp_gemm_desc* d, void* stream);
+
+/* Number of kernels launched by this library since load (all entry points). */
+int64_t zp_launch_count(void);
 
 #ifdef __cplusplus
 }

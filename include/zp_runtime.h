@@ -115,6 +115,11 @@ int zp_runtime_profile(zp_runtime* rt, int32_t stage_request, zp_profile* out);
  * b and returns the seconds between the two events. */
 int zp_runtime_mark(zp_runtime* rt, int32_t slot);
 int zp_runtime_elapsed(zp_runtime* rt, int32_t a, int32_t b, double* seconds);
+/* Per-launch CUDA-event timing of the dense (linear-layer) GEMMs. mode 1: enable + reset,
+ * 0: disable, 2: synchronise and return the summed algorithmic FLOPs, event seconds and launch
+ * count since the last reset. */
+int zp_runtime_gemm_stats(zp_runtime* rt, int32_t mode, double* flops, double* seconds,
+                          int64_t* launches);
 int zp_runtime_sync(zp_runtime* rt);
 
 #ifdef __cplusplus

@@ -41,8 +41,12 @@ class GemmDesc(C.Structure):
         ("aux", C.c_void_p),
         ("aux_out", C.c_void_p),
         ("max_ctas", C.c_int32),
+        ("split_k", C.c_int32),
     ]
 
 
 lib.zp_gemm.argtypes = [C.POINTER(GemmDesc), C.c_void_p]
 lib.zp_gemm.restype = C.c_int
+
+lib.zp_launch_count.argtypes = []
+lib.zp_launch_count.restype = C.c_int64

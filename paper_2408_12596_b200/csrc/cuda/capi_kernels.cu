@@ -1,6 +1,7 @@
 // extern "C" wrappers of the individual kernels (include/zp_kernels.h).
 #include "../../../include/zp_kernels.h"
 #include "gemm.h"
+#include "kernels.h"
 
 extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
   if (!d) return 1;
@@ -16,6 +17,9 @@ extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
   a.aux = d->aux;
   a.aux_out = d->aux_out;
   a.max_ctas = d->max_ctas;
+  a.split_k = d->split_k;
   const cudaError_t e = zp::gemm(a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : 5;
 }
+
+extern "C" int64_t zp_launch_count(void) { return zp::launch_count(); }

@@ -12,6 +12,7 @@
 #include <mutex>
 
 #include "gemm.h"
+#include "kernels.h"
 #include "ptx.cuh"
 
 namespace zp {
@@ -37,10 +38,12 @@ struct TileInfo {
 };
 
 struct Sched {
-  int m_tiles, n_tiles, nb1, total;
+  int m_tiles, n_tiles, nb1, total, split_k;
   int M, N, K, BN, causal;
-  __device__ TileInfo tile(int t) const {
+  __device__ TileInfo tile(int unit) const {
     TileInfo ti;
+    const int split = unit % split_k;
+    const int t = unit / split_k;
     const int per_batch = m_tiles * n_tiles;
     const int z = t / per_batch;
     const int r = t - z * per_batch;
@@ -59,6 +62,12 @@ struct Sched {
       kb1 = (kend + kBK - 1) / kBK;
     } else if (causal == kCausalKLower) {
       kb0 = ti.m0 / kBK;
+    }
+    if (split_k > 1) {
+      const int nk = kb1 - kb0;
+      const int per = (nk + split_k - 1) / split_k;
+      kb0 = kb0 + split * per;
+      kb1 = min(kb1, kb0 + per);
     }
     ti.kb0 = kb0;
     ti.kb1 = kb1;
@@ -97,6 +106,18 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]);
   const bool full = (n + 32 <= N);
   const int e = ep.epilogue;
+  if (e == kEpiAtomicF32) {
+    float* c = static_cast<float*>(ep.c) + off;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        atomicAdd(reinterpret_cast<float4*>(c + i),
+                  make_float4(ep.alpha * v[i], ep.alpha * v[i + 1], ep.alpha * v[i + 2], ep.alpha * v[i + 3]));
+    } else {
+      for (int i = 0; i < 32 && n + i < N; ++i) atomicAdd(c + i, ep.alpha * v[i]);
+    }
+    return;
+  }
   if (e == kEpiStoreF32 || e == kEpiAccumF32) {
     float* c = static_cast<float*>(ep.c) + off;
     if (full) {
@@ -425,7 +446,9 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   s.m_tiles = (a.M + kBM - 1) / kBM;
   s.n_tiles = (a.N + BN - 1) / BN;
   s.nb1 = a.nb1;
-  s.total = s.m_tiles * s.n_tiles * a.nb1 * a.nb2;
+  s.split_k = a.split_k > 1 ? a.split_k : 1;
+  if (s.split_k > 1 && a.epilogue != kEpiAtomicF32) return cudaErrorInvalidValue;
+  s.total = s.m_tiles * s.n_tiles * a.nb1 * a.nb2 * s.split_k;
   s.M = a.M;
   s.N = a.N;
   s.K = a.K;
@@ -446,6 +469,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   if (s.total < grid) grid = s.total;
   if (grid < 1) return cudaSuccess;
   kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, s, ep);
+  note_launch();
   return cudaGetLastError();
 }
 

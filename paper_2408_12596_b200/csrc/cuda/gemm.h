@@ -25,6 +25,7 @@ enum GemmEpilogue : int {
   kEpiBiasResidBf16 = 4,  // C(bf16) = acc + bias[n] + R[m, n]   (R may alias C)
   kEpiBiasGeluBf16 = 5,   // U(bf16) = acc + bias[n];  C(bf16) = gelu(U)
   kEpiGeluBwdBf16 = 6,    // C(bf16) = acc * gelu'(U[m, n])
+  kEpiAtomicF32 = 7,      // C(f32) += alpha*acc with fp32 vector atomics (split-K partials)
 };
 
 enum GemmCausal : int {
@@ -54,6 +55,7 @@ struct GemmArgs {
   const void* aux = nullptr;   // bf16, same layout as C (residual R or pre-activation U)
   void* aux_out = nullptr;     // bf16, same layout as C (U written by kEpiBiasGeluBf16)
   int max_ctas = 0;            // SM budget cap (0 = all SMs)
+  int split_k = 1;             // >1: K range split across CTAs; requires kEpiAtomicF32
 };
 
 // Returns cudaSuccess or the launch/encode error.

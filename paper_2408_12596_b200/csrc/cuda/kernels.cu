@@ -1,6 +1,7 @@
 // HBM-bound kernels: embedding, LayerNorm, causal softmax, cross-entropy, reductions,
 // and the ZeRO accumulate / AdamW update. 16-byte vector accesses, warp-shuffle
 // reductions, grid-stride loops capped at the rank's CTA budget.
+#include <atomic>
 #include <cmath>
 
 #include "kernels.h"
@@ -493,28 +494,33 @@ __global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, floa
 
 // ------------------------------------------------------------------ launchers
 
+std::atomic<int64_t> g_launches{0};
+void note_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+
 void init_normal(float* p32, bf16* p16, int64_t n, float stdv, uint64_t seed, uint64_t offset,
                  int ctas, cudaStream_t s) {
-  init_normal_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, stdv, seed, offset);
+  init_normal_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, stdv, seed, offset); note_launch();
 }
 void init_const(float* p32, bf16* p16, int64_t n, float value, int ctas, cudaStream_t s) {
-  init_const_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, value);
+  init_const_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(p32, p16, n, value); note_launch();
 }
 void synth_tokens(int32_t* tokens, int64_t first, int64_t count, int sp1, int vocab, uint64_t seed,
                   uint64_t it, int ctas, cudaStream_t s) {
   if (count <= 0) return;
   synth_tokens_k<<<grid_for(count * sp1, kThreads, ctas), kThreads, 0, s>>>(tokens, first, count,
-                                                                          sp1, vocab, seed, it);
+                                                                          sp1, vocab, seed, it); note_launch();
 }
 void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe, bf16* x,
                int64_t rows, int h, int ctas, cudaStream_t s) {
   embed_fwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, wte, wpe, x,
-                                                                          rows, h);
+                                                                          rows, h); note_launch();
 }
 void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
                int64_t rows, int h, int ctas, cudaStream_t s) {
   embed_bwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, dx, dwte32,
-                                                                          dwpe32, rows, h);
+                                                                          dwpe32, rows, h); note_launch();
 }
 
 #define ZP_LN_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(8) X(12) X(16)
@@ -526,7 +532,7 @@ cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, 
 #define X(NC)                                                                     \
   case NC:                                                                        \
     if (h % 256) return cudaErrorInvalidValue;                                    \
-    ln_fwd_k<NC><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows);         \
+    ln_fwd_k<NC><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows); note_launch();         \
     return cudaGetLastError();
     ZP_LN_CASES(X)
 #undef X
@@ -544,7 +550,7 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
 #define X(NC)                                                                              \
   case NC:                                                                                 \
     if (h % 256) return cudaErrorInvalidValue;                                             \
-    ln_bwd_k<NC><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows);    \
+    ln_bwd_k<NC><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); note_launch();    \
     return cudaGetLastError();
     ZP_LN_CASES(X)
 #undef X
@@ -554,17 +560,17 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
 }
 
 void softmax_causal_fwd(const float* S, bf16* P, int64_t rows, int seq, int ctas, cudaStream_t s) {
-  softmax_fwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(S, P, rows, seq);
+  softmax_fwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(S, P, rows, seq); note_launch();
 }
 void softmax_causal_bwd(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows, int seq,
                         int ctas, cudaStream_t s) {
   softmax_bwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(P, dP, dS, scale, rows,
-                                                                            seq);
+                                                                            seq); note_launch();
 }
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
                            int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s) {
   ce_k<<<grid_for(rows, 1, ctas, 8), kThreads, 0, s>>>(logits, tokens, seq, rows, vocab, ldv,
-                                                      grad_scale, row_loss);
+                                                      grad_scale, row_loss); note_launch();
 }
 
 void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* out, int ctas,
@@ -575,28 +581,28 @@ void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* 
   if (chunks > 256) chunks = 256;
   const int64_t chunk = (rows + chunks - 1) / chunks;
   chunks = int((rows + chunk - 1) / chunk);
-  colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work);
-  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, out);
+  colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work); note_launch();
+  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, out); note_launch();
 }
 void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s) {
-  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(part, nparts, N, out);
+  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(part, nparts, N, out); note_launch();
 }
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
-  cast_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(in, out, n);
+  cast_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();
 }
 void reduce_sum_f32(const float* x, int64_t n, float* out, cudaStream_t s) {
-  reduce_sum_k<<<1, kThreads, 0, s>>>(x, n, out);
+  reduce_sum_k<<<1, kThreads, 0, s>>>(x, n, out); note_launch();
 }
 void add_f32(float* dst, const float* src, int64_t n, int ctas, cudaStream_t s) {
-  add_f32_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(dst, src, n);
+  add_f32_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(dst, src, n); note_launch();
 }
 void accumulate_bf16(float* acc, const bf16* src, int64_t n, bool overwrite, int ctas,
                      cudaStream_t s) {
-  accumulate_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(acc, src, n, overwrite);
+  accumulate_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(acc, src, n, overwrite); note_launch();
 }
 void adam_update(float* p32, float* m, float* v, bf16* p16, const float* acc, const bf16* g16,
                  const float* g32, int64_t n, const AdamParams& ap, int ctas, cudaStream_t s) {
-  adam_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(p32, m, v, p16, acc, g16, g32, n, ap);
+  adam_k<<<grid_for(n / 4, kThreads, ctas), kThreads, 0, s>>>(p32, m, v, p16, acc, g16, g32, n, ap); note_launch();
 }
 
 }  // namespace zp

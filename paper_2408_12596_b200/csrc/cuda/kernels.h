@@ -9,6 +9,10 @@ namespace zp {
 
 using bf16 = __nv_bfloat16;
 
+// Count of kernels this library has launched (bench.py's gpu_launches claim).
+void note_launch(int64_t k = 1);
+int64_t launch_count();
+
 // ---- initialisation / data
 void init_normal(float* p32, bf16* p16, int64_t n, float stdv, uint64_t seed, uint64_t offset,
                  int ctas, cudaStream_t s);

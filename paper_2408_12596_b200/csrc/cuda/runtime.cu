@@ -205,6 +205,7 @@ struct Runtime {
   float* gkeep = nullptr; // summed gradient of the last iteration (parity)
   float* dwte32 = nullptr;
   float* dwpe32 = nullptr;
+  float* wgrad32 = nullptr;
   float* ln_part = nullptr;
   float* col_work = nullptr;
   float* loss_steps = nullptr;  // [kMaxSteps]
@@ -220,9 +221,25 @@ struct Runtime {
   int64_t state_len() const { return stage == 0 ? lay.total : shard(); }
 
   // ---------------------------------------------------------------- GEMM helpers
+  // Optional per-launch event timing of the dense (non-attention) GEMMs, for the roofline
+  // numbers bench.py reports (zp_runtime_gemm_stats).
+  bool gemm_timing = false;
+  struct GemmRec {
+    int s, e;
+    double flops;
+  };
+  std::vector<GemmRec> grec;
+  Timer gtm;
+
+  void launch_gemm(const GemmArgs& g, double dense_flops) {
+    int s0 = -1;
+    if (gemm_timing && dense_flops > 0) s0 = gtm.mark(st);
+    CK(gemm(g, st));
+    if (s0 >= 0) grec.push_back({s0, gtm.mark(st), dense_flops});
+  }
   void mm(int M, int N, int K, const bf16* A, int amaj, int64_t lda, const bf16* B, int bmaj,
           int64_t ldb, void* C, int64_t ldc, int epi, float alpha = 1.f, const bf16* bias = nullptr,
-          const bf16* aux = nullptr, bf16* aux_out = nullptr) {
+          const bf16* aux = nullptr, bf16* aux_out = nullptr, int split_k = 1) {
     GemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.a.ptr = A; g.a.major = amaj; g.a.ld = lda;
@@ -230,7 +247,8 @@ struct Runtime {
     g.c = C; g.ldc = ldc;
     g.alpha = alpha; g.epilogue = epi; g.bias = bias; g.aux = aux; g.aux_out = aux_out;
     g.max_ctas = ctas;
-    CK(gemm(g, st));
+    g.split_k = split_k;
+    launch_gemm(g, 2.0 * M * double(N) * K);
   }
   // Per-(head, sample) attention GEMM over s x s / s x 64 blocks.
   void mm_heads(int M, int N, int K, int64_t b, const bf16* A, int amaj, int64_t lda, int64_t a1,
@@ -243,7 +261,26 @@ struct Runtime {
     g.c = C; g.ldc = ldc; g.cs1 = c1; g.cs2 = c2;
     g.alpha = alpha; g.epilogue = epi; g.causal = causal;
     g.max_ctas = ctas;
-    CK(gemm(g, st));
+    launch_gemm(g, 0.0);
+  }
+  // Weight gradient dW[M, N] = sum over the T tokens: few output tiles, very long K. Split K
+  // across CTAs (fp32 atomics into a workspace, then a cast) when the tiles cannot fill the
+  // rank's SMs.
+  void wgrad(int M, int N, int64_t T, const bf16* A, int64_t lda, const bf16* B, int64_t ldb,
+             bf16* dst) {
+    const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+    const int64_t tiles = int64_t((M + 127) / 128) * ((N + bn - 1) / bn);
+    const int64_t kblocks = (T + 63) / 64;
+    int split = 1;
+    if (tiles < ctas) split = int(std::min<int64_t>((ctas + tiles - 1) / tiles, std::max<int64_t>(1, kblocks / 16)));
+    if (split <= 1) {
+      mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, dst, N, kEpiStoreBf16);
+      return;
+    }
+    CK(cudaMemsetAsync(wgrad32, 0, size_t(M) * N * 4, st));
+    mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, wgrad32, N, kEpiAtomicF32, 1.f, nullptr, nullptr,
+       nullptr, split);
+    cast_f32_bf16(wgrad32, dst, int64_t(M) * N, ctas, st);
   }
 
   // ---------------------------------------------------------------- activation plan
@@ -327,6 +364,7 @@ struct Runtime {
     const int64_t h = c.d_model;
     dwte32 = static_cast<float*>(must(arena.take_n<float>(int64_t(vocab_pad) * h), "dwte"));
     dwpe32 = static_cast<float*>(must(arena.take_n<float>(int64_t(c.seq_len) * h), "dwpe"));
+    wgrad32 = static_cast<float*>(must(arena.take_n<float>(std::max<int64_t>(3 * h, c.d_ff) * h), "wgrad"));
     ln_part = static_cast<float*>(must(arena.take_n<float>(int64_t(2) * 2 * 148 * h), "ln partials"));
     const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
     col_work = static_cast<float*>(must(arena.take_n<float>(256 * maxN), "colsum work"));
@@ -436,17 +474,17 @@ struct Runtime {
       LayerActs& L = A.l[i];
       // MLP
       colsum_bf16(A.dx, T, int(h), int(h), col_work, G + P.b_proj.off, ctas, st);
-      mm(h, f, T, A.dx, kMNMajor, h, L.g, kMNMajor, f, G + P.w_proj.off, f, kEpiStoreBf16);
+      wgrad(h, f, T, A.dx, h, L.g, f, G + P.w_proj.off);
       mm(T, f, h, A.dx, kKMajor, h, W + P.w_proj.off, kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
       colsum_bf16(A.du, T, int(f), int(f), col_work, G + P.b_fc.off, ctas, st);
-      mm(f, h, T, A.du, kMNMajor, f, L.ln2, kMNMajor, h, G + P.w_fc.off, h, kEpiStoreBf16);
+      wgrad(f, h, T, A.du, f, L.ln2, h, G + P.w_fc.off);
       mm(T, h, f, A.du, kKMajor, f, W + P.w_fc.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, W + P.ln2_g.off, A.dx, A.dx2, ln_part, &nblk, T, int(h),
                        ctas, st));
       ln_grads(P.ln2_g, P.ln2_b, nblk);
       // attention output projection
       colsum_bf16(A.dx2, T, int(h), int(h), col_work, G + P.b_o.off, ctas, st);
-      mm(h, h, T, A.dx2, kMNMajor, h, L.attn, kMNMajor, h, G + P.w_o.off, h, kEpiStoreBf16);
+      wgrad(h, h, T, A.dx2, h, L.attn, h, G + P.w_o.off);
       mm(T, h, h, A.dx2, kKMajor, h, W + P.w_o.off, kMNMajor, h, A.dO, h, kEpiStoreBf16);
       // attention core, per (head, sample)
       mm_heads(s, s, dh, b, A.dO, kKMajor, h, dh, s * h, L.qkv + 2 * h, kKMajor, 3 * h, dh, s * 3 * h, A.S, s,
@@ -460,7 +498,7 @@ struct Runtime {
                A.dqkv + h, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
       // QKV projection
       colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, G + P.b_qkv.off, ctas, st);
-      mm(3 * h, h, T, A.dqkv, kMNMajor, 3 * h, L.ln1, kMNMajor, h, G + P.w_qkv.off, h, kEpiStoreBf16);
+      wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, G + P.w_qkv.off);
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, W + P.w_qkv.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, W + P.ln1_g.off, A.dx2, A.dx, ln_part, &nblk, T, int(h),
                        ctas, st));
@@ -877,6 +915,7 @@ int zp_runtime_destroy(zp_runtime* h) {
   cudaStreamSynchronize(R.st);
   if (R.comm) ncclCommDestroy(R.comm);
   R.tm.destroy();
+  R.gtm.destroy();
   if (R.tokens) cudaFree(R.tokens);
   if (R.dscratch) cudaFree(R.dscratch);
   for (auto& e : R.marks)
@@ -1018,6 +1057,33 @@ int zp_runtime_elapsed(zp_runtime* h, int32_t a, int32_t b, double* seconds) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, R.marks[a], R.marks[b]));
     *seconds = double(ms) * 1e-3;
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_gemm_stats(zp_runtime* h, int32_t mode, double* flops, double* seconds, int64_t* launches) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (mode == 1) {
+      if (R.gtm.ev.empty()) R.gtm.init(1 << 15);
+      R.gtm.reset();
+      R.grec.clear();
+      R.gemm_timing = true;
+    } else if (mode == 0) {
+      R.gemm_timing = false;
+    } else {
+      CK(cudaStreamSynchronize(R.st));
+      double f = 0, t = 0;
+      for (const auto& g : R.grec) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, R.gtm.ev[g.s], R.gtm.ev[g.e]));
+        f += g.flops;
+        t += double(ms) * 1e-3;
+      }
+      if (flops) *flops = f;
+      if (seconds) *seconds = t;
+      if (launches) *launches = int64_t(R.grec.size());
+    }
     return ZP_OK;
   });
 }

@@ -1,0 +1,63 @@
+"""Poplar on B200: the reference pipeline (profile -> curves -> plan -> execute) with the latent
+device model replaced by the real runtime.
+
+    profile = rt.profile(stage)                      # Alg. 1, lockstep over ranks (C++)
+    plan    = poplar_plan(rt, profile, gbs, stage)   # Alg. 2, bit-exact zeroplan planner (C++)
+    timing  = rt.execute_iteration(plan, stage)      # real ZeRO iteration on this rank
+
+Reference call stack: proj/core/src/experiment.cpp:424-436 (run_through_plan) and
+simulator.cpp:49-116 (simulate_iteration) — same data structures, real devices.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+from . import host
+from .host import ClusterSpec, Device, ModelSpec
+
+# NVLink 5 per-direction bandwidth measured on this pool (peer copy, B200_PROFILING.md) and a
+# typical NCCL launch latency; they parameterise the planner's alpha-beta collective model
+# (reference comm.cpp:88-99), which on NVSwitch is uniform across ranks.
+NVLINK_BPS = 770e9
+NCCL_ALPHA = 25e-6
+
+
+def planner_inputs(rt, n: int, link_bw: float = NVLINK_BPS, alpha: float = NCCL_ALPHA):
+    """ModelSpec / ClusterSpec for `zeroplan::plan`: only the device count and the link model are
+    read by the planner (reference planner.cpp:343-347); the latent device fields are unused."""
+    m = rt.model
+    model = ModelSpec(float(rt.param_count), m.d_model, m.n_layer, 2.0, 16.0)
+    cluster = ClusterSpec([Device(1.0, 1.0, 0.0, 1.0)] * n, [link_bw] * n, alpha)
+    return model, cluster
+
+
+def poplar_plan(rt, profile: dict, gbs: int, stage: int, n: int, uniform: bool = False) -> dict:
+    api = host.product()
+    model, cluster = planner_inputs(rt, n)
+    if not uniform:
+        return api.plan(gbs, profile, stage, model, cluster)
+    comm = api.make_comm_profile(model, stage, cluster)
+    tail = max(d["optimizer_time"] for d in profile["devices"])
+    return api.make_uniform_plan(gbs, profile, stage, comm, tail)
+
+
+def rank_slice(plan: dict, rank: int):
+    """First global sample index and sample count of `rank` (ranks take contiguous ranges in
+    device order, so global sample j is the same sample for every allocation)."""
+    first = sum(d["gmbs"] for d in plan["devices"][:rank])
+    return first, plan["devices"][rank]["gmbs"]
+
+
+def iteration_report(timings: Sequence[dict], gbs: int) -> dict:
+    """Combine per-rank measured timings into the reference's IterationReport
+    (simulator.cpp:104-114). Collective k costs every rank min_j t_j(k) (the last rank to
+    arrive does not wait); anything above that on a faster rank is synchronisation idle.
+    busy_i = compute_i + sum_k min_j t_j(k) + optimizer_i; T = max_i wall_i; idle_i = T - busy_i."""
+    n = len(timings)
+    ncoll = min(len(t["coll_times"]) for t in timings)
+    floor = sum(min(t["coll_times"][k] for t in timings) for k in range(ncoll))
+    T = max(t["wall"] for t in timings)
+    busy = [t["compute"] + floor + t["optimizer"] for t in timings]
+    return {"iteration_time": T, "busy": busy, "idle": [T - b for b in busy],
+            "compute": [t["compute"] for t in timings], "comm_total": floor, "throughput": gbs / T,
+            "sync_idle_pct": [100.0 * max(0.0, T - b) / T for b in busy]}

@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .host import (Plan, Probe, StepTrace, plan_from_py, InvalidInputError, ZeroplanError, _ERR, OK, OOM)
+from .host import (Plan, Probe, Profile, StepTrace, plan_from_py, profile_to_py, ZeroplanError, _ERR, OK, OOM)
 
 lib = _lib.lib
 
@@ -63,6 +63,11 @@ _SIGS = {
     "zp_runtime_tensor_info": ([_P, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)], C.c_int),
     "zp_runtime_sync": ([_P], C.c_int),
+    "zp_runtime_profile": ([_P, C.c_int32, C.POINTER(Profile)], C.c_int),
+    "zp_runtime_mark": ([_P, C.c_int32], C.c_int),
+    "zp_runtime_elapsed": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double)], C.c_int),
+    "zp_runtime_gemm_stats": ([_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                               C.POINTER(C.c_int64)], C.c_int),
 }
 for _n, (_a, _r) in _SIGS.items():
     _f = getattr(lib, _n)
@@ -239,6 +244,27 @@ class Runtime:
 
     def sync(self):
         _check(lib.zp_runtime_sync(self.h))
+
+    # ---- Poplar Alg. 1 on the devices (collective)
+    def profile(self, stage_request: Optional[int] = None) -> dict:
+        p = Profile()
+        _check(lib.zp_runtime_profile(self.h, -1 if stage_request is None else stage_request, C.byref(p)))
+        return profile_to_py(p)
+
+    # ---- device timing
+    def mark(self, slot: int):
+        _check(lib.zp_runtime_mark(self.h, slot))
+
+    def elapsed(self, a: int, b: int) -> float:
+        out = C.c_double()
+        _check(lib.zp_runtime_elapsed(self.h, a, b, C.byref(out)))
+        return out.value
+
+    def gemm_timing(self, mode: int):
+        """1 = enable/reset, 0 = disable, 2 = collect -> (flops, seconds, launches)."""
+        f, t, n = C.c_double(), C.c_double(), C.c_int64()
+        _check(lib.zp_runtime_gemm_stats(self.h, mode, C.byref(f), C.byref(t), C.byref(n)))
+        return f.value, t.value, n.value
 
 
 def bf16_to_f32(u16: np.ndarray) -> np.ndarray:

@@ -19,7 +19,7 @@ def _lib():
 
 def run_gemm(A_store, a_major, B_store, b_major, M, N, K, out_dtype=torch.float32, epilogue=None,
              alpha=1.0, causal=0, nb=(1, 1), a_bs=(0, 0), b_bs=(0, 0), c=None, ldc=None, c_bs=(0, 0),
-             bias=None, aux=None, aux_out=None, lda=None, ldb=None, max_ctas=0, sync=True):
+             bias=None, aux=None, aux_out=None, lda=None, ldb=None, max_ctas=0, sync=True, split_k=1):
     L = _lib()
     if c is None:
         c = torch.zeros(nb[1] * nb[0] * M * N, dtype=out_dtype, device=A_store.device)
@@ -43,6 +43,7 @@ def run_gemm(A_store, a_major, B_store, b_major, M, N, K, out_dtype=torch.float3
     d.aux = aux.data_ptr() if aux is not None else None
     d.aux_out = aux_out.data_ptr() if aux_out is not None else None
     d.max_ctas = max_ctas
+    d.split_k = split_k
     rc = L.lib.zp_gemm(d, torch.cuda.current_stream().cuda_stream)
     assert rc == 0
     if sync:
@@ -168,6 +169,17 @@ def test_gemm_causal_modes(cuda):
     G = torch.randn(s, d, device=cuda).to(torch.bfloat16)
     dV = run_gemm(P, 1, G, 1, s, d, s, causal=3).view(s, d)
     assert relerr(dV, P.float().t() @ G.float()) < 1e-5
+
+
+@pytest.mark.parametrize("split", [2, 5, 16])
+def test_gemm_split_k_weight_grad(cuda, split):
+    # dW = dY^T X with both operands MN-major, K = tokens (long), fp32 atomics across splits.
+    T, M, N = 8192, 768, 3072
+    dY = (0.1 * torch.randn(T, M, device=cuda)).to(torch.bfloat16)
+    X = torch.randn(T, N, device=cuda).to(torch.bfloat16)
+    C = torch.zeros(M * N, device=cuda)
+    run_gemm(dY, 1, X, 1, M, N, T, epilogue=7, c=C, ldc=N, split_k=split)
+    assert relerr(C.view(M, N), dY.float().t() @ X.float()) < 1e-5
 
 
 def test_gemm_sm_budget(cuda):
