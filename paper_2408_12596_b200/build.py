@@ -34,6 +34,19 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
 INCLUDES = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(CSRC, "host")]
 
 
+def _nccl_libdir():
+    """Directory of the libnccl.so.2 that torch loads (the pip nvidia-nccl wheel): libzp links
+    against the same library so torch and the runtime never load two NCCL versions."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return d
+    except Exception:
+        pass
+    return None
+
+
 def _headers():
     hs = glob.glob(os.path.join(CSRC, "**", "*.h*"), recursive=True)
     hs += glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True)
@@ -79,8 +92,10 @@ def build(verbose: bool = False) -> str:
             if o.strip():
                 print(o)
     if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
-            "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart", "-lnccl",
+        nccl = _nccl_libdir()
+        nccl_flags = ["-L", nccl, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl] if nccl else ["-lnccl"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + nccl_flags + [
+            "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart",
             "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64"), "-Xlinker", "-Bsymbolic"]
         _compile(cmd)
     return LIB
