@@ -114,3 +114,24 @@ def test_run_step_trace(cuda):
     assert t["forward_compute"] > 0 and t["backward_compute"] > 0 and t["optimizer_step"] > 0
     assert t["fwd_allgather"] == 0.0
     rt.close()
+
+
+@pytest.mark.parametrize("layers,sm", [(1, 0), (2, 132), (12, 66)])
+def test_step_gpt2_small_shapes(cuda, layers, sm):
+    """GPT-2-small layer shapes (h=768, 12 heads, V=50257 padded to 50304, s=1024), SM budgets."""
+    from paper_2408_12596_b200.runtime import Runtime, GPT, bf16_to_f32
+    from oracle import step as so
+    cfg = GPT(n_layer=layers, d_model=768, n_head=12, vocab=50257, seq_len=1024)
+    rt = Runtime(cfg, seed=4, lr=1e-3, sm_budget=sm)
+    rt.keep_grads(True)
+    rt.resident_bytes(0)
+    P = {k: v.astype(np.float64) for k, v in rt.unflatten(bf16_to_f32(rt.params_bf16())).items()}
+    tok = np.random.default_rng(2).integers(0, cfg.vocab, (2, cfg.seq_len + 1)).astype(np.int32)
+    rt.load_tokens(tok)
+    t = rt.execute_iteration(make_plan(0, 2, 2, 2, 1), 0)
+    loss, G = so.gpt_loss_and_grads(P, tok, layers, 12, cfg.vocab, 2)
+    assert abs(t["loss_sum"] - loss) <= 1e-2 * abs(loss), (t["loss_sum"], loss)
+    g = rt.unflatten(rt.get_state(3)[2])
+    worst = max((so.rel_err(g[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
+    assert worst[0] < 2e-2, worst
+    rt.close()
