@@ -97,9 +97,13 @@ int zp_runtime_execute_iteration(zp_runtime* rt, const zp_allocation_plan* plan,
  * iteration (fp32; needs zp_runtime_keep_grads(rt, 1) before it). Copies this rank's shard
  * [begin, end) of the flat layout to host `out` (capacity >= end - begin floats). */
 int zp_runtime_get_state(zp_runtime* rt, int32_t kind, float* out, int64_t* begin, int64_t* end);
-int zp_runtime_get_params_bf16(zp_runtime* rt, uint16_t* out); /* full bf16 params (stages 0-2) */
+int zp_runtime_get_params_bf16(zp_runtime* rt, uint16_t* out); /* full bf16 params (Z3: owned slices) */
 int zp_runtime_set_params(zp_runtime* rt, const float* full_fp32); /* resets master + bf16 copy */
 int zp_runtime_keep_grads(zp_runtime* rt, int32_t on);
+/* Flat-layout ranges this rank owns, as (flat_begin, flat_end, shard_begin) triples: one range
+ * at stages 0-2, one per parameter group (embedding, each layer, final LN) at stage 3, where the
+ * shard buffers of zp_runtime_get_state are the concatenation of the owned slices. */
+int zp_runtime_owned_ranges(zp_runtime* rt, int64_t* triples, int32_t cap, int32_t* count);
 /* Flat-layout offset/shape of a named tensor ("wte", "wpe", "lnf_g", "lnf_b", "h{i}.ln1_g", ...,
  * "h{i}.w_qkv", "h{i}.b_qkv", "h{i}.w_o", "h{i}.b_o", "h{i}.w_fc", "h{i}.b_fc", "h{i}.w_proj",
  * "h{i}.b_proj", "h{i}.ln2_g", "h{i}.ln2_b"). */

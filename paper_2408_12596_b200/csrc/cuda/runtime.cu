@@ -80,7 +80,14 @@ struct Arena {
 // ------------------------------------------------------------------ parameter layout
 struct Tensor {
   int64_t off = 0, rows = 0, cols = 0;
+  int group = 0;
   int64_t numel() const { return rows * cols; }
+};
+// ZeRO-3 all-gather / reduce-scatter unit: the embedding (wte, wpe), each transformer layer,
+// and the final LayerNorm. Each group's flat region is padded to a multiple of n*256 elements so
+// rank r owns the r-th equal slice of every group.
+struct Group {
+  int64_t start = 0, len = 0;
 };
 struct LayerP {
   Tensor ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc, b_fc, w_proj, b_proj;
@@ -88,28 +95,39 @@ struct LayerP {
 struct Layout {
   Tensor wte, wpe, lnf_g, lnf_b;
   std::vector<LayerP> layers;
+  std::vector<Group> groups;  // 0 = embedding, 1..L = layers, L+1 = final LayerNorm
   std::map<std::string, Tensor> by_name;
-  int64_t logical = 0, total = 0;
+  int64_t logical = 0, total = 0, max_layer_group = 0, max_group = 0;
 };
 
 Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
   Layout L;
   int64_t cur = 0;
+  const int64_t unit = int64_t(world) * 256;
+  auto open_group = [&]() { L.groups.push_back(Group{cur, 0}); };
+  auto close_group = [&]() {
+    cur = round_up(cur, unit);
+    L.groups.back().len = cur - L.groups.back().start;
+  };
   auto add = [&](const std::string& name, int64_t r, int64_t k, int64_t logical_rows) {
     Tensor t;
     t.off = cur;
     t.rows = r;
     t.cols = k;
+    t.group = int(L.groups.size()) - 1;
     cur = round_up(cur + r * k, 64);
     L.logical += logical_rows * k;
     L.by_name[name] = t;
     return t;
   };
   const int h = c.d_model, f = c.d_ff;
+  open_group();
   L.wte = add("wte", vocab_pad, h, c.vocab);
   L.wpe = add("wpe", c.seq_len, h, c.seq_len);
+  close_group();
   for (int i = 0; i < c.n_layer; ++i) {
     const std::string p = "h" + std::to_string(i) + ".";
+    open_group();
     LayerP l;
     l.ln1_g = add(p + "ln1_g", 1, h, 1);
     l.ln1_b = add(p + "ln1_b", 1, h, 1);
@@ -123,11 +141,16 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
     l.b_fc = add(p + "b_fc", 1, f, 1);
     l.w_proj = add(p + "w_proj", h, f, h);
     l.b_proj = add(p + "b_proj", 1, h, 1);
+    close_group();
     L.layers.push_back(l);
+    L.max_layer_group = std::max(L.max_layer_group, L.groups.back().len);
   }
+  open_group();
   L.lnf_g = add("lnf_g", 1, h, 1);
   L.lnf_b = add("lnf_b", 1, h, 1);
-  L.total = round_up(cur, int64_t(world) * 256);
+  close_group();
+  L.total = cur;
+  for (const Group& g : L.groups) L.max_group = std::max(L.max_group, g.len);
   return L;
 }
 
@@ -147,7 +170,7 @@ struct Acts {
 };
 
 // ------------------------------------------------------------------ event timing
-enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4 };
+enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4, kAgF = 5, kAgB = 6, kRs = 7 };
 struct Span {
   int kind, start, end;
 };
@@ -203,6 +226,17 @@ struct Runtime {
   float* r32 = nullptr;   // Z1: [shard] reduce-scatter output
   bf16* r16 = nullptr;    // Z2: [shard] reduce-scatter output
   float* gkeep = nullptr; // summed gradient of the last iteration (parity)
+  // ZeRO-3: parameters exist only as this rank's shard plus per-group gather buffers
+  bf16* p16s = nullptr;          // [shard] bf16 parameter shard (shard order)
+  bf16* gb_emb = nullptr;        // gathered embedding group (kept for the whole micro-step)
+  bf16* gb_fin = nullptr;        // gathered final-LN group
+  bf16* gb_layer[2] = {nullptr, nullptr};  // gathered transformer layer (double buffer)
+  bf16* ggrp = nullptr;          // gradient of the group being reduced
+  std::vector<int64_t> shoff;    // shard-order offset of each group's owned slice
+  struct Owned {
+    int64_t flat_begin, flat_end, shard_begin;
+  };
+  std::vector<Owned> owned;      // flat ranges whose master / Adam state this rank holds
   float* dwte32 = nullptr;
   float* dwpe32 = nullptr;
   float* wgrad32 = nullptr;
@@ -217,8 +251,42 @@ struct Runtime {
   static constexpr int kMaxSteps = 4096;
 
   int64_t shard() const { return lay.total / n; }
-  int64_t shard_begin() const { return stage == 0 ? 0 : shard() * rank; }
+  int64_t shard_begin() const { return stage == 0 ? 0 : (stage == 3 ? 0 : shard() * rank); }
   int64_t state_len() const { return stage == 0 ? lay.total : shard(); }
+
+  void set_owned() {
+    owned.clear();
+    shoff.assign(lay.groups.size(), 0);
+    if (stage == 0) {
+      owned.push_back({0, lay.total, 0});
+    } else if (stage <= 2) {
+      owned.push_back({shard() * rank, shard() * (rank + 1), 0});
+    } else {
+      int64_t so = 0;
+      for (size_t g = 0; g < lay.groups.size(); ++g) {
+        const Group& G = lay.groups[g];
+        const int64_t part = G.len / n;
+        shoff[g] = so;
+        owned.push_back({G.start + part * rank, G.start + part * (rank + 1), so});
+        so += part;
+      }
+    }
+  }
+
+  // Parameter / gradient pointer of a tensor for the configured stage.
+  const bf16* Wp(const Tensor& t) const {
+    if (stage != 3) return p16 + t.off;
+    if (n == 1) return p16s + t.off;  // one rank: shard order == flat order
+    const Group& G = lay.groups[t.group];
+    const bf16* base = t.group == 0 ? gb_emb
+                     : (t.group == int(lay.groups.size()) - 1 ? gb_fin : gb_layer[(t.group - 1) & 1]);
+    return base + (t.off - G.start);
+  }
+  bf16* Gp(const Tensor& t) const {
+    if (stage != 3) return g16 + t.off;
+    if (n == 1) return r16 + t.off;
+    return ggrp + (t.off - lay.groups[t.group].start);
+  }
 
   // ---------------------------------------------------------------- GEMM helpers
   // Optional per-launch event timing of the dense (non-attention) GEMMs, for the roofline
@@ -337,7 +405,7 @@ struct Runtime {
   // ---------------------------------------------------------------- stage configuration
   void configure(int new_stage) {
     if (new_stage == stage) return;
-    if (new_stage < 0 || new_stage > 2) fail(ZP_EINVAL, "stage must be 0, 1 or 2 on this build");
+    if (new_stage < 0 || new_stage > 3) fail(ZP_EINVAL, "stage must be 0, 1, 2 or 3");
     arena.used = 0;
     arena.high = 0;
     stage = -1;
@@ -346,32 +414,49 @@ struct Runtime {
       if (!p) fail(ZP_OOM, std::string("resident state does not fit the HBM cap: ") + what);
       return p;
     };
-    p16 = static_cast<bf16*>(must(arena.take_n<bf16>(T), "bf16 params"));
-    g16 = static_cast<bf16*>(must(arena.take_n<bf16>(T), "bf16 grads"));
-    const int64_t SL = new_stage == 0 ? T : S;
-    p32 = static_cast<float*>(must(arena.take_n<float>(SL), "master params"));
-    m32 = static_cast<float*>(must(arena.take_n<float>(SL), "adam m"));
-    v32 = static_cast<float*>(must(arena.take_n<float>(SL), "adam v"));
+    auto B16 = [&](int64_t nel, const char* what) { return static_cast<bf16*>(must(arena.take_n<bf16>(nel), what)); };
+    auto F32 = [&](int64_t nel, const char* what) { return static_cast<float*>(must(arena.take_n<float>(nel), what)); };
+    p16 = g16 = p16s = r16 = ggrp = gb_emb = gb_fin = nullptr;
+    gb_layer[0] = gb_layer[1] = nullptr;
     acc = r32 = nullptr;
-    r16 = nullptr;
-    if (new_stage <= 1) acc = static_cast<float*>(must(arena.take_n<float>(T), "grad accumulator"));
-    if (new_stage == 1) r32 = static_cast<float*>(must(arena.take_n<float>(S), "rs shard"));
-    if (new_stage == 2) {
-      acc = static_cast<float*>(must(arena.take_n<float>(S), "grad accumulator shard"));
-      r16 = static_cast<bf16*>(must(arena.take_n<bf16>(S), "rs shard"));
+    const int64_t SL = new_stage == 0 ? T : S;
+    if (new_stage <= 2) {
+      p16 = B16(T, "bf16 params");
+      g16 = B16(T, "bf16 grads");
+    } else {
+      p16s = B16(S, "bf16 param shard");
+      if (n > 1) {
+        gb_emb = B16(lay.groups.front().len, "embedding gather buffer");
+        gb_fin = B16(lay.groups.back().len, "final gather buffer");
+        gb_layer[0] = B16(lay.max_layer_group, "layer gather buffer 0");
+        gb_layer[1] = B16(lay.max_layer_group, "layer gather buffer 1");
+        ggrp = B16(lay.max_group, "group gradient");
+      }
     }
-    gkeep = keep_grads ? static_cast<float*>(must(arena.take_n<float>(SL), "kept grads")) : nullptr;
+    p32 = F32(SL, "master params");
+    m32 = F32(SL, "adam m");
+    v32 = F32(SL, "adam v");
+    if (new_stage <= 1) acc = F32(T, "grad accumulator");
+    if (new_stage == 1) r32 = F32(S, "rs shard");
+    if (new_stage >= 2) {
+      acc = F32(S, "grad accumulator shard");
+      r16 = B16(S, "rs shard");
+    }
+    gkeep = keep_grads ? F32(SL, "kept grads") : nullptr;
     const int64_t h = c.d_model;
-    dwte32 = static_cast<float*>(must(arena.take_n<float>(int64_t(vocab_pad) * h), "dwte"));
-    dwpe32 = static_cast<float*>(must(arena.take_n<float>(int64_t(c.seq_len) * h), "dwpe"));
-    wgrad32 = static_cast<float*>(must(arena.take_n<float>(std::max<int64_t>(3 * h, c.d_ff) * h), "wgrad"));
-    ln_part = static_cast<float*>(must(arena.take_n<float>(int64_t(2) * 2 * 148 * h), "ln partials"));
+    dwte32 = F32(int64_t(vocab_pad) * h, "dwte");
+    dwpe32 = F32(int64_t(c.seq_len) * h, "dwpe");
+    wgrad32 = F32(std::max<int64_t>(3 * h, c.d_ff) * h, "wgrad");
+    ln_part = F32(int64_t(2) * 2 * 148 * h, "ln partials");
     const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
-    col_work = static_cast<float*>(must(arena.take_n<float>(256 * maxN), "colsum work"));
-    loss_steps = static_cast<float*>(must(arena.take_n<float>(kMaxSteps), "loss"));
+    col_work = F32(256 * maxN, "colsum work");
+    loss_steps = F32(kMaxSteps, "loss");
     stage = new_stage;
+    set_owned();
     resident_mark = arena.used;
-    CK(cudaMemsetAsync(g16, 0, size_t(T) * 2, st));
+    if (g16) CK(cudaMemsetAsync(g16, 0, size_t(T) * 2, st));
+    if (ggrp) CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
+    if (r16) CK(cudaMemsetAsync(r16, 0, size_t(S) * 2, st));
     CK(cudaMemsetAsync(m32, 0, size_t(SL) * 4, st));
     CK(cudaMemsetAsync(v32, 0, size_t(SL) * 4, st));
     init_params();
@@ -382,25 +467,29 @@ struct Runtime {
   // GPT-2 initialisation, a pure function of (seed, flat index): identical on every rank for
   // every sharding. Residual projections use std 0.02/sqrt(2L).
   void init_params() {
-    const int64_t lo = shard_begin(), hi = lo + state_len();
     auto init = [&](const Tensor& t, int kind, float stdv) {
-      // full bf16 copy
-      if (kind == 0)
-        init_normal(nullptr, p16 + t.off, t.numel(), stdv, d.seed, uint64_t(t.off), ctas, st);
-      else
-        init_const(nullptr, p16 + t.off, t.numel(), kind == 1 ? 1.f : 0.f, ctas, st);
-      // master shard overlap
-      const int64_t a = std::max(lo, t.off), e = std::min(hi, t.off + t.numel());
-      if (a < e) {
+      const float val = kind == 1 ? 1.f : 0.f;
+      if (p16) {  // full bf16 copy (stages 0-2)
         if (kind == 0)
-          init_normal(p32 + (a - lo), nullptr, e - a, stdv, d.seed, uint64_t(a), ctas, st);
+          init_normal(nullptr, p16 + t.off, t.numel(), stdv, d.seed, uint64_t(t.off), ctas, st);
         else
-          init_const(p32 + (a - lo), nullptr, e - a, kind == 1 ? 1.f : 0.f, ctas, st);
+          init_const(nullptr, p16 + t.off, t.numel(), val, ctas, st);
+      }
+      for (const Owned& o : owned) {  // master (and the Z3 bf16 shard) over the owned ranges
+        const int64_t a = std::max(o.flat_begin, t.off), e = std::min(o.flat_end, t.off + t.numel());
+        if (a >= e) continue;
+        float* dst = p32 + o.shard_begin + (a - o.flat_begin);
+        bf16* dst16 = p16s ? p16s + o.shard_begin + (a - o.flat_begin) : nullptr;
+        if (kind == 0)
+          init_normal(dst, dst16, e - a, stdv, d.seed, uint64_t(a), ctas, st);
+        else
+          init_const(dst, dst16, e - a, val, ctas, st);
       }
     };
     const float sp = 0.02f / std::sqrt(2.0f * c.n_layer);
     // padding between tensors stays zero
-    CK(cudaMemsetAsync(p16, 0, size_t(lay.total) * 2, st));
+    if (p16) CK(cudaMemsetAsync(p16, 0, size_t(lay.total) * 2, st));
+    if (p16s) CK(cudaMemsetAsync(p16s, 0, size_t(shard()) * 2, st));
     CK(cudaMemsetAsync(p32, 0, size_t(state_len()) * 4, st));
     Tensor wte_real = lay.wte;
     wte_real.rows = c.vocab;  // padded vocabulary rows stay zero
@@ -418,74 +507,125 @@ struct Runtime {
     init(lay.lnf_b, 2, 0);
   }
 
+  // ---------------------------------------------------------------- ZeRO-3 group collectives
+  // Issue order is fixed (every rank, with or without work, calls the same sequence):
+  //   forward : AG(0), AG(1) .. AG(L), AG(L+1)
+  //   backward: RS(L+1), then AG(i), RS(i) for i = L .. 1, then RS(0)
+  bf16* gather_dst(int g) {
+    if (g == 0) return gb_emb;
+    if (g == int(lay.groups.size()) - 1) return gb_fin;
+    return gb_layer[(g - 1) & 1];
+  }
+  void z3_gather(int g, int kind) {
+    if (stage != 3 || n == 1) return;
+    const Group& G = lay.groups[g];
+    const int s0 = tm.mark(st);
+    NK(ncclAllGather(p16s + shoff[g], gather_dst(g), size_t(G.len / n), ncclBfloat16, comm, st));
+    tm.close(kind, s0, st);
+  }
+  void z3_reduce(int g) {
+    if (stage != 3 || n == 1) return;
+    const Group& G = lay.groups[g];
+    const int s0 = tm.mark(st);
+    NK(ncclReduceScatter(ggrp, r16 + shoff[g], size_t(G.len / n), ncclBfloat16, ncclSum, comm, st));
+    tm.close(kRs, s0, st);
+  }
+  // Zero the reused group-gradient buffer so padding never carries another group's values.
+  void z3_clear_group(int g) {
+    if (stage != 3 || n == 1) return;
+    CK(cudaMemsetAsync(ggrp, 0, size_t(lay.groups[g].len) * 2, st));
+  }
+  // A rank with no samples in a ZeRO-3 micro-step still joins every collective, with zeros.
+  void z3_idle_step() {
+    if (n == 1) {
+      CK(cudaMemsetAsync(r16, 0, size_t(shard()) * 2, st));
+      return;
+    }
+    const int G = int(lay.groups.size());
+    CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
+    for (int g = 0; g < G; ++g) z3_gather(g, kAgF);
+    z3_reduce(G - 1);
+    for (int g = G - 2; g >= 1; --g) {
+      z3_gather(g, kAgB);
+      z3_reduce(g);
+    }
+    z3_reduce(0);
+  }
+
   // ---------------------------------------------------------------- forward / backward
   void forward(Acts& A, const int32_t* tok, bool with_loss, float grad_scale) {
     const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
     const float scale = 1.0f / std::sqrt(float(h / H));
-    bf16* W = p16;
-    embed_fwd(tok, int(s), W + lay.wte.off, W + lay.wpe.off, A.l[0].x_in, T, int(h), ctas, st);
+    const int NG = int(lay.groups.size());
+    z3_gather(0, kAgF);
+    embed_fwd(tok, int(s), Wp(lay.wte), Wp(lay.wpe), A.l[0].x_in, T, int(h), ctas, st);
     for (int i = 0; i < c.n_layer; ++i) {
       const LayerP& P = lay.layers[i];
       LayerActs& L = A.l[i];
+      z3_gather(i + 1, kAgF);
       bf16* x_out = (i + 1 < c.n_layer) ? A.l[i + 1].x_in : A.x_final;
-      CK(layernorm_fwd(L.x_in, W + P.ln1_g.off, W + P.ln1_b.off, L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
-      mm(T, 3 * h, h, L.ln1, kKMajor, h, W + P.w_qkv.off, kKMajor, h, L.qkv, 3 * h, kEpiBiasBf16, 1.f,
-         W + P.b_qkv.off);
+      CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), Wp(P.ln1_b), L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
+      mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiBiasBf16, 1.f,
+         Wp(P.b_qkv));
       mm_heads(s, s, h / H, b, L.qkv, kKMajor, 3 * h, h / H, s * 3 * h, L.qkv + h, kKMajor, 3 * h, h / H,
                s * 3 * h, A.S, s, s * s, H * s * s, kEpiStoreF32, scale, kCausalSkipUpper);
       softmax_causal_fwd(A.S, L.P, b * H * s, int(s), ctas, st);
       mm_heads(s, h / H, s, b, L.P, kKMajor, s, s * s, H * s * s, L.qkv + 2 * h, kMNMajor, 3 * h, h / H,
                s * 3 * h, L.attn, h, h / H, s * h, kEpiStoreBf16, 1.f, kCausalKUpper);
-      mm(T, h, h, L.attn, kKMajor, h, W + P.w_o.off, kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f,
-         W + P.b_o.off, L.x_in);
-      CK(layernorm_fwd(L.x_mid, W + P.ln2_g.off, W + P.ln2_b.off, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
-      mm(T, f, h, L.ln2, kKMajor, h, W + P.w_fc.off, kKMajor, h, L.g, f, kEpiBiasGeluBf16, 1.f,
-         W + P.b_fc.off, nullptr, L.u);
-      mm(T, h, f, L.g, kKMajor, f, W + P.w_proj.off, kKMajor, f, x_out, h, kEpiBiasResidBf16, 1.f,
-         W + P.b_proj.off, L.x_mid);
+      mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f,
+         Wp(P.b_o), L.x_in);
+      CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), Wp(P.ln2_b), L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
+      mm(T, f, h, L.ln2, kKMajor, h, Wp(P.w_fc), kKMajor, h, L.g, f, kEpiBiasGeluBf16, 1.f,
+         Wp(P.b_fc), nullptr, L.u);
+      mm(T, h, f, L.g, kKMajor, f, Wp(P.w_proj), kKMajor, f, x_out, h, kEpiBiasResidBf16, 1.f,
+         Wp(P.b_proj), L.x_mid);
     }
-    CK(layernorm_fwd(A.x_final, W + lay.lnf_g.off, W + lay.lnf_b.off, A.lnf, A.muf, A.rsf, T, int(h), ctas,
+    z3_gather(NG - 1, kAgF);
+    CK(layernorm_fwd(A.x_final, Wp(lay.lnf_g), Wp(lay.lnf_b), A.lnf, A.muf, A.rsf, T, int(h), ctas,
                      st));
-    mm(T, vocab_pad, h, A.lnf, kKMajor, h, W + lay.wte.off, kKMajor, h, A.logits, vocab_pad, kEpiStoreBf16);
+    mm(T, vocab_pad, h, A.lnf, kKMajor, h, Wp(lay.wte), kKMajor, h, A.logits, vocab_pad, kEpiStoreBf16);
     if (with_loss)
       cross_entropy_fwd_bwd(A.logits, tok, int(s), T, c.vocab, vocab_pad, grad_scale, A.row_loss, ctas, st);
   }
 
   void ln_grads(const Tensor& g, const Tensor& b, int nblk) {
     const int h = c.d_model;
-    sum_partials(ln_part, nblk, h, g16 + g.off, st);
-    sum_partials(ln_part + int64_t(nblk) * h, nblk, h, g16 + b.off, st);
+    sum_partials(ln_part, nblk, h, Gp(g), st);
+    sum_partials(ln_part + int64_t(nblk) * h, nblk, h, Gp(b), st);
   }
 
   void backward(Acts& A, const int32_t* tok) {
     const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s, dh = h / H;
     const float scale = 1.0f / std::sqrt(float(dh));
-    bf16* W = p16;
-    bf16* G = g16;
     int nblk = 0;
+    const int NG = int(lay.groups.size());
+    z3_clear_group(NG - 1);
     // LM head (tied with wte): dlnf = dlogits * wte ; dwte = dlogits^T * lnf
-    mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, W + lay.wte.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
+    mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, Wp(lay.wte), kMNMajor, h, A.dln, h, kEpiStoreBf16);
     mm(vocab_pad, h, T, A.logits, kMNMajor, vocab_pad, A.lnf, kMNMajor, h, dwte32, h, kEpiStoreF32);
-    CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, W + lay.lnf_g.off, nullptr, A.dx, ln_part, &nblk, T,
+    CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, Wp(lay.lnf_g), nullptr, A.dx, ln_part, &nblk, T,
                      int(h), ctas, st));
     ln_grads(lay.lnf_g, lay.lnf_b, nblk);
+    z3_reduce(NG - 1);
     for (int i = c.n_layer - 1; i >= 0; --i) {
       const LayerP& P = lay.layers[i];
       LayerActs& L = A.l[i];
+      z3_gather(i + 1, kAgB);
+      z3_clear_group(i + 1);
       // MLP
-      colsum_bf16(A.dx, T, int(h), int(h), col_work, G + P.b_proj.off, ctas, st);
-      wgrad(h, f, T, A.dx, h, L.g, f, G + P.w_proj.off);
-      mm(T, f, h, A.dx, kKMajor, h, W + P.w_proj.off, kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
-      colsum_bf16(A.du, T, int(f), int(f), col_work, G + P.b_fc.off, ctas, st);
-      wgrad(f, h, T, A.du, f, L.ln2, h, G + P.w_fc.off);
-      mm(T, h, f, A.du, kKMajor, f, W + P.w_fc.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
-      CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, W + P.ln2_g.off, A.dx, A.dx2, ln_part, &nblk, T, int(h),
+      colsum_bf16(A.dx, T, int(h), int(h), col_work, Gp(P.b_proj), ctas, st);
+      wgrad(h, f, T, A.dx, h, L.g, f, Gp(P.w_proj));
+      mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_proj), kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
+      colsum_bf16(A.du, T, int(f), int(f), col_work, Gp(P.b_fc), ctas, st);
+      wgrad(f, h, T, A.du, f, L.ln2, h, Gp(P.w_fc));
+      mm(T, h, f, A.du, kKMajor, f, Wp(P.w_fc), kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h),
                        ctas, st));
       ln_grads(P.ln2_g, P.ln2_b, nblk);
       // attention output projection
-      colsum_bf16(A.dx2, T, int(h), int(h), col_work, G + P.b_o.off, ctas, st);
-      wgrad(h, h, T, A.dx2, h, L.attn, h, G + P.w_o.off);
-      mm(T, h, h, A.dx2, kKMajor, h, W + P.w_o.off, kMNMajor, h, A.dO, h, kEpiStoreBf16);
+      colsum_bf16(A.dx2, T, int(h), int(h), col_work, Gp(P.b_o), ctas, st);
+      wgrad(h, h, T, A.dx2, h, L.attn, h, Gp(P.w_o));
+      mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
       // attention core, per (head, sample)
       mm_heads(s, s, dh, b, A.dO, kKMajor, h, dh, s * h, L.qkv + 2 * h, kKMajor, 3 * h, dh, s * 3 * h, A.S, s,
                s * s, H * s * s, kEpiStoreF32, 1.f, kCausalSkipUpper);
@@ -497,17 +637,20 @@ struct Runtime {
       mm_heads(s, dh, s, b, A.dS, kMNMajor, s, s * s, H * s * s, L.qkv, kMNMajor, 3 * h, dh, s * 3 * h,
                A.dqkv + h, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
       // QKV projection
-      colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, G + P.b_qkv.off, ctas, st);
-      wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, G + P.w_qkv.off);
-      mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, W + P.w_qkv.off, kMNMajor, h, A.dln, h, kEpiStoreBf16);
-      CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, W + P.ln1_g.off, A.dx2, A.dx, ln_part, &nblk, T, int(h),
+      colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, Gp(P.b_qkv), ctas, st);
+      wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
+      mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h),
                        ctas, st));
       ln_grads(P.ln1_g, P.ln1_b, nblk);
+      z3_reduce(i + 1);
     }
     CK(cudaMemsetAsync(dwpe32, 0, size_t(c.seq_len) * h * 4, st));
+    z3_clear_group(0);
     embed_bwd(tok, int(s), A.dx, dwte32, dwpe32, T, int(h), ctas, st);
-    cast_f32_bf16(dwte32, G + lay.wte.off, int64_t(vocab_pad) * h, ctas, st);
-    cast_f32_bf16(dwpe32, G + lay.wpe.off, int64_t(c.seq_len) * h, ctas, st);
+    cast_f32_bf16(dwte32, Gp(lay.wte), int64_t(vocab_pad) * h, ctas, st);
+    cast_f32_bf16(dwpe32, Gp(lay.wpe), int64_t(c.seq_len) * h, ctas, st);
+    z3_reduce(0);
   }
 
   // ---------------------------------------------------------------- collectives
@@ -586,16 +729,20 @@ struct Runtime {
         ++active;
       } else if (stage == 2) {
         CK(cudaMemsetAsync(g16, 0, size_t(total) * 2, st));  // joins the collective with zeros
+      } else if (stage == 3) {
+        z3_idle_step();  // gathers and zero-gradient reduce-scatters, same order as a real step
       }
       if (stage <= 1) {
         if (b > 0) {
           accumulate_bf16(acc, g16, total, !any_local, ctas, st);
           any_local = true;
         }
-      } else {  // Z2: reduce-scatter every micro-step
+      } else if (stage == 2) {  // Z2: reduce-scatter every micro-step
         bf16* src = (n == 1) ? g16 : r16;
         reduce_scatter_bf16(g16, r16);
         if (!last) accumulate_bf16(acc, src, sh, k == 0, ctas, st);
+      } else {  // Z3: the per-group reduce-scatters already landed in r16 during backward
+        if (!last) accumulate_bf16(acc, r16, sh, k == 0, ctas, st);
       }
     }
     if (stage <= 1 && !any_local) CK(cudaMemsetAsync(acc, 0, size_t(total) * 4, st));
@@ -621,16 +768,16 @@ struct Runtime {
       tm.close(kOpt, o0, st);
       all_gather_params();
     } else {
-      const bf16* g = (n == 1) ? g16 : r16;
+      const bf16* g = (stage == 2 && n == 1) ? g16 : r16;
       const float* a = steps.size() > 1 ? acc : nullptr;
       if (gkeep) {
         accumulate_bf16(gkeep, g, L, true, ctas, st);
         if (a) add_f32(gkeep, a, L, ctas, st);
       }
       const int o0 = tm.mark(st);
-      adam_update(p32, m32, v32, p16 + shard_begin(), a, g, nullptr, L, ap, ctas, st);
+      adam_update(p32, m32, v32, stage == 3 ? p16s : p16 + shard_begin(), a, g, nullptr, L, ap, ctas, st);
       tm.close(kOpt, o0, st);
-      all_gather_params();
+      if (stage == 2) all_gather_params();  // Z3 gathers on demand in the next forward
     }
     tm.close(kWall, t0, st);
     last_gscale = gscale;
@@ -665,7 +812,9 @@ struct Runtime {
     arena.high = arena.used = resident_mark;
     Acts A;
     plan_acts(1, &A, &arena);  // throws ZP_OOM when batch 1 does not fit
-    forward(A, tokens, false, 0.f);
+    // The probe is local: at ZeRO-3 the forward would need the other ranks' all-gathers, so
+    // there the high-water mark is the reservation itself (identical by construction).
+    if (stg != 3) forward(A, tokens, false, 0.f);
     CK(cudaStreamSynchronize(st));
     p.after_forward = double(arena.high);
     p.total = double(arena.cap);
@@ -686,9 +835,13 @@ struct Runtime {
     out->optimizer_step = t.optimizer;
     if (stg <= 1) {
       out->allreduce = t.comm;
-    } else {
+    } else if (stg == 2) {
       out->reduce_scatter = t.n_collectives > 0 ? t.coll_times[0] : 0.0;
       out->allreduce = t.n_collectives > 1 ? t.coll_times[1] : 0.0;
+    } else {
+      out->fwd_allgather = t_agf;
+      out->bwd_allgather = t_agb;
+      out->reduce_scatter = t_rs;
     }
     return oom >= 0 ? ZP_OOM : ZP_OK;
   }
@@ -736,7 +889,7 @@ struct Runtime {
   // ZeRO-2 reduce-scatters always have all ranks. Stage escalation needs every rank to fit batch 1
   // (profiler.cpp:135-147). The per-rank results are all-gathered into one ProfileResult.
   int profile(int stage_request, zp_profile* out) {
-    for (int s = stage_request < 0 ? 0 : stage_request; s <= 2; ++s) {
+    for (int s = stage_request < 0 ? 0 : stage_request; s <= 3; ++s) {
       zp_probe pr{};
       bool fits = true;
       try {
@@ -799,9 +952,11 @@ struct Runtime {
     fail(ZP_EINFEASIBLE, "model too large: a single batch does not fit on every rank");
   }
 
+  double t_agf = 0, t_agb = 0, t_rs = 0;  // ZeRO-3 split of the last collect()
   void collect(zp_rank_timing* t, int64_t active, size_t nsteps) {
     CK(cudaStreamSynchronize(st));
     std::memset(t, 0, sizeof(*t));
+    t_agf = t_agb = t_rs = 0;
     for (const Span& sp : tm.spans) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, tm.ev[sp.start], tm.ev[sp.end]));
@@ -810,8 +965,14 @@ struct Runtime {
         case kFwd: t->forward += sec; break;
         case kBwd: t->backward += sec; break;
         case kComm:
+        case kAgF:
+        case kAgB:
+        case kRs:
           t->comm += sec;
           if (t->n_collectives < 512) t->coll_times[t->n_collectives++] = sec;
+          if (sp.kind == kAgF) t_agf += sec;
+          if (sp.kind == kAgB) t_agb += sec;
+          if (sp.kind == kRs) t_rs += sec;
           break;
         case kOpt: t->optimizer += sec; break;
         case kWall: t->wall = sec; break;
@@ -987,7 +1148,7 @@ int zp_runtime_get_state(zp_runtime* h, int32_t kind, float* out, int64_t* begin
     CK(cudaStreamSynchronize(R.st));
     CK(cudaMemcpy(out, src, size_t(R.state_len()) * 4, cudaMemcpyDeviceToHost));
     *begin = R.shard_begin();
-    *end = R.shard_begin() + R.state_len();
+    *end = R.shard_begin() + R.state_len();  // ZeRO-3: shard order, see zp_runtime_owned_ranges
     return ZP_OK;
   });
 }
@@ -997,7 +1158,13 @@ int zp_runtime_get_params_bf16(zp_runtime* h, uint16_t* out) {
     zp::Runtime& R = h->rt;
     if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
     CK(cudaStreamSynchronize(R.st));
-    CK(cudaMemcpy(out, R.p16, size_t(R.lay.total) * 2, cudaMemcpyDeviceToHost));
+    if (R.stage != 3) {
+      CK(cudaMemcpy(out, R.p16, size_t(R.lay.total) * 2, cudaMemcpyDeviceToHost));
+    } else {  // only this rank's owned slices are filled
+      for (const auto& o : R.owned)
+        CK(cudaMemcpy(out + o.flat_begin, R.p16s + o.shard_begin, size_t(o.flat_end - o.flat_begin) * 2,
+                      cudaMemcpyDeviceToHost));
+    }
     return ZP_OK;
   });
 }
@@ -1009,11 +1176,29 @@ int zp_runtime_set_params(zp_runtime* h, const float* full) {
     float* tmp = nullptr;
     CK(cudaMalloc(&tmp, size_t(R.lay.total) * 4));
     CK(cudaMemcpyAsync(tmp, full, size_t(R.lay.total) * 4, cudaMemcpyHostToDevice, R.st));
-    zp::cast_f32_bf16(tmp, R.p16, R.lay.total, R.ctas, R.st);
-    CK(cudaMemcpyAsync(R.p32, tmp + R.shard_begin(), size_t(R.state_len()) * 4, cudaMemcpyDeviceToDevice,
-                       R.st));
+    if (R.p16) zp::cast_f32_bf16(tmp, R.p16, R.lay.total, R.ctas, R.st);
+    for (const auto& o : R.owned) {
+      const int64_t len = o.flat_end - o.flat_begin;
+      CK(cudaMemcpyAsync(R.p32 + o.shard_begin, tmp + o.flat_begin, size_t(len) * 4, cudaMemcpyDeviceToDevice,
+                         R.st));
+      if (R.p16s) zp::cast_f32_bf16(tmp + o.flat_begin, R.p16s + o.shard_begin, len, R.ctas, R.st);
+    }
     CK(cudaStreamSynchronize(R.st));
     CK(cudaFree(tmp));
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_owned_ranges(zp_runtime* h, int64_t* triples, int32_t cap, int32_t* count) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
+    *count = int32_t(R.owned.size());
+    for (size_t i = 0; i < R.owned.size() && int32_t(i) < cap; ++i) {
+      triples[3 * i] = R.owned[i].flat_begin;
+      triples[3 * i + 1] = R.owned[i].flat_end;
+      triples[3 * i + 2] = R.owned[i].shard_begin;
+    }
     return ZP_OK;
   });
 }
