@@ -43,6 +43,17 @@ typedef struct zp_gemm_desc {
 
 int zp_gemm(const zp_gemm_desc* d, void* stream);
 
+/* Fused causal attention, head_dim 64 (tcgen05; scores never reach HBM).
+ * qkv [batch*seq, 3*heads*64] bf16 (Q | K | V); out [batch*seq, heads*64] bf16;
+ * lse [batch*heads*seq] fp32 (natural log of the row sum of exp(scores / 8)). */
+int zp_attention_fwd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq, int32_t heads,
+                     int32_t max_ctas, void* stream);
+/* Gradients of the above: dout [batch*seq, heads*64] -> dqkv [batch*seq, 3*heads*64] bf16.
+ * Workspaces: dvec [batch*heads*seq] fp32, dq32 [batch*seq, heads*64] fp32. */
+int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
+                     float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t max_ctas,
+                     void* stream);
+
 /* Number of kernels launched by this library since load (all entry points). */
 int64_t zp_launch_count(void);
 

@@ -1,0 +1,638 @@
+// Fused causal attention for head_dim 64 on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// Forward (one CTA task = 128 queries of one (head, sample)): for every 128-key tile at or
+// below the diagonal, S = Q K^T lands in TMEM, four softmax warps read it row-per-thread,
+// run the online softmax in registers, write P (bf16) into a SWIZZLE_128B shared tile and the
+// MMA warp computes P V into TMEM; the softmax warps fold it into a register accumulator.
+// Nothing of size s x s ever reaches HBM: the kernel reads Q, K, V once per query tile and
+// writes O and the row log-sum-exp.
+//
+// Backward (one CTA task = 128 keys of one (head, sample)): for every query tile at or above
+// the diagonal, S = Q K^T and dP = dO V^T land in TMEM; the softmax warps rebuild
+// P = exp(S - LSE) and dS = P (dP - D) into shared memory; the MMA warp accumulates
+// dV += P^T dO and dK += dS^T Q in TMEM (the shared P / dS tiles are read as MN-major
+// operands, no transpose) and computes dQ_tile = dS K, which the softmax warps add into an
+// fp32 dQ buffer with vector atomics.
+//
+// Warp roles: 0-3 softmax / epilogue (TMEM lanes 0-127), 4 TMA producer, 5 MMA issuer.
+#include <cmath>
+
+#include "attention.h"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace zp {
+namespace {
+
+constexpr int kT = 128;          // query / key tile
+constexpr int kD = 64;           // head dim
+constexpr int kTile = kT * kD * 2;  // one [128, 64] bf16 tile = 16 KiB
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// K-major SWIZZLE_128B operand: 128 rows x 64 elements, k16 step = +32 B.
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int k16) {
+  return ptx::smem_desc_sw128(base + k16 * 32, 16, 1024);
+}
+// K-major operand made of two 64-wide K blocks (a [128, 128] tile): k16 steps 0..7.
+__device__ __forceinline__ uint64_t kdesc2(uint32_t base, int k16) {
+  return ptx::smem_desc_sw128(base + (k16 >> 2) * kTile + (k16 & 3) * 32, 16, 1024);
+}
+// MN-major operand whose K index runs over the 128 rows of a tile: k16 step = +2048 B; the
+// MN extent is split into 64-wide chunks kTile apart.
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int k16) {
+  return ptx::smem_desc_sw128(base + k16 * 2048, kTile, 1024);
+}
+
+// Byte offset of element (row r, col k) in a [128, 128] bf16 tile stored as two K-major
+// SWIZZLE_128B [128, 64] blocks. Writes 8 consecutive columns (one 16-byte chunk) per call.
+__device__ __forceinline__ uint32_t p_off(int r, int k) {
+  const int blk = k >> 6, chunk = (k & 63) >> 3;
+  return blk * kTile + r * 128 + ((chunk ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+struct AttnTask {
+  int tile, z;  // tile index (query tile in fwd, key tile in bwd) and z = sample * H + head
+};
+
+// Longest tasks first: forward query tile qt needs qt+1 key tiles; backward key tile kt needs
+// nt-kt query tiles.
+__device__ __forceinline__ AttnTask fwd_task(int t, int nz, int nt) {
+  return {nt - 1 - t / nz, t % nz};
+}
+__device__ __forceinline__ AttnTask bwd_task(int t, int nz) { return {t / nz, t % nz}; }
+
+// ============================================================================ forward
+struct FwdSmem {
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + kTile;           // 2 stages
+  static constexpr int kV = kK + 2 * kTile;       // 2 stages
+  static constexpr int kP = kV + 2 * kTile;       // [128, 128] = 2 tiles
+  static constexpr int kBar = kP + 2 * kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, bf16* __restrict__ out,
+                    float* __restrict__ lse, int seq, int heads, int nz, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmem::kBar);
+  uint64_t* q_full = bar + 0;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;   // [2]
+  uint64_t* kv_empty = bar + 4;  // [2]
+  uint64_t* s_full = bar + 6;
+  uint64_t* s_free = bar + 7;
+  uint64_t* p_full = bar + 8;
+  uint64_t* o_full = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = int(ptx::warp_id());
+  const int lane = threadIdx.x & 31;
+  const int nt = seq / kT;
+  const int ntasks = nt * nz;
+  const int h = heads * kD;
+
+  if (warp == 4 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_qkv);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+    }
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(o_full, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, 256);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_o = tmem + 128;
+
+  if (warp == 4) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0, item = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = fwd_task(t, nz, nt);
+        const int smp = tk.z / heads, head = tk.z % heads;
+        const int row0 = smp * seq;
+        ptx::mbar_wait(q_empty, (item & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(q_full, kTile);
+        ptx::tma_load_4d(sm + FwdSmem::kQ, &map_qkv, q_full, head * kD, row0 + tk.tile * kT, 0, 0);
+        for (int j = 0; j <= tk.tile; ++j) {
+          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&kv_full[stage], 2 * kTile);
+          ptx::tma_load_4d(sm + FwdSmem::kK + stage * kTile, &map_qkv, &kv_full[stage], h + head * kD,
+                           row0 + j * kT, 0, 0);
+          ptx::tma_load_4d(sm + FwdSmem::kV + stage * kTile, &map_qkv, &kv_full[stage], 2 * h + head * kD,
+                           row0 + j * kT, 0, 0);
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, 64, 0, 1);
+      const uint32_t sq = ptx::smem_u32(sm + FwdSmem::kQ);
+      const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
+      int stage = 0;
+      uint32_t phase = 0, item = 0, it = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = fwd_task(t, nz, nt);
+        ptx::mbar_wait(q_full, item & 1);
+        for (int j = 0; j <= tk.tile; ++j, ++it) {
+          ptx::mbar_wait(&kv_full[stage], phase);
+          ptx::mbar_wait(s_free, (it & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t sk = ptx::smem_u32(sm + FwdSmem::kK + stage * kTile);
+          const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + stage * kTile);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_s, k > 0);
+          ptx::umma_commit(s_full);
+          if (j == tk.tile) ptx::umma_commit(q_empty);
+          ptx::mbar_wait(p_full, it & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_o, kdesc2(sp, k), mndesc(sv, k), id_o, k > 0);
+          ptx::umma_commit(o_full);
+          ptx::umma_commit(&kv_empty[stage]);
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {  // -------------------------------------------------------------- softmax warps 0-3
+    const int r = warp * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+    const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+      const AttnTask tk = fwd_task(t, nz, nt);
+      const int smp = tk.z / heads, head = tk.z % heads;
+      float o[kD];
+#pragma unroll
+      for (int i = 0; i < kD; ++i) o[i] = 0.f;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j <= tk.tile; ++j, ++it) {
+        ptx::mbar_wait(s_full, it & 1);
+        ptx::tc_fence_after();
+        float s[kT];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_free);
+        if (j == tk.tile) {  // diagonal tile: key > query is masked
+#pragma unroll
+          for (int i = 0; i < kT; ++i)
+            if (i > r) s[i] = -INFINITY;
+        }
+        float mx = m;
+#pragma unroll
+        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, s[i]);
+        const float alpha = exp2f(m - mx);
+        m = mx;
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < kT; c += 8) {
+          float p[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            p[i] = exp2f(s[c + i] - mx);
+            sum += p[i];
+          }
+          st_shared_v4(sp + p_off(r, c), pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
+                       pack_bf16(p[6], p[7]));
+        }
+        l = l * alpha + sum;
+        fence_proxy_async();
+        ptx::mbar_arrive(p_full);
+#pragma unroll
+        for (int i = 0; i < kD; ++i) o[i] *= alpha;
+        ptx::mbar_wait(o_full, it & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
+        }
+        ptx::tc_fence_before();
+      }
+      // epilogue: O / l -> bf16 row, natural-log LSE
+      const float inv = 1.f / l;
+      const int64_t row = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
+      bf16* dst = out + row * h + head * kD;
+#pragma unroll
+      for (int c = 0; c < kD; c += 8) {
+        uint4 u;
+        u.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
+        u.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
+        u.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
+        u.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+        *reinterpret_cast<uint4*>(dst + c) = u;
+      }
+      lse[int64_t(tk.z) * seq + int64_t(tk.tile) * kT + r] = (m + log2f(l)) / kLog2e;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 256);
+  }
+}
+
+// ============================================================================ backward
+struct BwdSmem {
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTile;
+  static constexpr int kQ = kV + kTile;     // 2 stages
+  static constexpr int kDO = kQ + 2 * kTile;  // 2 stages
+  static constexpr int kP = kDO + 2 * kTile;  // [128, 128]
+  static constexpr int kDS = kP + 2 * kTile;  // [128, 128]
+  static constexpr int kBar = kDS + 2 * kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                    const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
+                    bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::kBar);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* kv_empty = bar + 1;
+  uint64_t* qd_full = bar + 2;   // [2]
+  uint64_t* qd_empty = bar + 4;  // [2]
+  uint64_t* sp_full = bar + 6;
+  uint64_t* s_free = bar + 7;
+  uint64_t* ps_full = bar + 8;
+  uint64_t* mm_done = bar + 9;
+  uint64_t* acc_free = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = int(ptx::warp_id());
+  const int lane = threadIdx.x & 31;
+  const int nt = seq / kT;
+  const int ntasks = nt * nz;
+  const int h = heads * kD;
+  const float scale_log2 = scale * kLog2e;
+
+  if (warp == 4 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_qkv);
+    ptx::tma_prefetch_desc(&map_do);
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qd_full[i], 1);
+      ptx::mbar_init(&qd_empty[i], 1);
+    }
+    ptx::mbar_init(sp_full, 1);
+    ptx::mbar_init(s_free, 128);
+    ptx::mbar_init(ps_full, 128);
+    ptx::mbar_init(mm_done, 1);
+    ptx::mbar_init(acc_free, 128);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
+
+  if (warp == 4) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0, item = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = bwd_task(t, nz);
+        const int smp = tk.z / heads, head = tk.z % heads;
+        const int row0 = smp * seq;
+        ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile);
+        ptx::tma_load_4d(sm + BwdSmem::kK, &map_qkv, kv_full, h + head * kD, row0 + tk.tile * kT, 0, 0);
+        ptx::tma_load_4d(sm + BwdSmem::kV, &map_qkv, kv_full, 2 * h + head * kD, row0 + tk.tile * kT, 0, 0);
+        for (int i = tk.tile; i < nt; ++i) {
+          ptx::mbar_wait(&qd_empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&qd_full[stage], 2 * kTile);
+          ptx::tma_load_4d(sm + BwdSmem::kQ + stage * kTile, &map_qkv, &qd_full[stage], head * kD,
+                           row0 + i * kT, 0, 0);
+          ptx::tma_load_4d(sm + BwdSmem::kDO + stage * kTile, &map_do, &qd_full[stage], head * kD,
+                           row0 + i * kT, 0, 0);
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
+      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dV, dK (A^T, B MN-major)
+      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dQ
+      const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK);
+      const uint32_t sv = ptx::smem_u32(sm + BwdSmem::kV);
+      const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
+      const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
+      int stage = 0;
+      uint32_t phase = 0, item = 0, it = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = bwd_task(t, nz);
+        ptx::mbar_wait(kv_full, item & 1);
+        ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // epilogue of the previous task read dK/dV
+        for (int i = tk.tile; i < nt; ++i, ++it) {
+          ptx::mbar_wait(&qd_full[stage], phase);
+          ptx::mbar_wait(s_free, (it & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + stage * kTile);
+          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + stage * kTile);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
+          ptx::umma_commit(sp_full);
+          ptx::mbar_wait(ps_full, it & 1);
+          ptx::tc_fence_after();
+          const bool first = (i == tk.tile);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dv, mndesc(spp, k), mndesc(sdo, k), id_t, (!first || k > 0));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dk, mndesc(sds, k), mndesc(sq, k), id_t, (!first || k > 0));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dq, kdesc2(sds, k), mndesc(sk, k), id_q, k > 0);
+          ptx::umma_commit(mm_done);
+          ptx::umma_commit(&qd_empty[stage]);
+          if (i == nt - 1) ptx::umma_commit(kv_empty);
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {  // -------------------------------------------------------------- softmax warps 0-3
+    const int r = warp * 32 + lane;
+    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+    const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
+    const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+      const AttnTask tk = bwd_task(t, nz);
+      const int smp = tk.z / heads, head = tk.z % heads;
+      for (int i = tk.tile; i < nt; ++i, ++it) {
+        const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
+        const float lse2 = lse[qrow] * kLog2e;
+        const float dd = dvec[qrow];
+        ptx::mbar_wait(sp_full, it & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t vs[32], vp[32];
+          ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, vs);
+          ptx::tmem_ld_32x32b_x32(t_dp + lane_off + c * 32, vp);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int g = 0; g < 32; g += 8) {
+            float p[8], ds[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int key = c * 32 + g + e;
+              const bool masked = (i == tk.tile) && (key > r);
+              const float pv = masked ? 0.f : exp2f(__uint_as_float(vs[g + e]) * scale_log2 - lse2);
+              p[e] = pv;
+              ds[e] = pv * (__uint_as_float(vp[g + e]) - dd) * scale;
+            }
+            const uint32_t off = p_off(r, c * 32 + g);
+            st_shared_v4(spp + off, pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
+                         pack_bf16(p[6], p[7]));
+            st_shared_v4(sds + off, pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
+                         pack_bf16(ds[6], ds[7]));
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_free);
+        fence_proxy_async();
+        ptx::mbar_arrive(ps_full);
+        ptx::mbar_wait(mm_done, it & 1);
+        ptx::tc_fence_after();
+        // dQ tile (128 x 64) += into the fp32 dQ buffer
+        float* dq = dq32 + (int64_t(smp) * seq + int64_t(i) * kT + r) * h + head * kD;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(t_dq + lane_off + c * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            atomicAdd(reinterpret_cast<float4*>(dq + c * 32 + e),
+                      make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                                  __uint_as_float(v[e + 3])));
+        }
+        ptx::tc_fence_before();
+      }
+      // epilogue: dK, dV rows of this key tile -> bf16 into dqkv
+      const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        bf16* dst = dqkv + krow * 3 * h + (which == 0 ? h : 2 * h) + head * kD;
+        const uint32_t src = (which == 0 ? t_dk : t_dv) + lane_off;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(src + c * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+            u.y = pack_bf16(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+            u.z = pack_bf16(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
+            u.w = pack_bf16(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+            *reinterpret_cast<uint4*>(dst + c * 32 + e) = u;
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(acc_free);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// D[z, q] = sum_d dO[q, head*64 + d] * O[q, head*64 + d]  (one warp per (token, head))
+__global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __restrict__ O, float* __restrict__ dvec,
+                                 int64_t tokens, int seq, int heads) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  const int h = heads * kD;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; w < tokens * heads; w += warps) {
+    const int64_t tok = w / heads;
+    const int head = int(w % heads);
+    const int64_t off = tok * h + head * kD + lane * 2;
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dO + off));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(O + off));
+    float v = a.x * b.x + a.y * b.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      const int64_t smp = tok / seq;
+      const int q = int(tok % seq);
+      dvec[(smp * heads + head) * seq + q] = v;
+    }
+  }
+}
+
+// dqkv[:, 0:h] (bf16, row stride 3h) = dq32 [T, h]
+__global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __restrict__ dqkv, int64_t tokens, int h) {
+  const int64_t n4 = tokens * h / 4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = i * 4;
+    const int64_t tok = e / h;
+    const int col = int(e % h);
+    const float4 v = reinterpret_cast<const float4*>(dq32)[i];
+    uint2 o;
+    o.x = pack_bf16(v.x, v.y);
+    o.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(dqkv + tok * 3 * h + col) = o;
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a row-major [rows, cols] bf16 matrix, box = 64 columns x 128 rows, SWIZZLE_128B.
+bool map_rows(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {cuuint64_t(cols), cuuint64_t(rows), 1, 1};
+  cuuint64_t strides[3] = {cuuint64_t(cols * 2), cuuint64_t(rows * cols * 2), cuuint64_t(rows * cols * 2)};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int device_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+}  // namespace
+
+cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
+                          int ctas, cudaStream_t s) {
+  if (seq % kT || batch < 1) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         FwdSmem::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap m;
+  const int h = heads * kD;
+  if (!map_rows(&m, qkv, batch * seq, 3 * h)) return cudaErrorInvalidValue;
+  const int nz = int(batch) * heads;
+  const int ntasks = (seq / kT) * nz;
+  int grid = std::min(ntasks, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
+  const float scale_log2 = (1.0f / std::sqrt(float(kD))) * kLog2e;
+  attn_fwd_kernel<<<grid, kThreads, FwdSmem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
+                          float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s) {
+  if (seq % kT || batch < 1) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         BwdSmem::kBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int h = heads * kD;
+  const int64_t T = batch * seq;
+  CUtensorMap mq, md;
+  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
+  const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
+  attn_dvec_kernel<<<std::min<int64_t>(cap * 4, (T * heads + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
+  note_launch();
+  cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
+  if (e != cudaSuccess) return e;
+  const int nz = int(batch) * heads;
+  const int ntasks = (seq / kT) * nz;
+  attn_bwd_kernel<<<std::min(ntasks, cap), kThreads, BwdSmem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
+                                                                          heads, nz, 1.0f / std::sqrt(float(kD)));
+  note_launch();
+  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace zp

@@ -1,5 +1,6 @@
 // extern "C" wrappers of the individual kernels (include/zp_kernels.h).
 #include "../../../include/zp_kernels.h"
+#include "attention.h"
 #include "gemm.h"
 #include "kernels.h"
 
@@ -23,3 +24,20 @@ extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
 }
 
 extern "C" int64_t zp_launch_count(void) { return zp::launch_count(); }
+
+extern "C" int zp_attention_fwd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq,
+                                int32_t heads, int32_t max_ctas, void* stream) {
+  const cudaError_t e = zp::attention_fwd(static_cast<const zp::bf16*>(qkv), static_cast<zp::bf16*>(out), lse,
+                                          batch, seq, heads, max_ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : 5;
+}
+
+extern "C" int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                                float* dvec, float* dq32, void* dqkv, int64_t batch, int32_t seq,
+                                int32_t heads, int32_t max_ctas, void* stream) {
+  const cudaError_t e = zp::attention_bwd(static_cast<const zp::bf16*>(qkv), static_cast<const zp::bf16*>(out),
+                                          static_cast<const zp::bf16*>(dout), lse, dvec, dq32,
+                                          static_cast<zp::bf16*>(dqkv), batch, seq, heads, max_ctas,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : 5;
+}

@@ -60,6 +60,7 @@ _SIGS = {
     "zp_runtime_get_params_bf16": ([_P, _P], C.c_int),
     "zp_runtime_set_params": ([_P, _P], C.c_int),
     "zp_runtime_keep_grads": ([_P, C.c_int32], C.c_int),
+    "zp_runtime_owned_ranges": ([_P, C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_tensor_info": ([_P, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)], C.c_int),
     "zp_runtime_sync": ([_P], C.c_int),
@@ -208,6 +209,23 @@ class Runtime:
         b, e = C.c_int64(), C.c_int64()
         _check(lib.zp_runtime_get_state(self.h, kind, out.ctypes.data, C.byref(b), C.byref(e)))
         return b.value, e.value, out[: e.value - b.value].copy()
+
+    def owned_ranges(self):
+        """[(flat_begin, flat_end, shard_begin)] of the state this rank holds."""
+        buf = (C.c_int64 * (3 * 1024))()
+        cnt = C.c_int32()
+        _check(lib.zp_runtime_owned_ranges(self.h, buf, 1024, C.byref(cnt)))
+        return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(cnt.value)]
+
+    def state_flat(self, kind: int):
+        """State `kind` scattered into the flat layout: (values, mask of owned elements)."""
+        _, _, shard = self.get_state(kind)
+        flat = np.zeros(self.padded_params, dtype=np.float32)
+        mask = np.zeros(self.padded_params, dtype=bool)
+        for fb, fe, sb in self.owned_ranges():
+            flat[fb:fe] = shard[sb:sb + (fe - fb)]
+            mask[fb:fe] = True
+        return flat, mask
 
     def params_bf16(self) -> np.ndarray:
         out = np.zeros(self.padded_params, dtype=np.uint16)

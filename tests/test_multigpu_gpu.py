@@ -30,29 +30,30 @@ def _worker(rank, world, q_in, q_out, stage, plan, tokens):
                      sm_budget=[148, 74][rank % 2], seed=11, lr=1e-3)
         rt.keep_grads(True)
         rt.resident_bytes(stage)
-        p16 = bf16_to_f32(rt.params_bf16()) if rank == 0 else None
+        m0, mask0 = rt.state_flat(0)  # master == bf16 weights at initialisation
         first = sum(d["gmbs"] for d in plan["devices"][:rank])
         cnt = plan["devices"][rank]["gmbs"]
         rt.load_tokens(tokens[first:first + max(cnt, 1)])
         t = rt.execute_iteration(plan, stage)
-        b, e, g = rt.get_state(3)
-        after = rt.params_bf16()
-        q_out.put((rank, "ok", b, e, g, p16, after, t["loss_sum"], len(t["coll_times"])))
+        g, mask = rt.state_flat(3)
+        after = rt.state_flat(0)[0] if stage == 3 else rt.params_bf16()
+        layout = {n: rt.tensor_info(n) for n in rt.tensor_names()}  # offsets depend on world size
+        q_out.put((rank, "ok", mask, layout, g, (m0, mask0), after, t["loss_sum"], len(t["coll_times"])))
         rt.close()
     except Exception as ex:  # pragma: no cover
         import traceback
         q_out.put((rank, traceback.format_exc(), None, None, None, None, None, None, None))
 
 
-@pytest.mark.parametrize("stage", [0, 1, 2])
+@pytest.mark.parametrize("stage", [0, 1, 2, 3])
 def test_two_rank_hetero_step_matches_oracle(stage):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     import torch.multiprocessing as mp
     from oracle import step as so
-    if stage == 2:
-        plan = _plan(2, [dict(device_id=0, b=3, gmbs=5, lbs=2, predicted_time=0.0),
+    if stage >= 2:
+        plan = _plan(stage, [dict(device_id=0, b=3, gmbs=5, lbs=2, predicted_time=0.0),
                          dict(device_id=1, b=1, gmbs=2, lbs=1, predicted_time=0.0)], gas=2)
     else:
         plan = _plan(stage, [dict(device_id=0, b=3, gmbs=5, lbs=2, predicted_time=0.0),
@@ -68,16 +69,17 @@ def test_two_rank_hetero_step_matches_oracle(stage):
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), [r[1] for r in res]
-    # summed gradient: full on every rank (Z0) or the rank's shard (Z1/2)
+    # summed gradient: full on every rank (Z0) or the ranks' owned slices (Z1-3)
     if stage == 0:
         g = res[0][4]
         assert np.array_equal(res[0][4], res[1][4])
     else:
-        g = np.concatenate([res[0][4], res[1][4]])
-        assert res[0][3] == res[1][2]
-    p16 = res[0][5]
+        assert not np.any(res[0][2] & res[1][2])
+        g = np.where(res[0][2], res[0][4], res[1][4])
+    (m0a, k0a), (m0b, k0b) = res[0][5], res[1][5]
+    p16 = np.where(k0a, m0a, m0b)
     # oracle on the union of the samples
-    names = _names()
+    names = res[0][3]
     P = _unflat(p16, names)
     loss, G = so.gpt_loss_and_grads({k: v.astype(np.float64) for k, v in P.items()}, tokens, TINY["n_layer"],
                                     TINY["n_head"], TINY["vocab"], B)
@@ -85,21 +87,9 @@ def test_two_rank_hetero_step_matches_oracle(stage):
     worst = max((so.rel_err(Gg[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
     assert worst[0] < 2e-2, worst
     assert abs(res[0][7] + res[1][7] - loss) <= 1e-2 * abs(loss)
-    # all ranks end the iteration with identical bf16 parameters
-    assert np.array_equal(res[0][6], res[1][6])
-
-
-_LAYOUT = None
-
-
-def _names():
-    global _LAYOUT
-    if _LAYOUT is None:
-        from paper_2408_12596_b200.runtime import Runtime, GPT
-        rt = Runtime(GPT(**TINY), world_size=1, device=0, hbm_cap_bytes=1 << 30)
-        _LAYOUT = {n: rt.tensor_info(n) for n in rt.tensor_names()}
-        rt.close()
-    return _LAYOUT
+    # all ranks end the iteration with identical bf16 parameters (Z0-2, gathered)
+    if stage < 3:
+        assert np.array_equal(res[0][6], res[1][6])
 
 
 def _unflat(flat, layout):

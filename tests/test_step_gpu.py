@@ -39,7 +39,7 @@ def tokens_for(B, seed=0):
 
 
 @pytest.mark.parametrize("stage,b,lbs,gas", [(0, 4, 4, 1), (0, 3, 1, 2), (1, 2, 2, 2), (2, 4, 4, 1),
-                                             (2, 3, 1, 2)])
+                                             (2, 3, 1, 2), (3, 4, 4, 1), (3, 2, 1, 3)])
 def test_step_matches_fp64_oracle(cuda, stage, b, lbs, gas):
     from paper_2408_12596_b200.runtime import bf16_to_f32
     from oracle import step as so
@@ -47,18 +47,18 @@ def test_step_matches_fp64_oracle(cuda, stage, b, lbs, gas):
     rt = runtime(cuda)
     rt.resident_bytes(stage)  # configure the stage (initialises parameters)
     P16 = bf16_to_f32(rt.params_bf16())
-    _, _, master0 = rt.get_state(0)
+    master0, _ = rt.state_flat(0)
     tok = tokens_for(B)
     rt.load_tokens(tok)
     t = rt.execute_iteration(make_plan(stage, B, b, lbs, gas), stage)
     loss, G = oracle_grads(rt, P16, tok, B)
     assert abs(t["loss_sum"] - loss) <= 1e-2 * abs(loss)
-    _, _, g = rt.get_state(3)
+    g, _ = rt.state_flat(3)
     Gg = rt.unflatten(g)
     worst = max((so.rel_err(Gg[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
     assert worst[0] < 2e-2, worst
     # AdamW update kernel (fp32 path): same gradient in, rel 1e-5 out.
-    _, _, master1 = rt.get_state(0)
+    master1, _ = rt.state_flat(0)
     ref, _, _ = so.adamw(master0.astype(np.float64), 0.0, 0.0, g.astype(np.float64), 1, 1e-3, 0.9, 0.95, 1e-8, 0.0)
     assert so.rel_err(master1, ref) < 1e-5
     # parameters against the oracle's own gradient (bf16 path)
@@ -82,15 +82,15 @@ def test_plans_are_equivalent(cuda):
     B = 8
     tok = tokens_for(B, seed=5)
     grads = []
-    for stage, b, lbs, gas in ((0, 8, 8, 1), (0, 3, 2, 3), (2, 5, 3, 2)):
+    for stage, b, lbs, gas in ((0, 8, 8, 1), (0, 3, 2, 3), (2, 5, 3, 2), (3, 3, 2, 3)):
         rt = runtime(cuda, seed=9)
         rt.resident_bytes(stage)
         rt.load_tokens(tok)
         rt.execute_iteration(make_plan(stage, B, b, lbs, gas), stage)
-        grads.append(rt.get_state(3)[2])
+        grads.append(rt.state_flat(3)[0])
         rt.close()
-    assert so.rel_err(grads[1], grads[0]) < 1e-2
-    assert so.rel_err(grads[2], grads[0]) < 1e-2
+    for g in grads[1:]:
+        assert so.rel_err(g, grads[0]) < 1e-2
 
 
 def test_memory_probe_and_oom(cuda):
