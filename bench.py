@@ -41,8 +41,8 @@ CONFIGS = {
                label="C1: GPT-tiny L4 h256 V8192 s256, ZeRO-1, SM 148 vs 74"),
     "c2": dict(model="gpt2-small", stage=2, tiers=[132, 66], caps=[0], gbs_per_gpu=512,
                label="C2: GPT-2 small (124M) s1024, ZeRO-2, SM budgets 132 vs 66"),
-    "c3": dict(model="gpt2-medium", stage=2, tiers=[148, 74], caps=[0, 80], gbs_per_gpu=256,
-               label="C3-shape: GPT-2 medium (355M) s1024, ZeRO-2, 2 SM tiers x HBM caps 180/80 GB"),
+    "c3": dict(model="gpt2-medium", stage=3, tiers=[148, 148, 74, 74], caps=[0, 80], gbs_per_gpu=256,
+               label="C3: GPT-2 medium (355M) s1024, ZeRO-3, 2 SM tiers (148/74) x 2 HBM caps (180/80 GB)"),
 }
 
 

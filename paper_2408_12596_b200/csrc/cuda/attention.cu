@@ -33,9 +33,6 @@ constexpr float kLog2e = 1.4426950408889634f;
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 // K-major SWIZZLE_128B operand: 128 rows x 64 elements, k16 step = +32 B.
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int k16) {

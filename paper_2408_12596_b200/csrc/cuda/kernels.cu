@@ -1,4 +1,4 @@
-// HBM-bound kernels: embedding, LayerNorm, causal softmax, cross-entropy, reductions,
+// HBM-bound kernels: embedding, LayerNorm, cross-entropy, reductions,
 // and the ZeRO accumulate / AdamW update. 16-byte vector accesses, warp-shuffle
 // reductions, grid-stride loops capped at the rank's CTA budget.
 #include <atomic>
@@ -250,51 +250,6 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy
   for (int i = threadIdx.x; i < h; i += kThreads) {
     part[int64_t(blockIdx.x) * h + i] = sg[i];
     part[int64_t(gridDim.x + blockIdx.x) * h + i] = sb[i];
-  }
-}
-
-// ------------------------------------------------------------------ causal softmax
-
-// Row r of S (fp32, row length seq) is query q = r % seq; keys 0..q are valid. P gets zeros in
-// (q, kend) with kend = the end of q's 128-row tile, the K range the P*V GEMM reduces over.
-__global__ void softmax_fwd_k(const float* S, bf16* P, int64_t rows, int seq) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
-  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
-    const int q = int(r % seq);
-    const float* s = S + r * seq;
-    bf16* p = P + r * seq;
-    const int nvalid = q + 1;
-    const int kend = min(seq, (q / 128 + 1) * 128);
-    float mx = -INFINITY;
-    for (int k = lane; k < nvalid; k += 32) mx = fmaxf(mx, s[k]);
-    mx = warp_max(mx);
-    float sum = 0.f;
-    for (int k = lane; k < nvalid; k += 32) sum += __expf(s[k] - mx);
-    const float inv = 1.0f / warp_sum(sum);
-    for (int k = lane; k < kend; k += 32)
-      p[k] = __float2bfloat16_rn(k < nvalid ? __expf(s[k] - mx) * inv : 0.f);
-  }
-}
-
-__global__ void softmax_bwd_k(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows,
-                              int seq) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
-  for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
-    const int q = int(r % seq);
-    const bf16* p = P + r * seq;
-    const float* dp = dP + r * seq;
-    bf16* ds = dS + r * seq;
-    const int nvalid = q + 1;
-    const int kend = min(seq, (q / 128 + 1) * 128);
-    float dot = 0.f;
-    for (int k = lane; k < nvalid; k += 32) dot += __bfloat162float(p[k]) * dp[k];
-    dot = warp_sum(dot);
-    for (int k = lane; k < kend; k += 32) {
-      const float v = k < nvalid ? scale * __bfloat162float(p[k]) * (dp[k] - dot) : 0.f;
-      ds[k] = __float2bfloat16_rn(v);
-    }
   }
 }
 
@@ -559,14 +514,6 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
   }
 }
 
-void softmax_causal_fwd(const float* S, bf16* P, int64_t rows, int seq, int ctas, cudaStream_t s) {
-  softmax_fwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(S, P, rows, seq); note_launch();
-}
-void softmax_causal_bwd(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows, int seq,
-                        int ctas, cudaStream_t s) {
-  softmax_bwd_k<<<grid_for(rows, kThreads / 32, ctas, 8), kThreads, 0, s>>>(P, dP, dS, scale, rows,
-                                                                            seq); note_launch();
-}
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
                            int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s) {
   ce_k<<<grid_for(rows, 1, ctas, 8), kThreads, 0, s>>>(logits, tokens, seq, rows, vocab, ldv,

@@ -26,7 +26,6 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
                int64_t rows, int h, int ctas, cudaStream_t s);
 cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean,
                           float* rstd, int64_t rows, int h, int ctas, cudaStream_t s);
-void softmax_causal_fwd(const float* S, bf16* P, int64_t rows, int seq, int ctas, cudaStream_t s);
 // per-row CE on bf16 logits [rows, ldv] (first `vocab` columns valid); overwrites logits with
 // dlogits * grad_scale, writes per-row loss.
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
@@ -37,8 +36,6 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
                           int64_t rows, int h, int ctas, cudaStream_t s);
-void softmax_causal_bwd(const bf16* P, const float* dP, bf16* dS, float scale, int64_t rows, int seq,
-                        int ctas, cudaStream_t s);
 void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
                int64_t rows, int h, int ctas, cudaStream_t s);
 // out[n] = sum over rows of X[r, n] (X bf16 [rows, ld]); partial workspace [chunks][N] f32.

@@ -24,6 +24,7 @@
 
 #include "../../../include/zp_runtime.h"
 #include "profiler_search.hpp"
+#include "attention.h"
 #include "gemm.h"
 #include "kernels.h"
 
@@ -156,16 +157,16 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
 
 // ------------------------------------------------------------------ activations of one micro-step
 struct LayerActs {
-  bf16 *x_in, *ln1, *qkv, *P, *attn, *x_mid, *ln2, *u, *g;
-  float *mu1, *rs1, *mu2, *rs2;
+  bf16 *x_in, *ln1, *qkv, *attn, *x_mid, *ln2, *u, *g;
+  float *mu1, *rs1, *mu2, *rs2, *lse;
 };
 struct Acts {
   int64_t b = 0;
   std::vector<LayerActs> l;
   bf16 *x_final, *lnf, *logits;
   float *muf, *rsf, *row_loss;
-  float* S;  // [b, H, s, s] fp32: attention scores, reused for dP
-  bf16* dS;  // [b, H, s, s]
+  float* dvec;  // [b, H, s] rowsum(dO * O)
+  float* dq32;  // [T, h] fp32 dQ accumulator of the fused attention backward
   bf16 *dx, *dx2, *dln, *dO, *dqkv, *du;
 };
 
@@ -318,19 +319,6 @@ struct Runtime {
     g.split_k = split_k;
     launch_gemm(g, 2.0 * M * double(N) * K);
   }
-  // Per-(head, sample) attention GEMM over s x s / s x 64 blocks.
-  void mm_heads(int M, int N, int K, int64_t b, const bf16* A, int amaj, int64_t lda, int64_t a1,
-                int64_t a2, const bf16* B, int bmaj, int64_t ldb, int64_t b1, int64_t b2, void* C,
-                int64_t ldc, int64_t c1, int64_t c2, int epi, float alpha, int causal) {
-    GemmArgs g;
-    g.M = M; g.N = N; g.K = K; g.nb1 = c.n_head; g.nb2 = int(b);
-    g.a.ptr = A; g.a.major = amaj; g.a.ld = lda; g.a.bs1 = a1; g.a.bs2 = a2;
-    g.b.ptr = B; g.b.major = bmaj; g.b.ld = ldb; g.b.bs1 = b1; g.b.bs2 = b2;
-    g.c = C; g.ldc = ldc; g.cs1 = c1; g.cs2 = c2;
-    g.alpha = alpha; g.epilogue = epi; g.causal = causal;
-    g.max_ctas = ctas;
-    launch_gemm(g, 0.0);
-  }
   // Weight gradient dW[M, N] = sum over the T tokens: few output tiles, very long K. Split K
   // across CTAs (fp32 atomics into a workspace, then a cast) when the tiles cannot fill the
   // rank's SMs.
@@ -374,7 +362,6 @@ struct Runtime {
       L.x_in = B16(T * h);
       L.ln1 = B16(T * h);
       L.qkv = B16(T * 3 * h);
-      L.P = B16(b * H * s * s);
       L.attn = B16(T * h);
       L.x_mid = B16(T * h);
       L.ln2 = B16(T * h);
@@ -384,6 +371,7 @@ struct Runtime {
       L.rs1 = F32(T);
       L.mu2 = F32(T);
       L.rs2 = F32(T);
+      L.lse = F32(b * H * s);
     }
     A.x_final = B16(T * h);
     A.lnf = B16(T * h);
@@ -391,8 +379,8 @@ struct Runtime {
     A.rsf = F32(T);
     A.logits = B16(T * vocab_pad);
     A.row_loss = F32(T);
-    A.S = F32(b * H * s * s);
-    A.dS = B16(b * H * s * s);
+    A.dvec = F32(b * H * s);
+    A.dq32 = F32(T * h);
     A.dx = B16(T * h);
     A.dx2 = B16(T * h);
     A.dln = B16(T * h);
@@ -555,7 +543,6 @@ struct Runtime {
   // ---------------------------------------------------------------- forward / backward
   void forward(Acts& A, const int32_t* tok, bool with_loss, float grad_scale) {
     const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
-    const float scale = 1.0f / std::sqrt(float(h / H));
     const int NG = int(lay.groups.size());
     z3_gather(0, kAgF);
     embed_fwd(tok, int(s), Wp(lay.wte), Wp(lay.wpe), A.l[0].x_in, T, int(h), ctas, st);
@@ -567,11 +554,7 @@ struct Runtime {
       CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), Wp(P.ln1_b), L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
       mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiBiasBf16, 1.f,
          Wp(P.b_qkv));
-      mm_heads(s, s, h / H, b, L.qkv, kKMajor, 3 * h, h / H, s * 3 * h, L.qkv + h, kKMajor, 3 * h, h / H,
-               s * 3 * h, A.S, s, s * s, H * s * s, kEpiStoreF32, scale, kCausalSkipUpper);
-      softmax_causal_fwd(A.S, L.P, b * H * s, int(s), ctas, st);
-      mm_heads(s, h / H, s, b, L.P, kKMajor, s, s * s, H * s * s, L.qkv + 2 * h, kMNMajor, 3 * h, h / H,
-               s * 3 * h, L.attn, h, h / H, s * h, kEpiStoreBf16, 1.f, kCausalKUpper);
+      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st));
       mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f,
          Wp(P.b_o), L.x_in);
       CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), Wp(P.ln2_b), L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
@@ -595,8 +578,7 @@ struct Runtime {
   }
 
   void backward(Acts& A, const int32_t* tok) {
-    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s, dh = h / H;
-    const float scale = 1.0f / std::sqrt(float(dh));
+    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
     int nblk = 0;
     const int NG = int(lay.groups.size());
     z3_clear_group(NG - 1);
@@ -626,16 +608,8 @@ struct Runtime {
       colsum_bf16(A.dx2, T, int(h), int(h), col_work, Gp(P.b_o), ctas, st);
       wgrad(h, h, T, A.dx2, h, L.attn, h, Gp(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
-      // attention core, per (head, sample)
-      mm_heads(s, s, dh, b, A.dO, kKMajor, h, dh, s * h, L.qkv + 2 * h, kKMajor, 3 * h, dh, s * 3 * h, A.S, s,
-               s * s, H * s * s, kEpiStoreF32, 1.f, kCausalSkipUpper);
-      softmax_causal_bwd(L.P, A.S, A.dS, scale, b * H * s, int(s), ctas, st);
-      mm_heads(s, dh, s, b, L.P, kMNMajor, s, s * s, H * s * s, A.dO, kMNMajor, h, dh, s * h, A.dqkv + 2 * h,
-               3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
-      mm_heads(s, dh, s, b, A.dS, kKMajor, s, s * s, H * s * s, L.qkv + h, kMNMajor, 3 * h, dh, s * 3 * h,
-               A.dqkv, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKUpper);
-      mm_heads(s, dh, s, b, A.dS, kMNMajor, s, s * s, H * s * s, L.qkv, kMNMajor, 3 * h, dh, s * 3 * h,
-               A.dqkv + h, 3 * h, dh, s * 3 * h, kEpiStoreBf16, 1.f, kCausalKLower);
+      // fused attention backward (recomputes P from the saved LSE)
+      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st));
       // QKV projection
       colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, Gp(P.b_qkv), ctas, st);
       wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
