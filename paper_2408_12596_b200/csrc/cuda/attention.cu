@@ -502,25 +502,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// D[z, q] = sum_d dO[q, head*64 + d] * O[q, head*64 + d]  (one warp per (token, head))
+// D[z, q] = sum_d dO[q, head*64 + d] * O[q, head*64 + d]. One warp per token row: lane l reads
+// 16-byte chunks l, l+32, ... (8 lanes per head per pass), reduced over groups of 8 lanes.
 __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __restrict__ O, float* __restrict__ dvec,
                                  int64_t tokens, int seq, int heads) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
   const int h = heads * kD;
-  for (int64_t w = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; w < tokens * heads; w += warps) {
-    const int64_t tok = w / heads;
-    const int head = int(w % heads);
-    const int64_t off = tok * h + head * kD + lane * 2;
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dO + off));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(O + off));
-    float v = a.x * b.x + a.y * b.y;
+  const int passes = h / 256;
+  for (int64_t tok = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; tok < tokens; tok += warps) {
+    const int64_t smp = tok / seq;
+    const int q = int(tok % seq);
+    for (int k = 0; k < passes; ++k) {
+      const int chunk = lane + 32 * k;
+      const uint4 a = *reinterpret_cast<const uint4*>(dO + tok * h + chunk * 8);
+      const uint4 b = *reinterpret_cast<const uint4*>(O + tok * h + chunk * 8);
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+      float v = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) {
-      const int64_t smp = tok / seq;
-      const int q = int(tok % seq);
-      dvec[(smp * heads + head) * seq + q] = v;
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(b2[e]);
+        v += x.x * y.x + x.y * y.y;
+      }
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      if ((lane & 7) == 0) {
+        const int head = chunk / 8;
+        dvec[(smp * heads + head) * seq + q] = v;
+      }
     }
   }
 }
@@ -618,7 +629,8 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   CUtensorMap mq, md;
   if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
-  attn_dvec_kernel<<<std::min<int64_t>(cap * 4, (T * heads + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
+  if (h % 256) return cudaErrorInvalidValue;
+  attn_dvec_kernel<<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
   note_launch();
   cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
   if (e != cudaSuccess) return e;

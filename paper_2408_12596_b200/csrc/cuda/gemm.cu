@@ -20,16 +20,19 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle span of bf16
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // 4 control warps + 8 epilogue warps
+constexpr int kEpiWarps = 8;
+constexpr int kStageBufBytes = 32 * 64 * 2;  // one warp's [32 rows x 64 cols] bf16 TMA-store box
 
 template <int BN>
 struct Cfg {
   static constexpr int kATileBytes = kBM * kBK * 2;
   static constexpr int kBTileBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kEpiBytes = kEpiWarps * 2 * kStageBufBytes;  // double-buffered per warp
+  static constexpr int kStages = (232448 - kEpiBytes - 1024 - 256) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TileInfo {
@@ -84,18 +87,100 @@ struct EpiParams {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* aux;
   __nv_bfloat16* aux_out;
+  int tma_store;  // bf16 output written through swizzled smem boxes + TMA stores
 };
 
+// GELU (tanh form) with the MUFU tanh approximation (rel. error ~2^-11, below bf16 output
+// rounding).
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  const float t = ptx::tanh_approx(k0 * (x + k1 * x * x * x));
   return 0.5f * x * (1.0f + t);
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  const float t = ptx::tanh_approx(k0 * (x + k1 * x * x * x));
   return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+}
+
+// bf16-output epilogue math on 32 consecutive columns [n, n+32) of one row; leaves the final
+// values in v. `valid` = row < M; columns >= N are computed from zeros and clipped by the store.
+__device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32], int64_t off, int n,
+                                              int N, bool valid) {
+  const int e = ep.epilogue;
+  const bool full = valid && (n + 32 <= N);
+  if (e == kEpiStoreBf16) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
+    return;
+  }
+  if (e == kEpiBiasBf16 || e == kEpiBiasResidBf16 || e == kEpiBiasGeluBf16) {
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        const uint4 braw = *reinterpret_cast<const uint4*>(ep.bias + n + i);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 bf = __bfloat1622float2(b2[j]);
+          v[i + 2 * j] += bf.x;
+          v[i + 2 * j + 1] += bf.y;
+        }
+      }
+    } else if (valid) {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] += __bfloat162float(ep.bias[n + i]);
+    }
+    if (e == kEpiBiasResidBf16) {
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 rraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rraw);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 rf = __bfloat1622float2(r2[j]);
+            v[i + 2 * j] += rf.x;
+            v[i + 2 * j + 1] += rf.y;
+          }
+        }
+      } else if (valid) {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] += __bfloat162float(ep.aux[off + i]);
+      }
+    } else if (e == kEpiBiasGeluBf16) {
+      __nv_bfloat16* u = ep.aux_out + off;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 o;
+          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+          *reinterpret_cast<uint4*>(u + i) = o;
+        }
+      } else if (valid) {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) u[i] = __float2bfloat16_rn(v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+    }
+  } else if (e == kEpiGeluBwdBf16) {
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        const uint4 uraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
+        const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uraw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 uf = __bfloat1622float2(u2[j]);
+          v[i + 2 * j] *= gelu_tanh_grad(uf.x);
+          v[i + 2 * j + 1] *= gelu_tanh_grad(uf.y);
+        }
+      }
+    } else if (valid) {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] *= gelu_tanh_grad(__bfloat162float(ep.aux[off + i]));
+    }
+  }
 }
 
 // Writes 32 consecutive columns [n, n+32) of one row.
@@ -114,7 +199,7 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
         atomicAdd(reinterpret_cast<float4*>(c + i),
                   make_float4(ep.alpha * v[i], ep.alpha * v[i + 1], ep.alpha * v[i + 2], ep.alpha * v[i + 3]));
     } else {
-      for (int i = 0; i < 32 && n + i < N; ++i) atomicAdd(c + i, ep.alpha * v[i]);
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) atomicAdd(c + i, ep.alpha * v[i]);
     }
     return;
   }
@@ -132,84 +217,15 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
         *reinterpret_cast<float4*>(c + i) = o;
       }
     } else {
-      for (int i = 0; i < 32 && n + i < N; ++i) {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) {
         const float o = ep.alpha * v[i];
         c[i] = (e == kEpiAccumF32) ? c[i] + o : o;
       }
     }
     return;
   }
-  // bf16 outputs
-  if (e == kEpiStoreBf16) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] *= ep.alpha;
-  } else if (e == kEpiBiasBf16 || e == kEpiBiasResidBf16 || e == kEpiBiasGeluBf16) {
-    if (full) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        const uint4 braw = *reinterpret_cast<const uint4*>(ep.bias + n + i);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 bf = __bfloat1622float2(b2[j]);
-          v[i + 2 * j] += bf.x;
-          v[i + 2 * j + 1] += bf.y;
-        }
-      }
-    } else {
-      for (int i = 0; i < 32 && n + i < N; ++i) v[i] += __bfloat162float(ep.bias[n + i]);
-    }
-    if (e == kEpiBiasResidBf16) {
-      if (full) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          const uint4 rraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
-          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rraw);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 rf = __bfloat1622float2(r2[j]);
-            v[i + 2 * j] += rf.x;
-            v[i + 2 * j + 1] += rf.y;
-          }
-        }
-      } else {
-        for (int i = 0; i < 32 && n + i < N; ++i) v[i] += __bfloat162float(ep.aux[off + i]);
-      }
-    } else if (e == kEpiBiasGeluBf16) {
-      __nv_bfloat16* u = ep.aux_out + off;
-      if (full) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 o;
-          __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
-          *reinterpret_cast<uint4*>(u + i) = o;
-        }
-      } else {
-        for (int i = 0; i < 32 && n + i < N; ++i) u[i] = __float2bfloat16_rn(v[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-    }
-  } else if (e == kEpiGeluBwdBf16) {
-    if (full) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        const uint4 uraw = *reinterpret_cast<const uint4*>(ep.aux + off + i);
-        const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uraw);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 uf = __bfloat1622float2(u2[j]);
-          v[i + 2 * j] *= gelu_tanh_grad(uf.x);
-          v[i + 2 * j + 1] *= gelu_tanh_grad(uf.y);
-        }
-      }
-    } else {
-      for (int i = 0; i < 32 && n + i < N; ++i)
-        v[i] *= gelu_tanh_grad(__bfloat162float(ep.aux[off + i]));
-    }
-  }
+  // bf16 outputs, direct row stores (batched GEMMs / unaligned outputs)
+  epi_bf16_math(ep, v, off, n, N, true);
   __nv_bfloat16* c = static_cast<__nv_bfloat16*>(ep.c) + off;
   if (full) {
 #pragma unroll
@@ -221,21 +237,25 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
       *reinterpret_cast<uint4*>(c + i) = o;
     }
   } else {
-    for (int i = 0; i < 32 && n + i < N; ++i) c[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (n + i < N) c[i] = __float2bfloat16_rn(v[i]);
   }
 }
 
 template <int BN, int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, Sched sched, EpiParams ep) {
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c, Sched sched, EpiParams ep) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::kStages * C::kATileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* smem_epi = smem + C::kStages * C::kStageBytes;  // [8 warps][2][32 x 64] bf16, SW128
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + C::kEpiBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::kStages;
   uint64_t* tfull = bars + 2 * C::kStages;
@@ -248,13 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
     ptx::tma_prefetch_desc(&map_b);
+    if (ep.tma_store) ptx::tma_prefetch_desc(&map_c);
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 128);
+      ptx::mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     ptx::fence_barrier_init();
   }
@@ -342,8 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue
-    const int q = warp - 4;  // TMEM lane quarter
+    // ------------------------------------------------------------ epilogue (8 warps)
+    // warp w reads TMEM lane quarter w % 4 (rows 32q..32q+31) and column half (w - 4) / 4.
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int cols = BN >= 128 ? BN / 2 : (half == 0 ? BN : 0);
+    const int c_begin = BN >= 128 ? half * (BN / 2) : 0;
+    uint8_t* stage_buf = smem_epi + (warp - 4) * 2 * kStageBufBytes;
+    int buf = 0;
     int local = 0;
     for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
       const TileInfo ti = sched.tile(t);
@@ -352,19 +379,65 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
       const int row = ti.m0 + q * 32 + lane;
+      const bool valid = row < sched.M;
       const int64_t row_off = ti.z1 * ep.cs1 + ti.z2 * ep.cs2 + int64_t(row) * ep.ldc;
+      const uint32_t tbase = tmem_base + acc * BN + (uint32_t(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + c + (uint32_t(q * 32) << 16), r);
-        ptx::tmem_ld_wait();
-        const int n = ti.n0 + c;
-        if (row < sched.M && n < sched.N) epilogue_row32(ep, r, row_off + n, n, sched.N);
+      for (int c = c_begin; c < c_begin + cols && ti.n0 + c < sched.N; c += 64) {
+        if (ep.tma_store) {
+          float v[2][32];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tbase + c + 32 * g, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[g][i] = __uint_as_float(r[i]);
+          }
+#pragma unroll
+          for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + ti.n0 + c + 32 * g, ti.n0 + c + 32 * g,
+                                                    sched.N, valid);
+          // this warp's staging box was last handed to TMA two chunks ago: wait until read
+          if (lane == 0) ptx::bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* sb = stage_buf + buf * kStageBufBytes;
+          const uint32_t srow = ptx::smem_u32(sb) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float* w = &v[j >> 2][(j & 3) * 8];
+            uint32_t p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(w[2 * k], w[2 * k + 1]);
+              p[k] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(srow + ((j ^ (lane & 7)) << 4)),
+                         "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3])
+                         : "memory");
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&map_c, sb, ti.n0 + c, ti.m0 + q * 32);
+            ptx::bulk_commit();
+          }
+          buf ^= 1;
+        } else {
+#pragma unroll 1
+          for (int g = 0; g < 2; ++g) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tbase + c + 32 * g, r);
+            ptx::tmem_ld_wait();
+            const int n = ti.n0 + c + 32 * g;
+            if (valid && n < sched.N) epilogue_row32(ep, r, row_off + n, n, sched.N);
+          }
+        }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       ++local;
     }
+    if (ep.tma_store && lane == 0) ptx::bulk_wait<0>();
   }
 
   ptx::tc_fence_before();
@@ -415,6 +488,20 @@ bool make_map(CUtensorMap* map, const GemmOperand& op, int64_t inner, int64_t ro
   return r == CUDA_SUCCESS;
 }
 
+// Output map: [M rows, N cols] bf16 with row stride ldc; box = 64 cols x 32 rows, SWIZZLE_128B
+// (matches the epilogue warps' staging layout).
+bool make_store_map(CUtensorMap* map, void* c, int64_t M, int64_t N, int64_t ldc) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc || (ldc * 2) % 16) return false;
+  cuuint64_t dims[2] = {cuuint64_t(N), cuuint64_t(M)};
+  cuuint64_t strides[1] = {cuuint64_t(ldc * 2)};
+  cuuint32_t box[2] = {64, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -436,12 +523,19 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   const bool ok_a = A_MN ? make_map(&ma, a.a, a.M, a.K, a.nb1, a.nb2, 64)
                          : make_map(&ma, a.a, a.K, a.M, a.nb1, a.nb2, kBM);
   const bool ok_b = B_MN ? make_map(&mb, a.b, a.N, a.K, a.nb1, a.nb2, 64)
                          : make_map(&mb, a.b, a.K, a.N, a.nb1, a.nb2, BN);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  // bf16 outputs of plain (unbatched) GEMMs go through TMA stores.
+  const bool bf16_out = a.epilogue == kEpiStoreBf16 || a.epilogue == kEpiBiasBf16 ||
+                        a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiBiasGeluBf16 ||
+                        a.epilogue == kEpiGeluBwdBf16;
+  bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
+  if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
+  if (!tma_store) mc = ma;  // unused placeholder
   Sched s;
   s.m_tiles = (a.M + kBM - 1) / kBM;
   s.n_tiles = (a.N + BN - 1) / BN;
@@ -464,11 +558,12 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.bias = static_cast<const __nv_bfloat16*>(a.bias);
   ep.aux = static_cast<const __nv_bfloat16*>(a.aux);
   ep.aux_out = static_cast<__nv_bfloat16*>(a.aux_out);
+  ep.tma_store = tma_store ? 1 : 0;
   int grid = num_sms();
   if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
   if (s.total < grid) grid = s.total;
   if (grid < 1) return cudaSuccess;
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, s, ep);
+  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, s, ep);
   note_launch();
   return cudaGetLastError();
 }

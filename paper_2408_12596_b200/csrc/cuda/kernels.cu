@@ -268,35 +268,56 @@ __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
   return sh[0];
 }
 
-__global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* tok, int seq,
-                                                 int64_t rows, int vocab, int ldv, float gscale,
-                                                 float* row_loss) {
-  __shared__ float sh[32];
+// Combines two (max, sum-of-exp) pairs of an online softmax.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  const float mx = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mx)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mx));
+  m = mx;
+}
+
+// One CTA per row: pass 1 computes the row's max and sum of exp online (one read of the
+// logits), pass 2 overwrites the logits with (softmax - onehot) * gscale.
+__global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* tok, int seq, int64_t rows,
+                                                 int vocab, int ldv, float gscale, float* row_loss) {
+  __shared__ float shm[kThreads / 32], shs[kThreads / 32];
   const int nvec = ldv / 8;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     bf16* lg = logits + r * ldv;
     const int64_t smp = r / seq;
     const int pos = int(r % seq);
     const int target = tok[smp * (seq + 1) + pos + 1];
-    float mx = -INFINITY;
+    float m = -INFINITY, sum = 0.f;
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
+      float cm = -INFINITY;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (i * 8 + k < vocab) mx = fmaxf(mx, f[k]);
-    }
-    mx = block_reduce(mx, sh, true);
-    float sum = 0.f;
-    for (int i = threadIdx.x; i < nvec; i += kThreads) {
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
+        if (i * 8 + k < vocab) cm = fmaxf(cm, f[k]);
+      if (cm == -INFINITY) continue;
+      float cs = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (i * 8 + k < vocab) sum += __expf(f[k] - mx);
+        if (i * 8 + k < vocab) cs += __expf(f[k] - cm);
+      lse_merge(m, sum, cm, cs);
     }
-    sum = block_reduce(sum, sh, false);
-    const float lse = mx + logf(sum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      lse_merge(m, sum, m2, s2);
+    }
+    __syncthreads();
+    if (lane == 0) {
+      shm[w] = m;
+      shs[w] = sum;
+    }
+    __syncthreads();
+    m = shm[0];
+    sum = shs[0];
+    for (int k = 1; k < kThreads / 32; ++k) lse_merge(m, sum, shm[k], shs[k]);
+    const float lse = m + logf(sum);
     const float tl = __bfloat162float(lg[target]);
     __syncthreads();  // everyone has read lg[target] before it is overwritten
     const float inv = 1.0f / sum;
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* to
       for (int k = 0; k < 8; ++k) {
         const int col = i * 8 + k;
         float gv = 0.f;
-        if (col < vocab) gv = (__expf(f[k] - mx) * inv - (col == target ? 1.f : 0.f)) * gscale;
+        if (col < vocab) gv = (__expf(f[k] - m) * inv - (col == target ? 1.f : 0.f)) * gscale;
         f[k] = gv;
       }
       *reinterpret_cast<uint4*>(lg + i * 8) = pack8(f);
@@ -318,33 +339,34 @@ __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* to
 
 // ------------------------------------------------------------------ reductions
 
-// Partial column sums: block (32, 8) covers 64 columns (2 per thread) x one row chunk.
-__global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_t chunk,
-                              float* work) {
-  __shared__ float sh[8][64];
-  const int c = blockIdx.x * 64 + threadIdx.x * 2;
+// Partial column sums: block (32, 8) covers 256 columns (8 per thread, 16-byte loads) x one
+// row chunk; warp rows read 512 contiguous bytes.
+__global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_t chunk, float* work) {
+  __shared__ float sh[8][256];
+  const int c = blockIdx.x * 256 + threadIdx.x * 8;
   const int64_t r0 = blockIdx.y * chunk;
   const int64_t r1 = min(rows, r0 + chunk);
-  float a = 0.f, b = 0.f;
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 0.f;
   if (c < N) {
     for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
-      const float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(X + r * ld + c));
-      a += v.x;
-      b += v.y;
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(X + r * ld + c), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += f[k];
     }
   }
-  sh[threadIdx.y][threadIdx.x * 2] = a;
-  sh[threadIdx.y][threadIdx.x * 2 + 1] = b;
-  __syncthreads();
-  if (threadIdx.y == 0 && c < N) {
-    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      s0 += sh[k][threadIdx.x * 2];
-      s1 += sh[k][threadIdx.x * 2 + 1];
-    }
-    work[int64_t(blockIdx.y) * N + c] = s0;
-    if (c + 1 < N) work[int64_t(blockIdx.y) * N + c + 1] = s1;
+  for (int k = 0; k < 8; ++k) sh[threadIdx.y][threadIdx.x * 8 + k] = a[k];
+  __syncthreads();
+  const int t = threadIdx.y * 32 + threadIdx.x;  // 256 threads, one column each
+  const int col = blockIdx.x * 256 + t;
+  if (col < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += sh[k][t];
+    work[int64_t(blockIdx.y) * N + col] = s;
   }
 }
 
@@ -522,7 +544,7 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
 
 void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* out, int ctas,
                  cudaStream_t s) {
-  const int col_blocks = (N + 63) / 64;
+  const int col_blocks = (N + 255) / 256;
   int chunks = (ctas * 4 + col_blocks - 1) / col_blocks;
   if (chunks < 1) chunks = 1;
   if (chunks > 256) chunks = 256;
