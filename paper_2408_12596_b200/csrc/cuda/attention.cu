@@ -278,6 +278,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ============================================================================ backward
+// Warp roles: 0-7 P/dS builders (TMEM lane quarter w % 4, key half w / 4), 8-11 dQ reducers and
+// dK/dV epilogue (lane quarter w % 4), 12 TMA producer, 13 MMA issuer. The dQ atomics of query
+// tile i overlap the P/dS construction of tile i+1.
+constexpr int kBwdThreads = 448;
+
 struct BwdSmem {
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTile;
@@ -289,7 +294,7 @@ struct BwdSmem {
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                     const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
                     bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale) {
@@ -305,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* ps_full = bar + 8;
   uint64_t* mm_done = bar + 9;
   uint64_t* acc_free = bar + 10;
+  uint64_t* dq_free = bar + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
 
   const int warp = int(ptx::warp_id());
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int h = heads * kD;
   const float scale_log2 = scale * kLog2e;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::tma_prefetch_desc(&map_do);
     ptx::mbar_init(kv_full, 1);
@@ -324,20 +330,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&qd_empty[i], 1);
     }
     ptx::mbar_init(sp_full, 1);
-    ptx::mbar_init(s_free, 128);
-    ptx::mbar_init(ps_full, 128);
+    ptx::mbar_init(s_free, 256);
+    ptx::mbar_init(ps_full, 256);
     ptx::mbar_init(mm_done, 1);
     ptx::mbar_init(acc_free, 128);
+    ptx::mbar_init(dq_free, 128);
     ptx::fence_barrier_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, 512);
+  if (warp == 12) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
 
-  if (warp == 4) {
+  if (warp == 12) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0, item = 0;
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 13) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
       constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dV, dK (A^T, B MN-major)
@@ -390,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
           ptx::umma_commit(sp_full);
           ptx::mbar_wait(ps_full, it & 1);
+          ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
           ptx::tc_fence_after();
           const bool first = (i == tk.tile);
 #pragma unroll
@@ -408,67 +416,82 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {  // -------------------------------------------------------------- softmax warps 0-3
-    const int r = warp * 32 + lane;
-    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+  } else if (warp < 8) {  // ------------------------------------------ P / dS builders
+    const int q4 = warp & 3, kh = warp >> 2;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
     const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
     const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
       const AttnTask tk = bwd_task(t, nz);
-      const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
         const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
         const float lse2 = lse[qrow] * kLog2e;
         const float dd = dvec[qrow];
+        // S/dP(i) complete implies the MMAs of tile i-1 (which read P/dS) completed: in order.
         ptx::mbar_wait(sp_full, it & 1);
         ptx::tc_fence_after();
+        uint32_t vs[2][32], vp[2][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t vs[32], vp[32];
-          ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, vs);
-          ptx::tmem_ld_32x32b_x32(t_dp + lane_off + c * 32, vp);
-          ptx::tmem_ld_wait();
+        for (int c = 0; c < 2; ++c) {
+          ptx::tmem_ld_32x32b_x32(t_s + lane_off + kh * 64 + c * 32, vs[c]);
+          ptx::tmem_ld_32x32b_x32(t_dp + lane_off + kh * 64 + c * 32, vp[c]);
+        }
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_free);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
 #pragma unroll
           for (int g = 0; g < 32; g += 8) {
             float p[8], ds[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int key = c * 32 + g + e;
+              const int key = kh * 64 + c * 32 + g + e;
               const bool masked = (i == tk.tile) && (key > r);
-              const float pv = masked ? 0.f : exp2f(__uint_as_float(vs[g + e]) * scale_log2 - lse2);
+              const float pv = masked ? 0.f : exp2f(__uint_as_float(vs[c][g + e]) * scale_log2 - lse2);
               p[e] = pv;
-              ds[e] = pv * (__uint_as_float(vp[g + e]) - dd) * scale;
+              ds[e] = pv * (__uint_as_float(vp[c][g + e]) - dd) * scale;
             }
-            const uint32_t off = p_off(r, c * 32 + g);
+            const uint32_t off = p_off(r, kh * 64 + c * 32 + g);
             st_shared_v4(spp + off, pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
                          pack_bf16(p[6], p[7]));
             st_shared_v4(sds + off, pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
                          pack_bf16(ds[6], ds[7]));
           }
         }
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(s_free);
         fence_proxy_async();
         ptx::mbar_arrive(ps_full);
+      }
+    }
+  } else {  // --------------------------------------------------------- warps 8-11: dQ + dK/dV out
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+      const AttnTask tk = bwd_task(t, nz);
+      const int smp = tk.z / heads, head = tk.z % heads;
+      for (int i = tk.tile; i < nt; ++i, ++it) {
         ptx::mbar_wait(mm_done, it & 1);
         ptx::tc_fence_after();
-        // dQ tile (128 x 64) += into the fp32 dQ buffer
+        uint32_t v[2][32];
+        ptx::tmem_ld_32x32b_x32(t_dq + lane_off, v[0]);
+        ptx::tmem_ld_32x32b_x32(t_dq + lane_off + 32, v[1]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(dq_free);
         float* dq = dq32 + (int64_t(smp) * seq + int64_t(i) * kT + r) * h + head * kD;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_dq + lane_off + c * 32, v);
-          ptx::tmem_ld_wait();
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             atomicAdd(reinterpret_cast<float4*>(dq + c * 32 + e),
-                      make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                                  __uint_as_float(v[e + 3])));
-        }
-        ptx::tc_fence_before();
+                      make_float4(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1]),
+                                  __uint_as_float(v[c][e + 2]), __uint_as_float(v[c][e + 3])));
       }
-      // epilogue: dK, dV rows of this key tile -> bf16 into dqkv
+      // epilogue: dK, dV rows of this key tile -> bf16 into dqkv (all MMAs of the task are done)
       const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
@@ -496,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 12) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
@@ -509,26 +532,28 @@ __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __rest
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
   const int h = heads * kD;
-  const int passes = h / 256;
+  const int nchunks = h / 8;  // 16-byte chunks per row; 8 chunks per head
   for (int64_t tok = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; tok < tokens; tok += warps) {
     const int64_t smp = tok / seq;
     const int q = int(tok % seq);
-    for (int k = 0; k < passes; ++k) {
+    for (int k = 0; k * 32 < nchunks; ++k) {
       const int chunk = lane + 32 * k;
-      const uint4 a = *reinterpret_cast<const uint4*>(dO + tok * h + chunk * 8);
-      const uint4 b = *reinterpret_cast<const uint4*>(O + tok * h + chunk * 8);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
       float v = 0.f;
+      if (chunk < nchunks) {
+        const uint4 a = *reinterpret_cast<const uint4*>(dO + tok * h + chunk * 8);
+        const uint4 b = *reinterpret_cast<const uint4*>(O + tok * h + chunk * 8);
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(b2[e]);
-        v += x.x * y.x + x.y * y.y;
+        for (int e = 0; e < 4; ++e) {
+          const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(b2[e]);
+          v += x.x * y.x + x.y * y.y;
+        }
       }
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 4);
-      if ((lane & 7) == 0) {
+      if ((lane & 7) == 0 && chunk < nchunks) {
         const int head = chunk / 8;
         dvec[(smp * heads + head) * seq + q] = v;
       }
@@ -629,14 +654,13 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   CUtensorMap mq, md;
   if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
-  if (h % 256) return cudaErrorInvalidValue;
   attn_dvec_kernel<<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
   note_launch();
   cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
   if (e != cudaSuccess) return e;
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
-  attn_bwd_kernel<<<std::min(ntasks, cap), kThreads, BwdSmem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
+  attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
                                                                           heads, nz, 1.0f / std::sqrt(float(kD)));
   note_launch();
   attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h);

@@ -238,15 +238,23 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy
       *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
     }
   }
+  // Fold the 8 warps' column partials into shared memory one warp at a time (plain
+  // read-modify-write, no shared atomics: lanes own disjoint 8-column groups).
+  const int w = threadIdx.x / 32;
+  for (int turn = 0; turn < kThreads / 32; ++turn) {
+    if (w == turn) {
 #pragma unroll
-  for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NC; ++c) {
+        const int col = (c * 32 + lane) * 8;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int col = (c * 32 + lane) * 8 + k;
-      atomicAdd(&sg[col], accg[c][k]);
-      atomicAdd(&sb[col], accb[c][k]);
+        for (int k = 0; k < 8; ++k) {
+          sg[col + k] += accg[c][k];
+          sb[col + k] += accb[c][k];
+        }
+      }
     }
-  __syncthreads();
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < h; i += kThreads) {
     part[int64_t(blockIdx.x) * h + i] = sg[i];
     part[int64_t(gridDim.x + blockIdx.x) * h + i] = sb[i];

@@ -174,11 +174,13 @@ struct Acts {
 enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4, kAgF = 5, kAgB = 6, kRs = 7 };
 struct Span {
   int kind, start, end;
+  bool nested;  // a collective issued inside a forward/backward span (ZeRO-3 gathers / scatters)
 };
 struct Timer {
   std::vector<cudaEvent_t> ev;
   std::vector<Span> spans;
   int next = 0;
+  bool in_compute = false;  // set while a forward/backward span is open
   void init(int n) {
     ev.resize(n);
     for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -196,7 +198,10 @@ struct Timer {
     CK(cudaEventRecord(ev[next], s));
     return next++;
   }
-  void close(int kind, int start, cudaStream_t s) { spans.push_back({kind, start, mark(s)}); }
+  void close(int kind, int start, cudaStream_t s) {
+    const bool coll = kind == kComm || kind == kAgF || kind == kAgB || kind == kRs;
+    spans.push_back({kind, start, mark(s), coll && in_compute});
+  }
 };
 
 }  // namespace
@@ -693,10 +698,14 @@ struct Runtime {
       if (b > 0) {
         const int32_t* tok = tokens + sample * (c.seq_len + 1);
         const int f0 = tm.mark(st);
+        tm.in_compute = true;
         forward(A, tok, true, gscale);
+        tm.in_compute = false;
         tm.close(kFwd, f0, st);
         const int b0 = tm.mark(st);
+        tm.in_compute = true;
         backward(A, tok);
+        tm.in_compute = false;
         tm.close(kBwd, b0, st);
         reduce_sum_f32(A.row_loss, b * c.seq_len, loss_steps + k, st);
         sample += b;
@@ -942,6 +951,15 @@ struct Runtime {
         case kAgF:
         case kAgB:
         case kRs:
+          // Collectives nested in a forward/backward span are not the rank's own compute: on a
+          // fast rank they include the wait for the slowest rank (reference profiler.cpp:25-47
+          // subtracts them; with lockstep ZeRO-3 they would otherwise hide the heterogeneity).
+          if (sp.nested) {
+            if (sp.kind == kAgF)
+              t->forward -= sec;
+            else
+              t->backward -= sec;
+          }
           t->comm += sec;
           if (t->n_collectives < 512) t->coll_times[t->n_collectives++] = sec;
           if (sp.kind == kAgF) t_agf += sec;
