@@ -43,6 +43,11 @@ CONFIGS = {
                label="C2: GPT-2 small (124M) s1024, ZeRO-2, SM budgets 132 vs 66"),
     "c3": dict(model="gpt2-medium", stage=3, tiers=[148, 148, 74, 74], caps=[0, 80], gbs_per_gpu=256,
                label="C3: GPT-2 medium (355M) s1024, ZeRO-3, 2 SM tiers (148/74) x 2 HBM caps (180/80 GB)"),
+    # 5 fast + 3 slow ranks at N=8 (tier list indexed by rank)
+    "c4": dict(model="llama-1.3b", stage=3, tiers=[148, 148, 74, 148, 74, 148, 74, 148], caps=[0],
+               gbs_per_gpu=128, label="C4: Llama-style 1.3B s2048, ZeRO-3 bf16, 5 fast (148 SM) + 3 slow (74 SM)"),
+    "c5": dict(model="llama-7b", stage=3, tiers=[148, 104, 74, 148, 104, 74, 148, 74], caps=[0, 0, 0, 96],
+               gbs_per_gpu=64, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/96 GB"),
 }
 
 
@@ -304,6 +309,17 @@ def main():
     rt.gemm_timing(0)
     g_all = allgather((gflops, gsec, glaunch, tier))
 
+    # HBM-bound update kernel: fused accumulate + AdamW + bf16 cast over this rank's shard, timed
+    # by its CUDA events in the last timed iteration. Bytes per element: p32/m/v read+write (24),
+    # bf16 param write (2), gradient read (bf16 2 at Z2/3 + fp32 accumulator 4 when gas > 1; fp32 4
+    # at Z0/1).
+    shard = rt.padded_params if stage == 0 else rt.padded_params // world
+    steps_r = rank_micro_steps(plan, rank, stage)
+    gbytes = 4 if stage <= 1 else (2 + (4 if steps_r > 1 else 0))
+    adam_bytes = shard * (26 + gbytes)
+    adam_s = last_timing["optimizer"]
+    adam_all = allgather((adam_bytes, adam_s))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sps, cores, dt = cpu_step_sample(cfg["model"])
@@ -338,6 +354,11 @@ def main():
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "peak_note": f"MEASURED_PEAKS bf16 {peaks['bf16_tflops']} x {tr}/148 SM budget",
                          "launches": nl},
+            "roofline_hbm": {"kernel": "adam_k (fused accumulate + AdamW + bf16 cast), rank 0", "bound": "hbm",
+                             "achieved": adam_all[0][0] / adam_all[0][1] / 1e9 if adam_all[0][1] else None,
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": (adam_all[0][0] / adam_all[0][1] / 1e9 / peaks["hbm_gbs"]) if adam_all[0][1] else None,
+                             "bytes_per_launch": adam_all[0][0]},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

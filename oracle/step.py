@@ -134,3 +134,132 @@ def rel_err(a, b):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ----------------------------------------------------------------------------- Llama family
+# RMSNorm (eps 1e-5), rotary Q/K (rotate-half, theta 1e4, head_dim 64), SwiGLU MLP whose fused
+# gate/up weight interleaves 32-row blocks (rows r with r % 64 < 32 are gate rows), no biases,
+# untied LM head. Same global-batch loss normalisation as the GPT step.
+
+def rms_fwd(x, g, eps=1e-5):
+    rs = 1.0 / np.sqrt((x * x).mean(-1, keepdims=True) + eps)
+    xh = x * rs
+    return xh * g, (xh, rs)
+
+
+def rms_bwd(dy, g, cache):
+    xh, rs = cache
+    gd = dy * g
+    m2 = (gd * xh).mean(-1, keepdims=True)
+    return rs * (gd - xh * m2), (dy * xh).sum(0)
+
+
+def rope_tables(s, theta=10000.0):
+    j = np.arange(32, dtype=np.float64)
+    inv = theta ** (-2.0 * j / 64.0)
+    ang = np.arange(s, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang), np.sin(ang)
+
+
+def rope_apply(x, cos, sin, inverse=False):
+    """x: [b, H, s, 64]."""
+    sn = -sin if inverse else sin
+    a, b = x[..., :32], x[..., 32:]
+    return np.concatenate([a * cos - b * sn, b * cos + a * sn], axis=-1)
+
+
+def gu_split(w):
+    r = np.arange(w.shape[0])
+    return w[(r % 64) < 32], w[(r % 64) >= 32]
+
+
+def gu_merge(dg, du):
+    f = dg.shape[0]
+    out = np.zeros((2 * f,) + dg.shape[1:], dtype=dg.dtype)
+    r = np.arange(2 * f)
+    out[(r % 64) < 32] = dg
+    out[(r % 64) >= 32] = du
+    return out
+
+
+def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int, vocab: int,
+                         global_batch: int):
+    b, sp1 = tokens.shape
+    s = sp1 - 1
+    inp, tgt = tokens[:, :s], tokens[:, 1:]
+    h = P["wte"].shape[1]
+    dh = h // n_head
+    T = b * s
+    cos, sin = rope_tables(s)
+    x = P["wte"][inp.reshape(-1)].copy()
+    mask = np.triu(np.ones((s, s), dtype=bool), 1)
+    caches = []
+    heads = lambda m: m.reshape(b, s, n_head, dh).transpose(0, 2, 1, 3)  # noqa: E731
+    for i in range(n_layer):
+        p = lambda n: P[f"h{i}.{n}"]  # noqa: E731
+        x_in = x
+        a, c1 = rms_fwd(x_in, p("ln1_g")[0])
+        qkv = a @ p("w_qkv").T
+        q = rope_apply(heads(qkv[:, :h]), cos, sin)
+        k = rope_apply(heads(qkv[:, h:2 * h]), cos, sin)
+        v = heads(qkv[:, 2 * h:])
+        S = (q @ k.transpose(0, 1, 3, 2)) / np.sqrt(dh)
+        S = np.where(mask, -np.inf, S)
+        S = S - S.max(-1, keepdims=True)
+        Pm = np.exp(S)
+        Pm /= Pm.sum(-1, keepdims=True)
+        o = (Pm @ v).transpose(0, 2, 1, 3).reshape(T, h)
+        x_mid = x_in + o @ p("w_o").T
+        m, c2 = rms_fwd(x_mid, p("ln2_g")[0])
+        wg, wu = gu_split(p("w_gu"))
+        ga, ub = m @ wg.T, m @ wu.T
+        sg = 1.0 / (1.0 + np.exp(-ga))
+        hh = ga * sg * ub
+        x = x_mid + hh @ p("w_down").T
+        caches.append((x_in, a, c1, q, k, v, Pm, o, x_mid, m, c2, ga, ub, sg, hh))
+    xf, cf = rms_fwd(x, P["lnf_g"][0])
+    W = P["lm_head"][:vocab]
+    logits = xf @ W.T
+    mx = logits.max(-1, keepdims=True)
+    lse = mx[:, 0] + np.log(np.exp(logits - mx).sum(-1))
+    t = tgt.reshape(-1)
+    scale = 1.0 / (global_batch * s)
+    loss = float((lse - logits[np.arange(T), t]).sum() * scale)
+    dlog = np.exp(logits - lse[:, None])
+    dlog[np.arange(T), t] -= 1.0
+    dlog *= scale
+    G = {k_: np.zeros_like(v_) for k_, v_ in P.items()}
+    G["lm_head"][:vocab] = dlog.T @ xf
+    dx, G["lnf_g"][0] = rms_bwd(dlog @ W, P["lnf_g"][0], cf)
+    unheads = lambda m: m.transpose(0, 2, 1, 3).reshape(T, h)  # noqa: E731
+    for i in reversed(range(n_layer)):
+        p = lambda n: P[f"h{i}.{n}"]  # noqa: E731
+        x_in, a, c1, q, k, v, Pm, o, x_mid, m, c2, ga, ub, sg, hh = caches[i]
+        G[f"h{i}.w_down"] = dx.T @ hh
+        dhh = dx @ p("w_down")
+        silu = ga * sg
+        dub = dhh * silu
+        dga = dhh * ub * sg * (1.0 + ga * (1.0 - sg))
+        wg, wu = gu_split(p("w_gu"))
+        G[f"h{i}.w_gu"] = gu_merge(dga.T @ m, dub.T @ m)
+        dm = dga @ wg + dub @ wu
+        d2, G[f"h{i}.ln2_g"][0] = rms_bwd(dm, p("ln2_g")[0], c2)
+        dx_mid = dx + d2
+        G[f"h{i}.w_o"] = dx_mid.T @ o
+        dO = heads(dx_mid @ p("w_o"))
+        dV = Pm.transpose(0, 1, 3, 2) @ dO
+        dP = dO @ v.transpose(0, 1, 3, 2)
+        dS = Pm * (dP - (Pm * dP).sum(-1, keepdims=True)) / np.sqrt(dh)
+        dQ = rope_apply(dS @ k, cos, sin, inverse=True)
+        dK = rope_apply(dS.transpose(0, 1, 3, 2) @ q, cos, sin, inverse=True)
+        dqkv = np.concatenate([unheads(dQ), unheads(dK), unheads(dV)], axis=1)
+        G[f"h{i}.w_qkv"] = dqkv.T @ a
+        d1, G[f"h{i}.ln1_g"][0] = rms_bwd(dqkv @ p("w_qkv"), p("ln1_g")[0], c1)
+        dx = dx_mid + d1
+    np.add.at(G["wte"], inp.reshape(-1), dx)
+    return loss, G
+
+
+def loss_and_grads(P, tokens, n_layer, n_head, vocab, global_batch, arch=0):
+    f = llama_loss_and_grads if arch == 1 else gpt_loss_and_grads
+    return f(P, tokens, n_layer, n_head, vocab, global_batch)

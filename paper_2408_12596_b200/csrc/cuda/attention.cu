@@ -77,16 +77,20 @@ __device__ __forceinline__ AttnTask fwd_task(int t, int nz, int nt) {
 __device__ __forceinline__ AttnTask bwd_task(int t, int nz) { return {t / nz, t % nz}; }
 
 // ============================================================================ forward
+// Warp roles: 0-7 softmax (TMEM lane quarter w % 4, key half w / 4), 8 TMA producer, 9 MMA.
+constexpr int kFwdThreads = 320;
+
 struct FwdSmem {
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kTile;           // 2 stages
   static constexpr int kV = kK + 2 * kTile;       // 2 stages
   static constexpr int kP = kV + 2 * kTile;       // [128, 128] = 2 tiles
-  static constexpr int kBar = kP + 2 * kTile;
+  static constexpr int kRed = kP + 2 * kTile;   // [2 halves][128 rows] fp32 exchange
+  static constexpr int kBar = kRed + 2 * 128 * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, bf16* __restrict__ out,
                     float* __restrict__ lse, int seq, int heads, int nz, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ntasks = nt * nz;
   const int h = heads * kD;
 
-  if (warp == 4 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
@@ -117,19 +121,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&kv_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
-    ptx::mbar_init(s_free, 128);
-    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(s_free, 256);
+    ptx::mbar_init(p_full, 256);
     ptx::mbar_init(o_full, 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, 256);
+  if (warp == 8) ptx::tmem_alloc(tmem_slot, 256);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_s = tmem, t_o = tmem + 128;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0, item = 0;
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, 64, 0, 1);
@@ -188,77 +192,88 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {  // -------------------------------------------------------------- softmax warps 0-3
-    const int r = warp * 32 + lane;  // query row within the tile == TMEM lane
-    const uint32_t lane_off = uint32_t(warp * 32) << 16;
+  } else {  // -------------------------------------------------------------- softmax warps 0-7
+    // Warp (q4, kh) owns query rows 32*q4..+31 and keys 64*kh..+63 of every S tile, and O columns
+    // 32*kh..+31. The two halves of a row exchange their maxima through shared memory.
+    const int q4 = warp & 3, kh = warp >> 2;
+    const int r = q4 * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
     const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
+    float* red = reinterpret_cast<float*>(sm + FwdSmem::kRed);  // [2][128]
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
       const AttnTask tk = fwd_task(t, nz, nt);
       const int smp = tk.z / heads, head = tk.z % heads;
-      float o[kD];
+      float o[32];
 #pragma unroll
-      for (int i = 0; i < kD; ++i) o[i] = 0.f;
+      for (int i = 0; i < 32; ++i) o[i] = 0.f;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j <= tk.tile; ++j, ++it) {
         ptx::mbar_wait(s_full, it & 1);
         ptx::tc_fence_after();
-        float s[kT];
+        float sv[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, v);
+          ptx::tmem_ld_32x32b_x32(t_s + lane_off + kh * 64 + c * 32, v);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
         if (j == tk.tile) {  // diagonal tile: key > query is masked
 #pragma unroll
-          for (int i = 0; i < kT; ++i)
-            if (i > r) s[i] = -INFINITY;
+          for (int i = 0; i < 64; ++i)
+            if (kh * 64 + i > r) sv[i] = -INFINITY;
         }
-        float mx = m;
+        float lm = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kT; ++i) mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < 64; ++i) lm = fmaxf(lm, sv[i]);
+        red[kh * 128 + r] = lm;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");  // the row's two halves
+        const float mx = fmaxf(m, fmaxf(red[r], red[128 + r]));
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");  // red reusable next tile
         const float alpha = exp2f(m - mx);
         m = mx;
         float sum = 0.f;
 #pragma unroll
-        for (int c = 0; c < kT; c += 8) {
+        for (int c = 0; c < 64; c += 8) {
           float p[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            p[i] = exp2f(s[c + i] - mx);
+            p[i] = exp2f(sv[c + i] - mx);
             sum += p[i];
           }
-          st_shared_v4(sp + p_off(r, c), pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
-                       pack_bf16(p[6], p[7]));
+          st_shared_v4(sp + p_off(r, kh * 64 + c), pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]),
+                       pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         }
         l = l * alpha + sum;
         fence_proxy_async();
         ptx::mbar_arrive(p_full);
 #pragma unroll
-        for (int i = 0; i < kD; ++i) o[i] *= alpha;
+        for (int i = 0; i < 32; ++i) o[i] *= alpha;
         ptx::mbar_wait(o_full, it & 1);
         ptx::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          ptx::tmem_ld_32x32b_x32(t_o + lane_off + kh * 32, v);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[c * 32 + i] += __uint_as_float(v[i]);
+          for (int i = 0; i < 32; ++i) o[i] += __uint_as_float(v[i]);
         }
         ptx::tc_fence_before();
       }
-      // epilogue: O / l -> bf16 row, natural-log LSE
-      const float inv = 1.f / l;
+      // combine the two halves' row sums, then O / l -> bf16 (this warp's 32 columns), LSE
+      red[kh * 128 + r] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+      const float lt = red[r] + red[128 + r];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+      const float inv = 1.f / lt;
       const int64_t row = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
-      bf16* dst = out + row * h + head * kD;
+      bf16* dst = out + row * h + head * kD + kh * 32;
 #pragma unroll
-      for (int c = 0; c < kD; c += 8) {
+      for (int c = 0; c < 32; c += 8) {
         uint4 u;
         u.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
         u.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
@@ -266,12 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         u.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
         *reinterpret_cast<uint4*>(dst + c) = u;
       }
-      lse[int64_t(tk.z) * seq + int64_t(tk.tile) * kT + r] = (m + log2f(l)) / kLog2e;
+      if (kh == 0) lse[int64_t(tk.z) * seq + int64_t(tk.tile) * kT + r] = (m + log2f(lt)) / kLog2e;
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 256);
   }
@@ -634,7 +649,7 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
   const int ntasks = (seq / kT) * nz;
   int grid = std::min(ntasks, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
   const float scale_log2 = (1.0f / std::sqrt(float(kD))) * kLog2e;
-  attn_fwd_kernel<<<grid, kThreads, FwdSmem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
+  attn_fwd_kernel<<<grid, kFwdThreads, FwdSmem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
   note_launch();
   return cudaGetLastError();
 }

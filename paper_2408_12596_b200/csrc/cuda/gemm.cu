@@ -116,7 +116,9 @@ __device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32
     return;
   }
   if (e == kEpiBiasBf16 || e == kEpiBiasResidBf16 || e == kEpiBiasGeluBf16) {
-    if (full) {
+    if (!ep.bias) {
+      // bias-free layers (Llama): residual / activation only
+    } else if (full) {
 #pragma unroll
       for (int i = 0; i < 32; i += 8) {
         const uint4 braw = *reinterpret_cast<const uint4*>(ep.bias + n + i);

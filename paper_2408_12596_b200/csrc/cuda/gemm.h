@@ -51,7 +51,7 @@ struct GemmArgs {
   float alpha = 1.0f;
   int epilogue = kEpiStoreBf16;
   int causal = kCausalNone;
-  const void* bias = nullptr;  // bf16 [N]
+  const void* bias = nullptr;  // bf16 [N]; may be null (no bias)
   const void* aux = nullptr;   // bf16, same layout as C (residual R or pre-activation U)
   void* aux_out = nullptr;     // bf16, same layout as C (U written by kEpiBiasGeluBf16)
   int max_ctas = 0;            // SM budget cap (0 = all SMs)

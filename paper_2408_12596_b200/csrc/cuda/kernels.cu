@@ -107,9 +107,11 @@ __global__ void embed_fwd_k(const int32_t* tok, int seq, const bf16* wte, const 
     const int32_t t = tok[smp * (seq + 1) + pos];
     float a[8], b[8];
     unpack8(*reinterpret_cast<const uint4*>(wte + int64_t(t) * h + c), a);
-    unpack8(*reinterpret_cast<const uint4*>(wpe + int64_t(pos) * h + c), b);
+    if (wpe) {
+      unpack8(*reinterpret_cast<const uint4*>(wpe + int64_t(pos) * h + c), b);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a[k] += b[k];
+      for (int k = 0; k < 8; ++k) a[k] += b[k];
+    }
     *reinterpret_cast<uint4*>(x + r * h + c) = pack8(a);
   }
 }
@@ -130,14 +132,15 @@ __global__ void embed_bwd_k(const int32_t* tok, int seq, const bf16* dx, float* 
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       atomicAdd(dwte + int64_t(t) * h + c + k, d[k]);
-      atomicAdd(dwpe + int64_t(pos) * h + c + k, d[k]);
+      if (dwpe) atomicAdd(dwpe + int64_t(pos) * h + c + k, d[k]);
     }
   }
 }
 
 // ------------------------------------------------------------------ LayerNorm (one warp per row)
 
-template <int NC>  // h = NC * 256
+// RMS = true: RMSNorm (no centring, no beta).
+template <int NC, bool RMS>  // h = NC * 256
 __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
                                                      const bf16* __restrict__ g,
                                                      const bf16* __restrict__ b, bf16* y,
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
 #pragma unroll
       for (int k = 0; k < 8; ++k) s += v[c][k];
     }
-    const float mu = warp_sum(s) * (1.0f / h);
+    const float mu = RMS ? 0.f : warp_sum(s) * (1.0f / h);
     float q = 0.f;
 #pragma unroll
     for (int c = 0; c < NC; ++c)
@@ -169,7 +172,12 @@ __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
       const int col = (c * 32 + lane) * 8;
       float gg[8], bb[8], o[8];
       unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
-      unpack8(*reinterpret_cast<const uint4*>(b + col), bb);
+      if (RMS) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bb[k] = 0.f;
+      } else {
+        unpack8(*reinterpret_cast<const uint4*>(b + col), bb);
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k] = (v[c][k] - mu) * rs * gg[k] + bb[k];
       *reinterpret_cast<uint4*>(y + r * h + col) = pack8(o);
@@ -181,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
   }
 }
 
-template <int NC>
+template <int NC, bool RMS>
 __global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy,
                                                      const bf16* __restrict__ x,
                                                      const float* __restrict__ mean,
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy
         accb[c][k] += dv[k];
       }
     }
-    const float m1 = warp_sum(s1) * (1.0f / h);
+    const float m1 = RMS ? 0.f : warp_sum(s1) * (1.0f / h);
     const float m2 = warp_sum(s2) * (1.0f / h);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -477,6 +485,76 @@ __global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, floa
 
 }  // namespace
 
+// ------------------------------------------------------------------ RoPE (rotate-half, head_dim 64)
+
+// In place on the Q and K column blocks of qkv [T, 3h]; inverse = rotation by -theta (backward).
+__global__ void rope_k(bf16* qkv, int64_t tokens, int seq, int h, float theta, float sign) {
+  const int pairs = h / 2;  // per Q or K block: heads * 32 pairs
+  const int64_t total = tokens * 2 * pairs;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (2 * pairs);
+    const int r = int(i % (2 * pairs));
+    const int blk = r / pairs;          // 0 = Q, 1 = K
+    const int p = r % pairs;
+    const int head = p / 32, j = p % 32;
+    const int pos = int(t % seq);
+    const float inv_freq = exp2f(-float(2 * j) / 64.0f * log2f(theta));
+    float sn, cs;
+    sincosf(float(pos) * inv_freq, &sn, &cs);
+    sn *= sign;
+    bf16* v = qkv + t * 3 * h + blk * h + head * 64;
+    const float a = __bfloat162float(v[j]), b = __bfloat162float(v[j + 32]);
+    v[j] = __float2bfloat16_rn(a * cs - b * sn);
+    v[j + 32] = __float2bfloat16_rn(b * cs + a * sn);
+  }
+}
+
+// ------------------------------------------------------------------ SwiGLU (gate/up interleaved
+// in 32-column blocks: feature j has gate at 64*(j/32) + j%32 and up 32 columns later)
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+__global__ void swiglu_fwd_k(const bf16* __restrict__ gu, bf16* __restrict__ out, int64_t tokens, int f) {
+  const int64_t total = tokens * (f / 8);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (f / 8);
+    const int j0 = int(i % (f / 8)) * 8;  // 8 features, same 32-block
+    const int64_t gbase = t * 2 * f + (j0 / 32) * 64 + (j0 % 32);
+    float a[8], b[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + gbase), a);
+    unpack8(*reinterpret_cast<const uint4*>(gu + gbase + 32), b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = a[k] * sigmoidf_(a[k]) * b[k];
+    *reinterpret_cast<uint4*>(out + t * f + j0) = pack8(o);
+  }
+}
+
+__global__ void swiglu_bwd_k(const bf16* __restrict__ gu, const bf16* __restrict__ dh, bf16* __restrict__ dgu,
+                             int64_t tokens, int f) {
+  const int64_t total = tokens * (f / 8);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (f / 8);
+    const int j0 = int(i % (f / 8)) * 8;
+    const int64_t gbase = t * 2 * f + (j0 / 32) * 64 + (j0 % 32);
+    float a[8], b[8], d[8], da[8], db[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + gbase), a);
+    unpack8(*reinterpret_cast<const uint4*>(gu + gbase + 32), b);
+    unpack8(*reinterpret_cast<const uint4*>(dh + t * f + j0), d);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float sg = sigmoidf_(a[k]);
+      const float silu = a[k] * sg;
+      db[k] = d[k] * silu;
+      da[k] = d[k] * b[k] * sg * (1.0f + a[k] * (1.0f - sg));
+    }
+    *reinterpret_cast<uint4*>(dgu + gbase) = pack8(da);
+    *reinterpret_cast<uint4*>(dgu + gbase + 32) = pack8(db);
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 
 std::atomic<int64_t> g_launches{0};
@@ -502,6 +580,16 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
   embed_fwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, wte, wpe, x,
                                                                           rows, h); note_launch();
 }
+void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s) {
+  rope_k<<<grid_for(tokens * h, kThreads, ctas), kThreads, 0, s>>>(qkv, tokens, seq, h, theta,
+                                                                  inverse ? -1.f : 1.f); note_launch();
+}
+void swiglu_fwd(const bf16* gu, bf16* out, int64_t tokens, int f, int ctas, cudaStream_t s) {
+  swiglu_fwd_k<<<grid_for(tokens * f / 8, kThreads, ctas), kThreads, 0, s>>>(gu, out, tokens, f); note_launch();
+}
+void swiglu_bwd(const bf16* gu, const bf16* dh, bf16* dgu, int64_t tokens, int f, int ctas, cudaStream_t s) {
+  swiglu_bwd_k<<<grid_for(tokens * f / 8, kThreads, ctas), kThreads, 0, s>>>(gu, dh, dgu, tokens, f); note_launch();
+}
 void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
                int64_t rows, int h, int ctas, cudaStream_t s) {
   embed_bwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, dx, dwte32,
@@ -517,7 +605,10 @@ cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, 
 #define X(NC)                                                                     \
   case NC:                                                                        \
     if (h % 256) return cudaErrorInvalidValue;                                    \
-    ln_fwd_k<NC><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows); note_launch();         \
+    if (b)                                                                        \
+      ln_fwd_k<NC, false><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows); \
+    else                                                                          \
+      ln_fwd_k<NC, true><<<grid, kThreads, 0, s>>>(x, g, b, y, mean, rstd, rows); note_launch();         \
     return cudaGetLastError();
     ZP_LN_CASES(X)
 #undef X
@@ -528,14 +619,17 @@ cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, 
 
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
-                          int64_t rows, int h, int ctas, cudaStream_t s) {
+                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms) {
   const int grid = grid_for(rows, kThreads / 32, ctas, 2);
   *nblk = grid;
   switch (h / 256) {
 #define X(NC)                                                                              \
   case NC:                                                                                 \
     if (h % 256) return cudaErrorInvalidValue;                                             \
-    ln_bwd_k<NC><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); note_launch();    \
+    if (rms)                                                                               \
+      ln_bwd_k<NC, true><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); \
+    else                                                                                   \
+      ln_bwd_k<NC, false><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); note_launch();    \
     return cudaGetLastError();
     ZP_LN_CASES(X)
 #undef X

@@ -24,6 +24,7 @@ void synth_tokens(int32_t* tokens, int64_t first, int64_t count, int seq_plus1, 
 // ---- forward
 void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe, bf16* x,
                int64_t rows, int h, int ctas, cudaStream_t s);
+// LayerNorm, or RMSNorm when b == nullptr (mean written as 0).
 cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mean,
                           float* rstd, int64_t rows, int h, int ctas, cudaStream_t s);
 // per-row CE on bf16 logits [rows, ldv] (first `vocab` columns valid); overwrites logits with
@@ -35,7 +36,12 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
 // dx = dres + LN_bwd(dy); dgamma/dbeta partials per block into part[2][nblk][h]; returns nblk.
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
-                          int64_t rows, int h, int ctas, cudaStream_t s);
+                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms = false);
+// Rotary embedding (rotate-half, head_dim 64) on the Q and K blocks of qkv [T, 3h], in place.
+void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s);
+// SwiGLU with gate/up interleaved in 32-column blocks of gu [T, 2f]: out [T, f].
+void swiglu_fwd(const bf16* gu, bf16* out, int64_t tokens, int f, int ctas, cudaStream_t s);
+void swiglu_bwd(const bf16* gu, const bf16* dh, bf16* dgu, int64_t tokens, int f, int ctas, cudaStream_t s);
 void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
                int64_t rows, int h, int ctas, cudaStream_t s);
 // out[n] = sum over rows of X[r, n] (X bf16 [rows, ld]); partial workspace [chunks][N] f32.

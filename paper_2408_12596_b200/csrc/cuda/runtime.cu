@@ -92,9 +92,10 @@ struct Group {
 };
 struct LayerP {
   Tensor ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc, b_fc, w_proj, b_proj;
+  Tensor w_gu, w_down;  // Llama: gate/up (interleaved 32-row blocks) and down projections
 };
 struct Layout {
-  Tensor wte, wpe, lnf_g, lnf_b;
+  Tensor wte, wpe, lnf_g, lnf_b, lm_head;
   std::vector<LayerP> layers;
   std::vector<Group> groups;  // 0 = embedding, 1..L = layers, L+1 = final LayerNorm
   std::map<std::string, Tensor> by_name;
@@ -122,6 +123,32 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
     return t;
   };
   const int h = c.d_model, f = c.d_ff;
+  if (c.arch == 1) {  // Llama family
+    open_group();
+    L.wte = add("wte", vocab_pad, h, c.vocab);
+    close_group();
+    for (int i = 0; i < c.n_layer; ++i) {
+      const std::string p = "h" + std::to_string(i) + ".";
+      open_group();
+      LayerP l;
+      l.ln1_g = add(p + "ln1_g", 1, h, 1);
+      l.w_qkv = add(p + "w_qkv", 3 * h, h, 3 * h);
+      l.w_o = add(p + "w_o", h, h, h);
+      l.ln2_g = add(p + "ln2_g", 1, h, 1);
+      l.w_gu = add(p + "w_gu", 2 * f, h, 2 * f);
+      l.w_down = add(p + "w_down", h, f, h);
+      close_group();
+      L.layers.push_back(l);
+      L.max_layer_group = std::max(L.max_layer_group, L.groups.back().len);
+    }
+    open_group();
+    L.lnf_g = add("lnf_g", 1, h, 1);
+    L.lm_head = add("lm_head", vocab_pad, h, c.vocab);
+    close_group();
+    L.total = cur;
+    for (const Group& g : L.groups) L.max_group = std::max(L.max_group, g.len);
+    return L;
+  }
   open_group();
   L.wte = add("wte", vocab_pad, h, c.vocab);
   L.wpe = add("wpe", c.seq_len, h, c.seq_len);
@@ -168,6 +195,7 @@ struct Acts {
   float* dvec;  // [b, H, s] rowsum(dO * O)
   float* dq32;  // [T, h] fp32 dQ accumulator of the fused attention backward
   bf16 *dx, *dx2, *dln, *dO, *dqkv, *du;
+  bf16* dh;  // Llama: gradient of the SwiGLU output [T, f] (du is then [T, 2f])
 };
 
 // ------------------------------------------------------------------ event timing
@@ -370,7 +398,7 @@ struct Runtime {
       L.attn = B16(T * h);
       L.x_mid = B16(T * h);
       L.ln2 = B16(T * h);
-      L.u = B16(T * f);
+      L.u = B16(T * f * (c.arch == 1 ? 2 : 1));
       L.g = B16(T * f);
       L.mu1 = F32(T);
       L.rs1 = F32(T);
@@ -391,7 +419,8 @@ struct Runtime {
     A.dln = B16(T * h);
     A.dO = B16(T * h);
     A.dqkv = B16(T * 3 * h);
-    A.du = B16(T * f);
+    A.du = B16(T * f * (c.arch == 1 ? 2 : 1));
+    A.dh = c.arch == 1 ? B16(T * f) : nullptr;
     return bytes;
   }
 
@@ -439,7 +468,7 @@ struct Runtime {
     const int64_t h = c.d_model;
     dwte32 = F32(int64_t(vocab_pad) * h, "dwte");
     dwpe32 = F32(int64_t(c.seq_len) * h, "dwpe");
-    wgrad32 = F32(std::max<int64_t>(3 * h, c.d_ff) * h, "wgrad");
+    wgrad32 = F32(std::max<int64_t>(3 * h, 2 * int64_t(c.d_ff)) * h, "wgrad");
     ln_part = F32(int64_t(2) * 2 * 148 * h, "ln partials");
     const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
     col_work = F32(256 * maxN, "colsum work");
@@ -487,6 +516,21 @@ struct Runtime {
     Tensor wte_real = lay.wte;
     wte_real.rows = c.vocab;  // padded vocabulary rows stay zero
     init(wte_real, 0, 0.02f);
+    if (c.arch == 1) {
+      for (const LayerP& l : lay.layers) {
+        init(l.ln1_g, 1, 0);
+        init(l.w_qkv, 0, 0.02f);
+        init(l.w_o, 0, sp);
+        init(l.ln2_g, 1, 0);
+        init(l.w_gu, 0, 0.02f);
+        init(l.w_down, 0, sp);
+      }
+      init(lay.lnf_g, 1, 0);
+      Tensor head_real = lay.lm_head;
+      head_real.rows = c.vocab;
+      init(head_real, 0, 0.02f);
+      return;
+    }
     init(lay.wpe, 0, 0.01f);
     for (const LayerP& l : lay.layers) {
       init(l.ln1_g, 1, 0); init(l.ln1_b, 2, 0);
@@ -547,6 +591,7 @@ struct Runtime {
 
   // ---------------------------------------------------------------- forward / backward
   void forward(Acts& A, const int32_t* tok, bool with_loss, float grad_scale) {
+    if (c.arch == 1) return forward_llama(A, tok, with_loss, grad_scale);
     const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
     const int NG = int(lay.groups.size());
     z3_gather(0, kAgF);
@@ -582,7 +627,82 @@ struct Runtime {
     sum_partials(ln_part + int64_t(nblk) * h, nblk, h, Gp(b), st);
   }
 
+  // ---------------------------------------------------------------- Llama family
+  // Pre-norm RMSNorm, rotary Q/K (theta 1e4), SwiGLU MLP, no biases, untied LM head.
+  void forward_llama(Acts& A, const int32_t* tok, bool with_loss, float grad_scale) {
+    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
+    const int NG = int(lay.groups.size());
+    z3_gather(0, kAgF);
+    embed_fwd(tok, int(s), Wp(lay.wte), nullptr, A.l[0].x_in, T, int(h), ctas, st);
+    for (int i = 0; i < c.n_layer; ++i) {
+      const LayerP& P = lay.layers[i];
+      LayerActs& L = A.l[i];
+      z3_gather(i + 1, kAgF);
+      bf16* x_out = (i + 1 < c.n_layer) ? A.l[i + 1].x_in : A.x_final;
+      CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), nullptr, L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
+      mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiStoreBf16);
+      rope(L.qkv, T, int(s), int(h), 10000.f, false, ctas, st);
+      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st));
+      mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_in);
+      CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), nullptr, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
+      mm(T, 2 * f, h, L.ln2, kKMajor, h, Wp(P.w_gu), kKMajor, h, L.u, 2 * f, kEpiStoreBf16);
+      swiglu_fwd(L.u, L.g, T, int(f), ctas, st);
+      mm(T, h, f, L.g, kKMajor, f, Wp(P.w_down), kKMajor, f, x_out, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_mid);
+    }
+    z3_gather(NG - 1, kAgF);
+    CK(layernorm_fwd(A.x_final, Wp(lay.lnf_g), nullptr, A.lnf, A.muf, A.rsf, T, int(h), ctas, st));
+    mm(T, vocab_pad, h, A.lnf, kKMajor, h, Wp(lay.lm_head), kKMajor, h, A.logits, vocab_pad, kEpiStoreBf16);
+    if (with_loss)
+      cross_entropy_fwd_bwd(A.logits, tok, int(s), T, c.vocab, vocab_pad, grad_scale, A.row_loss, ctas, st);
+  }
+
+  void backward_llama(Acts& A, const int32_t* tok) {
+    const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
+    int nblk = 0;
+    const int NG = int(lay.groups.size());
+    z3_clear_group(NG - 1);
+    // untied LM head: dlnf = dlogits * W_head ; dW_head = dlogits^T * lnf
+    mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, Wp(lay.lm_head), kMNMajor, h, A.dln, h, kEpiStoreBf16);
+    wgrad(vocab_pad, int(h), T, A.logits, vocab_pad, A.lnf, h, Gp(lay.lm_head));
+    CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, Wp(lay.lnf_g), nullptr, A.dx, ln_part, &nblk, T, int(h), ctas,
+                     st, true));
+    sum_partials(ln_part, nblk, int(h), Gp(lay.lnf_g), st);
+    z3_reduce(NG - 1);
+    for (int i = c.n_layer - 1; i >= 0; --i) {
+      const LayerP& P = lay.layers[i];
+      LayerActs& L = A.l[i];
+      z3_gather(i + 1, kAgB);
+      z3_clear_group(i + 1);
+      // MLP: down projection, SwiGLU, gate/up projection
+      wgrad(int(h), int(f), T, A.dx, h, L.g, f, Gp(P.w_down));
+      mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_down), kMNMajor, f, A.dh, f, kEpiStoreBf16);
+      swiglu_bwd(L.u, A.dh, A.du, T, int(f), ctas, st);
+      wgrad(int(2 * f), int(h), T, A.du, 2 * f, L.ln2, h, Gp(P.w_gu));
+      mm(T, h, 2 * f, A.du, kKMajor, 2 * f, Wp(P.w_gu), kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h), ctas, st,
+                       true));
+      sum_partials(ln_part, nblk, int(h), Gp(P.ln2_g), st);
+      // attention
+      wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gp(P.w_o));
+      mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
+      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st));
+      rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st);  // back to pre-rotation Q, K
+      wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
+      mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
+      CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h), ctas, st,
+                       true));
+      sum_partials(ln_part, nblk, int(h), Gp(P.ln1_g), st);
+      z3_reduce(i + 1);
+    }
+    z3_clear_group(0);
+    CK(cudaMemsetAsync(dwte32, 0, size_t(vocab_pad) * h * 4, st));
+    embed_bwd(tok, int(s), A.dx, dwte32, nullptr, T, int(h), ctas, st);
+    cast_f32_bf16(dwte32, Gp(lay.wte), int64_t(vocab_pad) * h, ctas, st);
+    z3_reduce(0);
+  }
+
   void backward(Acts& A, const int32_t* tok) {
+    if (c.arch == 1) return backward_llama(A, tok);
     const int64_t b = A.b, s = c.seq_len, h = c.d_model, f = c.d_ff, H = c.n_head, T = b * s;
     int nblk = 0;
     const int NG = int(lay.groups.size());
@@ -1031,7 +1151,7 @@ int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
       R.rank = desc->rank;
       const zp_gpt_config& c = R.c;
       if (c.d_model % 256 || c.d_model / c.n_head != 64 || c.d_model % c.n_head || c.seq_len % 128 ||
-          c.d_ff % 64 || c.vocab < 2 || c.n_layer < 1)
+          c.d_ff % 64 || c.vocab < 2 || c.n_layer < 1 || c.arch < 0 || c.arch > 1)
         zp::fail(ZP_EINVAL, "unsupported model shape (need d_model % 256 == 0, head_dim 64, seq % 128 == 0)");
       CK(cudaSetDevice(desc->device));
       int sms = 0;

@@ -20,7 +20,7 @@ lib = _lib.lib
 
 class GptConfig(C.Structure):
     _fields_ = [("n_layer", C.c_int32), ("d_model", C.c_int32), ("n_head", C.c_int32), ("d_ff", C.c_int32),
-                ("vocab", C.c_int32), ("seq_len", C.c_int32)]
+                ("vocab", C.c_int32), ("seq_len", C.c_int32), ("arch", C.c_int32)]
 
 
 class RuntimeDesc(C.Structure):
@@ -93,19 +93,21 @@ class GPT:
     vocab: int
     seq_len: int
     d_ff: int = 0
+    arch: int = 0  # 0 = GPT-2 family, 1 = Llama family
 
     def __post_init__(self):
         if not self.d_ff:
             self.d_ff = 4 * self.d_model
 
     def to_c(self) -> GptConfig:
-        return GptConfig(self.n_layer, self.d_model, self.n_head, self.d_ff, self.vocab, self.seq_len)
+        return GptConfig(self.n_layer, self.d_model, self.n_head, self.d_ff, self.vocab, self.seq_len, self.arch)
 
     def flops_per_sample(self) -> float:
         """Training FLOPs of one sample: 6 * N_matmul * s + 12 * L * h * s^2 (dense attention
         accounting)."""
         h, f, L, s = self.d_model, self.d_ff, self.n_layer, self.seq_len
-        n_mm = L * (4 * h * h + 2 * h * f) + self.vocab * h
+        mlp = 3 * h * f if self.arch == 1 else 2 * h * f
+        n_mm = L * (4 * h * h + mlp) + self.vocab * h
         return 6.0 * n_mm * s + 12.0 * L * h * s * s
 
 
@@ -113,6 +115,9 @@ MODELS = {
     "gpt-tiny": GPT(4, 256, 4, 8192, 256, 1024),
     "gpt2-small": GPT(12, 768, 12, 50257, 1024),
     "gpt2-medium": GPT(24, 1024, 16, 50257, 1024),
+    # Llama-style configs of BASELINE.json (head_dim 64: 32 heads at h=2048, 64 heads at h=4096)
+    "llama-1.3b": GPT(24, 2048, 32, 32000, 2048, 5504, arch=1),
+    "llama-7b": GPT(32, 4096, 64, 32000, 4096, 11008, arch=1),
 }
 
 
@@ -243,6 +248,11 @@ class Runtime:
         return o.value, r.value, c.value
 
     def tensor_names(self):
+        if self.model.arch == 1:
+            names = ["wte"]
+            for i in range(self.model.n_layer):
+                names += [f"h{i}.{n}" for n in ("ln1_g", "w_qkv", "w_o", "ln2_g", "w_gu", "w_down")]
+            return names + ["lnf_g", "lm_head"]
         names = ["wte", "wpe"]
         for i in range(self.model.n_layer):
             names += [f"h{i}.{n}" for n in ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b",

@@ -74,3 +74,59 @@ def test_split_batch_invariance():
     assert abs(lsum - l_all) < 1e-12
     for k in P:
         assert so.rel_err(acc[k], G_all[k]) < 1e-12
+
+
+def torch_llama(P, tokens, n_layer, n_head, vocab, B):
+    T = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in P.items()}
+    tok = torch.tensor(tokens, dtype=torch.long)
+    b, sp1 = tok.shape
+    s = sp1 - 1
+    inp, tgt = tok[:, :s], tok[:, 1:]
+    h = T["wte"].shape[1]
+    dh = h // n_head
+    j = torch.arange(32, dtype=torch.float64)
+    ang = torch.arange(s, dtype=torch.float64)[:, None] * (10000.0 ** (-2.0 * j / 64.0))[None]
+    cos, sin = torch.cos(ang), torch.sin(ang)
+
+    def rope(x):
+        a, b_ = x[..., :32], x[..., 32:]
+        return torch.cat([a * cos - b_ * sin, b_ * cos + a * sin], -1)
+
+    def rms(x, g):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-5) * g
+
+    x = T["wte"][inp]
+    for i in range(n_layer):
+        p = lambda n: T[f"h{i}.{n}"]  # noqa: E731
+        a = rms(x, p("ln1_g")[0])
+        qkv = a @ p("w_qkv").T
+        q, k, v = (qkv[..., m * h:(m + 1) * h].view(b, s, n_head, dh).transpose(1, 2) for m in range(3))
+        o = torch.nn.functional.scaled_dot_product_attention(rope(q), rope(k), v, is_causal=True)
+        x = x + o.transpose(1, 2).reshape(b, s, h) @ p("w_o").T
+        m_ = rms(x, p("ln2_g")[0])
+        w = p("w_gu")
+        r = torch.arange(w.shape[0])
+        wg, wu = w[(r % 64) < 32], w[(r % 64) >= 32]
+        x = x + (torch.nn.functional.silu(m_ @ wg.T) * (m_ @ wu.T)) @ p("w_down").T
+    xf = rms(x, T["lnf_g"][0])
+    logits = xf @ T["lm_head"][:vocab].T
+    loss = torch.nn.functional.cross_entropy(logits.reshape(-1, vocab), tgt.reshape(-1), reduction="sum") / (B * s)
+    loss.backward()
+    return loss.item(), {k: v.grad.numpy() for k, v in T.items()}
+
+
+def test_llama_oracle_matches_autograd():
+    rng = np.random.default_rng(4)
+    L, h, H, ff, V, Vp, s = 2, 128, 2, 64, 50, 64, 16
+    P = {"wte": rng.normal(0, 0.1, (Vp, h)), "lnf_g": 1 + rng.normal(0, 0.1, (1, h)),
+         "lm_head": rng.normal(0, 0.1, (Vp, h))}
+    for i in range(L):
+        P.update({f"h{i}.ln1_g": 1 + rng.normal(0, 0.1, (1, h)), f"h{i}.w_qkv": rng.normal(0, 0.1, (3 * h, h)),
+                  f"h{i}.w_o": rng.normal(0, 0.1, (h, h)), f"h{i}.ln2_g": 1 + rng.normal(0, 0.1, (1, h)),
+                  f"h{i}.w_gu": rng.normal(0, 0.1, (2 * ff, h)), f"h{i}.w_down": rng.normal(0, 0.1, (h, ff))})
+    tokens = rng.integers(0, V, (3, s + 1))
+    loss, G = so.llama_loss_and_grads(P, tokens, L, H, V, 5)
+    tl, TG = torch_llama(P, tokens, L, H, V, 5)
+    assert abs(loss - tl) <= 1e-12 * max(1.0, abs(tl))
+    for k in P:
+        assert so.rel_err(G[k], TG[k]) < 1e-10, k
