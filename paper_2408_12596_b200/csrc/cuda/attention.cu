@@ -160,35 +160,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp == 9) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      // S(j+1) is issued as soon as the softmax warps have pulled S(j) out of TMEM, before P V(j):
+      // the tensor pipe computes the next scores while the softmax of tile j runs.
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, 64, 0, 1);
       const uint32_t sq = ptx::smem_u32(sm + FwdSmem::kQ);
       const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
-      int stage = 0;
-      uint32_t phase = 0, item = 0, it = 0;
+      int ks = 0, kp = 0;              // K/V stage of the next S issue and of the next P V issue
+      uint32_t ks_ph = 0, item = 0, it = 0;
+      auto issue_s = [&](uint32_t s_parity) {
+        ptx::mbar_wait(&kv_full[ks], ks_ph);
+        ptx::mbar_wait(s_free, s_parity);
+        ptx::tc_fence_after();
+        const uint32_t sk = ptx::smem_u32(sm + FwdSmem::kK + ks * kTile);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_s, k > 0);
+        ptx::umma_commit(s_full);
+        if (++ks == 2) {
+          ks = 0;
+          ks_ph ^= 1;
+        }
+      };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = fwd_task(t, nz, nt);
+        const int nj = tk.tile + 1;
         ptx::mbar_wait(q_full, item & 1);
-        for (int j = 0; j <= tk.tile; ++j, ++it) {
-          ptx::mbar_wait(&kv_full[stage], phase);
-          ptx::mbar_wait(s_free, (it & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + FwdSmem::kK + stage * kTile);
-          const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + stage * kTile);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_s, k > 0);
-          ptx::umma_commit(s_full);
-          if (j == tk.tile) ptx::umma_commit(q_empty);
+        issue_s((it & 1) ^ 1);  // S(0): softmax finished reading the previous task's last S
+        if (nj == 1) ptx::umma_commit(q_empty);
+        for (int j = 0; j < nj; ++j, ++it) {
+          if (j + 1 < nj) {
+            issue_s(it & 1);  // S(j) has been read out of TMEM
+            if (j + 2 == nj) ptx::umma_commit(q_empty);
+          }
           ptx::mbar_wait(p_full, it & 1);
           ptx::tc_fence_after();
+          const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + kp * kTile);
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_o, kdesc2(sp, k), mndesc(sv, k), id_o, k > 0);
           ptx::umma_commit(o_full);
-          ptx::umma_commit(&kv_empty[stage]);
-          if (++stage == 2) {
-            stage = 0;
-            phase ^= 1;
-          }
+          ptx::umma_commit(&kv_empty[kp]);
+          kp ^= 1;
         }
       }
     }
@@ -387,6 +398,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 13) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      // S/dP of query tile i+1 are issued before the dV/dK/dQ products of tile i, so the builders
+      // compute P/dS(i+1) while the tensor pipe works on tile i.
       constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
       constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dV, dK (A^T, B MN-major)
       constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dQ
@@ -394,26 +407,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t sv = ptx::smem_u32(sm + BwdSmem::kV);
       const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
       const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
-      int stage = 0;
-      uint32_t phase = 0, item = 0, it = 0;
+      int ss = 0, sm2 = 0;  // Q/dO stage of the next S/dP issue and of the next dV/dK/dQ issue
+      uint32_t ss_ph = 0, item = 0, it = 0;
+      auto issue_sdp = [&](uint32_t s_parity) {
+        ptx::mbar_wait(&qd_full[ss], ss_ph);
+        ptx::mbar_wait(s_free, s_parity);
+        ptx::tc_fence_after();
+        const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
+        const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
+        ptx::umma_commit(sp_full);
+        if (++ss == 2) {
+          ss = 0;
+          ss_ph ^= 1;
+        }
+      };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task(t, nz);
         ptx::mbar_wait(kv_full, item & 1);
         ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // epilogue of the previous task read dK/dV
+        issue_sdp((it & 1) ^ 1);
         for (int i = tk.tile; i < nt; ++i, ++it) {
-          ptx::mbar_wait(&qd_full[stage], phase);
-          ptx::mbar_wait(s_free, (it & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + stage * kTile);
-          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + stage * kTile);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
-          ptx::umma_commit(sp_full);
+          if (i + 1 < nt) issue_sdp(it & 1);  // builders have pulled S/dP(i) out of TMEM
           ptx::mbar_wait(ps_full, it & 1);
           ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
           ptx::tc_fence_after();
+          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + sm2 * kTile);
+          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + sm2 * kTile);
           const bool first = (i == tk.tile);
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dv, mndesc(spp, k), mndesc(sdo, k), id_t, (!first || k > 0));
@@ -422,12 +445,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dq, kdesc2(sds, k), mndesc(sk, k), id_q, k > 0);
           ptx::umma_commit(mm_done);
-          ptx::umma_commit(&qd_empty[stage]);
+          ptx::umma_commit(&qd_empty[sm2]);
           if (i == nt - 1) ptx::umma_commit(kv_empty);
-          if (++stage == 2) {
-            stage = 0;
-            phase ^= 1;
-          }
+          sm2 ^= 1;
         }
       }
     }
@@ -444,7 +464,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
         const float lse2 = lse[qrow] * kLog2e;
         const float dd = dvec[qrow];
-        // S/dP(i) complete implies the MMAs of tile i-1 (which read P/dS) completed: in order.
         ptx::mbar_wait(sp_full, it & 1);
         ptx::tc_fence_after();
         uint32_t vs[2][32], vp[2][32];
@@ -456,25 +475,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
+        uint32_t pk[32], dk[32];  // packed bf16 pairs of this thread's 64 P and dS values
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
 #pragma unroll
-          for (int g = 0; g < 32; g += 8) {
-            float p[8], ds[8];
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2], dv[2];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int key = kh * 64 + c * 32 + g + e;
+            for (int u = 0; u < 2; ++u) {
+              const int key = kh * 64 + c * 32 + e + u;
               const bool masked = (i == tk.tile) && (key > r);
-              const float pv = masked ? 0.f : exp2f(__uint_as_float(vs[c][g + e]) * scale_log2 - lse2);
-              p[e] = pv;
-              ds[e] = pv * (__uint_as_float(vp[c][g + e]) - dd) * scale;
+              pv[u] = masked ? 0.f : exp2f(__uint_as_float(vs[c][e + u]) * scale_log2 - lse2);
+              dv[u] = pv[u] * (__uint_as_float(vp[c][e + u]) - dd) * scale;
             }
-            const uint32_t off = p_off(r, kh * 64 + c * 32 + g);
-            st_shared_v4(spp + off, pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
-                         pack_bf16(p[6], p[7]));
-            st_shared_v4(sds + off, pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
-                         pack_bf16(ds[6], ds[7]));
+            pk[c * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            dk[c * 16 + e / 2] = pack_bf16(dv[0], dv[1]);
           }
+        }
+        // P/dS smem is free once the dV/dK/dQ products of the previous tile completed
+        ptx::mbar_wait(mm_done, (it & 1) ^ 1);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const uint32_t off = p_off(r, kh * 64 + g * 8);
+          st_shared_v4(spp + off, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          st_shared_v4(sds + off, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
         }
         fence_proxy_async();
         ptx::mbar_arrive(ps_full);
