@@ -9,6 +9,7 @@
 // Pipelines: smem full/empty mbarriers (TMA <-> MMA) and TMEM full/empty mbarriers
 // (MMA <-> epilogue), so the epilogue of tile i overlaps the mainloop of tile i+1.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.h"
@@ -24,10 +25,12 @@ constexpr int kThreads = 384;   // 4 control warps + 8 epilogue warps
 constexpr int kEpiWarps = 8;
 constexpr int kStageBufBytes = 32 * 64 * 2;  // one warp's [32 rows x 64 cols] bf16 TMA-store box
 
-template <int BN>
+// CG = 1: one CTA per 128 x BN tile. CG = 2: a cluster pair computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2; each CTA stages its 128 rows of A and BN/2 rows of B.
+template <int BN, int CG = 1>
 struct Cfg {
   static constexpr int kATileBytes = kBM * kBK * 2;
-  static constexpr int kBTileBytes = BN * kBK * 2;
+  static constexpr int kBTileBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
   static constexpr int kEpiBytes = kEpiWarps * 2 * kStageBufBytes;  // double-buffered per warp
   static constexpr int kStages = (232448 - kEpiBytes - 1024 - 256) / kStageBytes;
@@ -42,7 +45,7 @@ struct TileInfo {
 
 struct Sched {
   int m_tiles, n_tiles, nb1, total, split_k;
-  int M, N, K, BN, causal;
+  int M, N, K, BN, causal, tile_m;  // tile_m = 128 * CTA-group size
   __device__ TileInfo tile(int unit) const {
     TileInfo ti;
     const int split = unit % split_k;
@@ -54,14 +57,14 @@ struct Sched {
     const int nb = r - mb * n_tiles;
     ti.z1 = z % nb1;
     ti.z2 = z / nb1;
-    ti.m0 = mb * kBM;
+    ti.m0 = mb * tile_m;
     ti.n0 = nb * BN;
     int kb0 = 0, kb1 = (K + kBK - 1) / kBK;
     ti.skip = false;
     if (causal == kCausalSkipUpper) {
-      ti.skip = ti.n0 > ti.m0 + kBM - 1;
+      ti.skip = ti.n0 > ti.m0 + tile_m - 1;
     } else if (causal == kCausalKUpper) {
-      const int kend = min(K, ti.m0 + kBM);
+      const int kend = min(K, ti.m0 + tile_m);
       kb1 = (kend + kBK - 1) / kBK;
     } else if (causal == kCausalKLower) {
       kb0 = ti.m0 / kBK;
@@ -245,12 +248,13 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
   }
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, Sched sched, EpiParams ep) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
+  constexpr int BNL = BN / CG;  // B rows staged by this CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -266,6 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cr = CG == 2 ? ptx::cluster_ctarank() : 0;  // rank in the CTA pair
+  const int unit0 = blockIdx.x / CG, units = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&map_a);
@@ -277,11 +283,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 32 * kEpiWarps);
+      ptx::mbar_init(&tempty[i], 32 * kEpiWarps * CG);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  if (CG == 2) ptx::cluster_sync();  // both CTAs' barriers exist before any remote arrive / TMA
+  if (warp == 2) {
+    if (CG == 2)
+      ptx::tmem_alloc2(tmem_slot, C::kTmemCols);
+    else
+      ptx::tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -292,30 +304,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ------------------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+      auto load = [&](void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3) {
+        if (CG == 2)
+          ptx::tma_load_4d_2sm(dst, map, bar, c0, c1, c2, c3);
+        else
+          ptx::tma_load_4d(dst, map, bar, c0, c1, c2, c3);
+      };
+      for (int t = unit0; t < sched.total; t += units) {
         const TileInfo ti = sched.tile(t);
         if (ti.skip) continue;
+        const int am = ti.m0 + int(cr) * kBM;   // this CTA's A rows
+        const int bn = ti.n0 + int(cr) * BNL;   // this CTA's B rows
         for (int kb = ti.kb0; kb < ti.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          // the leader's full barrier counts both CTAs' bytes
+          if (cr == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * C::kStageBytes);
           uint8_t* sa = smem_a + stage * C::kATileBytes;
           uint8_t* sb = smem_b + stage * C::kBTileBytes;
           const int k0 = kb * kBK;
           if (A_MN) {
 #pragma unroll
             for (int j = 0; j < kBM / 64; ++j)
-              ptx::tma_load_4d(sa + j * 64 * kBK * 2, &map_a, &full[stage], ti.m0 + 64 * j, k0,
-                               ti.z1, ti.z2);
+              load(sa + j * 64 * kBK * 2, &map_a, &full[stage], am + 64 * j, k0, ti.z1, ti.z2);
           } else {
-            ptx::tma_load_4d(sa, &map_a, &full[stage], k0, ti.m0, ti.z1, ti.z2);
+            load(sa, &map_a, &full[stage], k0, am, ti.z1, ti.z2);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              ptx::tma_load_4d(sb + j * 64 * kBK * 2, &map_b, &full[stage], ti.n0 + 64 * j, k0,
-                               ti.z1, ti.z2);
+            for (int j = 0; j < BNL / 64; ++j)
+              load(sb + j * 64 * kBK * 2, &map_b, &full[stage], bn + 64 * j, k0, ti.z1, ti.z2);
           } else {
-            ptx::tma_load_4d(sb, &map_b, &full[stage], k0, ti.n0, ti.z1, ti.z2);
+            load(sb, &map_b, &full[stage], k0, bn, ti.z1, ti.z2);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -325,13 +344,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+    if (lane == 0 && cr == 0) {
+      // ------------------------------------------------------------ MMA issuer (leader CTA)
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kBM * CG, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+      for (int t = unit0; t < sched.total; t += units) {
         const TileInfo ti = sched.tile(t);
         if (ti.skip) continue;
         const int acc = local & 1;
@@ -352,15 +371,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : ptx::smem_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? ptx::smem_desc_sw128(sb + kk * 2048, 64 * kBK * 2, 1024)
                                      : ptx::smem_desc_sw128(sb + kk * 32, 16, 1024);
-            ptx::umma_bf16(d_tmem, da, db, idesc, (kb > ti.kb0 || kk > 0) ? 1u : 0u);
+            if (CG == 2)
+              ptx::umma_bf16_2sm(d_tmem, da, db, idesc, (kb > ti.kb0 || kk > 0) ? 1u : 0u);
+            else
+              ptx::umma_bf16(d_tmem, da, db, idesc, (kb > ti.kb0 || kk > 0) ? 1u : 0u);
           }
-          ptx::umma_commit(&empty[stage]);
+          if (CG == 2)
+            ptx::umma_commit_pair(&empty[stage]);
+          else
+            ptx::umma_commit(&empty[stage]);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma_commit(&tfull[acc]);
+        if (CG == 2)
+          ptx::umma_commit_pair(&tfull[acc]);
+        else
+          ptx::umma_commit(&tfull[acc]);
         ++local;
       }
     }
@@ -374,13 +402,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stage_buf = smem_epi + (warp - 4) * 2 * kStageBufBytes;
     int buf = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < sched.total; t += gridDim.x) {
+    const uint32_t tempty_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
+    for (int t = unit0; t < sched.total; t += units) {
       const TileInfo ti = sched.tile(t);
       if (ti.skip) continue;
       const int acc = local & 1;
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
-      const int row = ti.m0 + q * 32 + lane;
+      const int mrow0 = ti.m0 + int(cr) * kBM;  // this CTA's 128 accumulator rows
+      const int row = mrow0 + q * 32 + lane;
       const bool valid = row < sched.M;
       const int64_t row_off = ti.z1 * ep.cs1 + ti.z2 * ep.cs2 + int64_t(row) * ep.ldc;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(q * 32) << 16);
@@ -420,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&map_c, sb, ti.n0 + c, ti.m0 + q * 32);
+            ptx::tma_store_2d(&map_c, sb, ti.n0 + c, mrow0 + q * 32);
             ptx::bulk_commit();
           }
           buf ^= 1;
@@ -436,7 +466,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
+      if (CG == 2)
+        ptx::mbar_arrive_cluster(tempty_leader + acc * 8);  // the leader's MMA reuses this TMEM
+      else
+        ptx::mbar_arrive(&tempty[acc]);
       ++local;
     }
     if (ep.tma_store && lane == 0) ptx::bulk_wait<0>();
@@ -444,9 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (CG == 2) ptx::cluster_sync();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, C::kTmemCols);
+    if (CG == 2)
+      ptx::tmem_dealloc2(tmem_base, C::kTmemCols);
+    else
+      ptx::tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
@@ -514,22 +551,26 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
-  using C = Cfg<BN>;
-  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  using C = Cfg<BN, CG>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
+    if (CG == 2) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      (void)e;
+    }
     attr_set = true;
   }
   CUtensorMap ma, mb, mc;
   const bool ok_a = A_MN ? make_map(&ma, a.a, a.M, a.K, a.nb1, a.nb2, 64)
                          : make_map(&ma, a.a, a.K, a.M, a.nb1, a.nb2, kBM);
   const bool ok_b = B_MN ? make_map(&mb, a.b, a.N, a.K, a.nb1, a.nb2, 64)
-                         : make_map(&mb, a.b, a.K, a.N, a.nb1, a.nb2, BN);
+                         : make_map(&mb, a.b, a.K, a.N, a.nb1, a.nb2, BN / CG);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   // bf16 outputs of plain (unbatched) GEMMs go through TMA stores.
   const bool bf16_out = a.epilogue == kEpiStoreBf16 || a.epilogue == kEpiBiasBf16 ||
@@ -539,7 +580,8 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
   if (!tma_store) mc = ma;  // unused placeholder
   Sched s;
-  s.m_tiles = (a.M + kBM - 1) / kBM;
+  s.tile_m = kBM * CG;
+  s.m_tiles = (a.M + s.tile_m - 1) / s.tile_m;
   s.n_tiles = (a.N + BN - 1) / BN;
   s.nb1 = a.nb1;
   s.split_k = a.split_k > 1 ? a.split_k : 1;
@@ -561,21 +603,57 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.aux = static_cast<const __nv_bfloat16*>(a.aux);
   ep.aux_out = static_cast<__nv_bfloat16*>(a.aux_out);
   ep.tma_store = tma_store ? 1 : 0;
-  int grid = num_sms();
-  if (a.max_ctas > 0 && a.max_ctas < grid) grid = a.max_ctas;
-  if (s.total < grid) grid = s.total;
-  if (grid < 1) return cudaSuccess;
-  kern<<<grid, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, s, ep);
+  int ctas = num_sms();
+  if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
+  int units = ctas / CG;  // persistent CTAs (pairs)
+  if (s.total < units) units = s.total;
+  if (units < 1) return cudaSuccess;
+  if (CG == 1) {
+    kern<<<units, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, s, ep);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units * CG);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, s, ep);
+    if (e != cudaSuccess) return e;
+  }
   note_launch();
   return cudaGetLastError();
 }
 
+// CTA pairs (2-SM MMA, M = 256) for plain GEMMs with enough rows and N >= 128; single CTAs
+// otherwise. ZP_GEMM_PAIRS=0 forces single-CTA tiles.
+bool use_pairs(const GemmArgs& a, int BN) {
+  static int env = -1;
+  if (env < 0) {
+    const char* v = getenv("ZP_GEMM_PAIRS");
+    env = (v && v[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && BN >= 128 && a.M >= 256 && a.nb1 == 1 && a.nb2 == 1 && a.causal == kCausalNone &&
+         (a.max_ctas == 0 || a.max_ctas >= 2);
+}
+
 template <int BN>
 cudaError_t dispatch_major(const GemmArgs& a, cudaStream_t s) {
-  if (a.a.major == kKMajor && a.b.major == kKMajor) return launch<BN, 0, 0>(a, s);
-  if (a.a.major == kKMajor && a.b.major == kMNMajor) return launch<BN, 0, 1>(a, s);
-  if (a.a.major == kMNMajor && a.b.major == kKMajor) return launch<BN, 1, 0>(a, s);
-  return launch<BN, 1, 1>(a, s);
+  if (use_pairs(a, BN)) {
+    if (a.a.major == kKMajor && a.b.major == kKMajor) return launch<BN, 0, 0, 2>(a, s);
+    if (a.a.major == kKMajor && a.b.major == kMNMajor) return launch<BN, 0, 1, 2>(a, s);
+    if (a.a.major == kMNMajor && a.b.major == kKMajor) return launch<BN, 1, 0, 2>(a, s);
+    return launch<BN, 1, 1, 2>(a, s);
+  }
+  if (a.a.major == kKMajor && a.b.major == kKMajor) return launch<BN, 0, 0, 1>(a, s);
+  if (a.a.major == kKMajor && a.b.major == kMNMajor) return launch<BN, 0, 1, 1>(a, s);
+  if (a.a.major == kMNMajor && a.b.major == kKMajor) return launch<BN, 1, 0, 1>(a, s);
+  return launch<BN, 1, 1, 1>(a, s);
 }
 
 }  // namespace

@@ -129,10 +129,13 @@ __global__ void embed_bwd_k(const int32_t* tok, int seq, const bf16* dx, float* 
     const int32_t t = tok[smp * (seq + 1) + pos];
     float d[8];
     unpack8(*reinterpret_cast<const uint4*>(dx + r * h + c), d);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      atomicAdd(dwte + int64_t(t) * h + c + k, d[k]);
-      if (dwpe) atomicAdd(dwpe + int64_t(pos) * h + c + k, d[k]);
+    float4* wt = reinterpret_cast<float4*>(dwte + int64_t(t) * h + c);
+    atomicAdd(wt, make_float4(d[0], d[1], d[2], d[3]));
+    atomicAdd(wt + 1, make_float4(d[4], d[5], d[6], d[7]));
+    if (dwpe) {
+      float4* wp = reinterpret_cast<float4*>(dwpe + int64_t(pos) * h + c);
+      atomicAdd(wp, make_float4(d[0], d[1], d[2], d[3]));
+      atomicAdd(wp + 1, make_float4(d[4], d[5], d[6], d[7]));
     }
   }
 }
@@ -395,7 +398,17 @@ __global__ void sum_partials_k(const float* part, int nparts, int N, bf16* out) 
 }
 
 __global__ void cast_k(const float* in, bf16* out, int64_t n) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    uint2 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+    o2[0] = __floats2bfloat162_rn(v.x, v.y);
+    o2[1] = __floats2bfloat162_rn(v.z, v.w);
+    reinterpret_cast<uint2*>(out)[i] = o;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
     out[i] = __float2bfloat16_rn(in[i]);
 }
@@ -659,7 +672,7 @@ void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t 
   sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(part, nparts, N, out); note_launch();
 }
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
-  cast_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();
+  cast_k<<<grid_for(n / 4 + 1, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();
 }
 void reduce_sum_f32(const float* x, int64_t n, float* out, cudaStream_t s) {
   reduce_sum_k<<<1, kThreads, 0, s>>>(x, n, out); note_launch();
