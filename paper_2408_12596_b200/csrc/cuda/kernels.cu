@@ -192,52 +192,42 @@ __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
   }
 }
 
-template <int NC, bool RMS>
-__global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy,
-                                                     const bf16* __restrict__ x,
-                                                     const float* __restrict__ mean,
-                                                     const float* __restrict__ rstd,
-                                                     const bf16* __restrict__ g,
-                                                     const bf16* dres, bf16* dx, float* part,
-                                                     int64_t rows) {
-  constexpr int h = NC * 256;
-  __shared__ float sg[h], sb[h];
-  for (int i = threadIdx.x; i < h; i += kThreads) sg[i] = sb[i] = 0.f;
-  __syncthreads();
+// LayerNorm / RMSNorm backward, rows: dx = dres + rstd * (g*dy - mean(g*dy) - xhat*mean(g*dy*xhat)).
+// One warp per row, two streaming passes (sums, then dx) so no row is held in registers.
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) ln_bwd_rows_k(const bf16* __restrict__ dy,
+                                                          const bf16* __restrict__ x,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd,
+                                                          const bf16* __restrict__ g, const bf16* dres,
+                                                          bf16* dx, int64_t rows, int h) {
   const int lane = threadIdx.x & 31;
-  float accg[NC][8], accb[NC][8];
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) accg[c][k] = accb[c][k] = 0.f;
   const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
+  const float inv_h = 1.0f / h;
   for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
     const float mu = mean[r], rs = rstd[r];
-    float xh[NC][8], gd[NC][8];
+    const bf16* xr = x + r * h;
+    const bf16* dyr = dy + r * h;
     float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = (c * 32 + lane) * 8;
+    for (int col = lane * 8; col < h; col += 256) {
       float xv[8], dv[8], gg[8];
-      unpack8(*reinterpret_cast<const uint4*>(x + r * h + col), xv);
-      unpack8(*reinterpret_cast<const uint4*>(dy + r * h + col), dv);
+      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
       unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        xh[c][k] = (xv[k] - mu) * rs;
-        gd[c][k] = gg[k] * dv[k];
-        s1 += gd[c][k];
-        s2 += gd[c][k] * xh[c][k];
-        accg[c][k] += dv[k] * xh[c][k];
-        accb[c][k] += dv[k];
+        const float gd = gg[k] * dv[k];
+        s1 += gd;
+        s2 += gd * (xv[k] - mu) * rs;
       }
     }
-    const float m1 = RMS ? 0.f : warp_sum(s1) * (1.0f / h);
-    const float m2 = warp_sum(s2) * (1.0f / h);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int col = (c * 32 + lane) * 8;
-      float o[8], rr[8];
+    const float m1 = RMS ? 0.f : warp_sum(s1) * inv_h;
+    const float m2 = warp_sum(s2) * inv_h;
+    for (int col = lane * 8; col < h; col += 256) {
+      float xv[8], dv[8], gg[8], rr[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
       if (dres) {
         unpack8(*reinterpret_cast<const uint4*>(dres + r * h + col), rr);
       } else {
@@ -245,30 +235,55 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_k(const bf16* __restrict__ dy
         for (int k = 0; k < 8; ++k) rr[k] = 0.f;
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) o[k] = rr[k] + rs * (gd[c][k] - m1 - xh[c][k] * m2);
+      for (int k = 0; k < 8; ++k) o[k] = rr[k] + rs * (gg[k] * dv[k] - m1 - (xv[k] - mu) * rs * m2);
       *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
     }
   }
-  // Fold the 8 warps' column partials into shared memory one warp at a time (plain
-  // read-modify-write, no shared atomics: lanes own disjoint 8-column groups).
-  const int w = threadIdx.x / 32;
-  for (int turn = 0; turn < kThreads / 32; ++turn) {
-    if (w == turn) {
+}
+
+// dgamma / dbeta partial column sums over a chunk of rows: block (32, 8) covers 256 columns.
+// part[chunk][h] holds dgamma partials, part[nchunks + chunk][h] dbeta partials.
+template <bool RMS>
+__global__ void ln_bwd_cols_k(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                              const float* __restrict__ mean, const float* __restrict__ rstd, int64_t rows,
+                              int h, int64_t chunk, float* part) {
+  __shared__ float sg[8][256], sb[8][256];
+  const int c = blockIdx.x * 256 + threadIdx.x * 8;
+  const int64_t r0 = blockIdx.y * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  float ag[8], ab[8];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const int col = (c * 32 + lane) * 8;
+  for (int k = 0; k < 8; ++k) ag[k] = ab[k] = 0.f;
+  if (c < h) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      const float mu = mean[r], rs = rstd[r];
+      float xv[8], dv[8];
+      unpack8(*reinterpret_cast<const uint4*>(x + r * h + c), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dy + r * h + c), dv);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          sg[col + k] += accg[c][k];
-          sb[col + k] += accb[c][k];
-        }
+      for (int k = 0; k < 8; ++k) {
+        ag[k] += dv[k] * (xv[k] - mu) * rs;
+        ab[k] += dv[k];
       }
     }
-    __syncthreads();
   }
-  for (int i = threadIdx.x; i < h; i += kThreads) {
-    part[int64_t(blockIdx.x) * h + i] = sg[i];
-    part[int64_t(gridDim.x + blockIdx.x) * h + i] = sb[i];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    sg[threadIdx.y][threadIdx.x * 8 + k] = ag[k];
+    sb[threadIdx.y][threadIdx.x * 8 + k] = ab[k];
+  }
+  __syncthreads();
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int col = blockIdx.x * 256 + t;
+  if (col < h) {
+    float a = 0.f, bsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a += sg[k][t];
+      bsum += sb[k][t];
+    }
+    part[int64_t(blockIdx.y) * h + col] = a;
+    if (!RMS) part[int64_t(gridDim.y + blockIdx.y) * h + col] = bsum;
   }
 }
 
@@ -287,19 +302,22 @@ __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
   return sh[0];
 }
 
-// Combines two (max, sum-of-exp) pairs of an online softmax.
+// Combines two (max, sum-of-exp2) pairs of an online softmax in the log2 domain.
 __device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
   const float mx = fmaxf(m, m2);
-  s = (m == -INFINITY ? 0.f : s * __expf(m - mx)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mx));
+  s = (m == -INFINITY ? 0.f : s * exp2f(m - mx)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mx));
   m = mx;
 }
 
-// One CTA per row: pass 1 computes the row's max and sum of exp online (one read of the
-// logits), pass 2 overwrites the logits with (softmax - onehot) * gscale.
+// One CTA per row. Pass 1: per-thread online max / sum of exp2 in the log2 domain (one read of
+// the logits, one exp2 per element, a rescale only when the running max grows). Pass 2:
+// overwrite the logits with (softmax - onehot) * gscale (one exp2 per element).
 __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* tok, int seq, int64_t rows,
                                                  int vocab, int ldv, float gscale, float* row_loss) {
+  constexpr float kL2e = 1.4426950408889634f;
   __shared__ float shm[kThreads / 32], shs[kThreads / 32];
   const int nvec = ldv / 8;
+  const int nfull = vocab / 8;  // chunks entirely inside the vocabulary
   const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     bf16* lg = logits + r * ldv;
@@ -311,15 +329,26 @@ __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* to
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
       float cm = -INFINITY;
+      if (i < nfull) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (i * 8 + k < vocab) cm = fmaxf(cm, f[k]);
+        for (int k = 0; k < 8; ++k) {
+          f[k] *= kL2e;
+          cm = fmaxf(cm, f[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          f[k] = (i * 8 + k < vocab) ? f[k] * kL2e : -INFINITY;
+          cm = fmaxf(cm, f[k]);
+        }
+      }
       if (cm == -INFINITY) continue;
-      float cs = 0.f;
+      if (cm > m) {
+        sum = (m == -INFINITY) ? 0.f : sum * exp2f(m - cm);
+        m = cm;
+      }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (i * 8 + k < vocab) cs += __expf(f[k] - cm);
-      lse_merge(m, sum, cm, cs);
+      for (int k = 0; k < 8; ++k) sum += exp2f(f[k] - m);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -336,18 +365,18 @@ __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* to
     m = shm[0];
     sum = shs[0];
     for (int k = 1; k < kThreads / 32; ++k) lse_merge(m, sum, shm[k], shs[k]);
-    const float lse = m + logf(sum);
+    const float lse = (m + log2f(sum)) / kL2e;  // natural log-sum-exp
     const float tl = __bfloat162float(lg[target]);
     __syncthreads();  // everyone has read lg[target] before it is overwritten
-    const float inv = 1.0f / sum;
+    const float coef = gscale / sum;
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(lg + i * 8), f);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int col = i * 8 + k;
-        float gv = 0.f;
-        if (col < vocab) gv = (__expf(f[k] - m) * inv - (col == target ? 1.f : 0.f)) * gscale;
+        float gv = (i < nfull || col < vocab) ? exp2f(f[k] * kL2e - m) * coef : 0.f;
+        if (col == target) gv -= gscale;
         f[k] = gv;
       }
       *reinterpret_cast<uint4*>(lg + i * 8) = pack8(f);
@@ -389,12 +418,20 @@ __global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_
   }
 }
 
+// out[c] = sum over k of part[k, c]: block (32 columns x 8 row stripes), coalesced 128-byte rows.
 __global__ void sum_partials_k(const float* part, int nparts, int N, bf16* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
+  __shared__ float sh[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
-  for (int k = 0; k < nparts; ++k) s += part[int64_t(k) * N + c];
-  out[c] = __float2bfloat16_rn(s);
+  if (c < N)
+    for (int k = threadIdx.y; k < nparts; k += 8) s += part[int64_t(k) * N + c];
+  sh[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < N) {
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s += sh[k][threadIdx.x];
+    out[c] = __float2bfloat16_rn(s);
+  }
 }
 
 __global__ void cast_k(const float* in, bf16* out, int64_t n) {
@@ -633,22 +670,25 @@ cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, 
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
                           int64_t rows, int h, int ctas, cudaStream_t s, bool rms) {
-  const int grid = grid_for(rows, kThreads / 32, ctas, 2);
-  *nblk = grid;
-  switch (h / 256) {
-#define X(NC)                                                                              \
-  case NC:                                                                                 \
-    if (h % 256) return cudaErrorInvalidValue;                                             \
-    if (rms)                                                                               \
-      ln_bwd_k<NC, true><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); \
-    else                                                                                   \
-      ln_bwd_k<NC, false><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, part, rows); note_launch();    \
-    return cudaGetLastError();
-    ZP_LN_CASES(X)
-#undef X
-    default:
-      return cudaErrorInvalidValue;
-  }
+  if (h % 256) return cudaErrorInvalidValue;
+  const int grid = grid_for(rows, kThreads / 32, ctas, 8);
+  if (rms)
+    ln_bwd_rows_k<true><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h);
+  else
+    ln_bwd_rows_k<false><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h);
+  note_launch();
+  const int col_blocks = h / 256;
+  int chunks = (ctas * 4 + col_blocks - 1) / col_blocks;
+  if (chunks > 4 * 148) chunks = 4 * 148;
+  const int64_t chunk = (rows + chunks - 1) / chunks;
+  chunks = int((rows + chunk - 1) / chunk);
+  *nblk = chunks;
+  if (rms)
+    ln_bwd_cols_k<true><<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(dy, x, mean, rstd, rows, h, chunk, part);
+  else
+    ln_bwd_cols_k<false><<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(dy, x, mean, rstd, rows, h, chunk, part);
+  note_launch();
+  return cudaGetLastError();
 }
 
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
@@ -666,10 +706,10 @@ void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* 
   const int64_t chunk = (rows + chunks - 1) / chunks;
   chunks = int((rows + chunk - 1) / chunk);
   colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work); note_launch();
-  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, out); note_launch();
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(work, chunks, N, out); note_launch();
 }
 void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s) {
-  sum_partials_k<<<(N + 255) / 256, 256, 0, s>>>(part, nparts, N, out); note_launch();
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(part, nparts, N, out); note_launch();
 }
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
   cast_k<<<grid_for(n / 4 + 1, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();

@@ -469,7 +469,7 @@ struct Runtime {
     dwte32 = F32(int64_t(vocab_pad) * h, "dwte");
     dwpe32 = F32(int64_t(c.seq_len) * h, "dwpe");
     wgrad32 = F32(std::max<int64_t>(3 * h, 2 * int64_t(c.d_ff)) * h, "wgrad");
-    ln_part = F32(int64_t(2) * 2 * 148 * h, "ln partials");
+    ln_part = F32(int64_t(2) * 4 * 148 * h, "ln partials");
     const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
     col_work = F32(256 * maxN, "colsum work");
     loss_steps = F32(kMaxSteps, "loss");
