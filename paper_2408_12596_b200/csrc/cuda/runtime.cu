@@ -13,10 +13,14 @@
 // Z1 reduce-scatter + all-gather at sync; Z2 bf16 reduce-scatter every micro-step + all-gather
 // of updated parameters at sync; Z3 adds the forward/backward parameter all-gathers. The
 // optimizer is AdamW on the rank's shard, fused with the shard's gradient accumulation.
+// With NVLink peer access (the default when every rank can map every other rank's arena),
+// the Z1/Z2 reduce-scatters are peer-memory pulls and the synchronisation point is one kernel:
+// reduce-scatter + AdamW + all-gather (peer.cu). ZP_PEER=0 selects the NCCL path instead.
 #include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -27,6 +31,7 @@
 #include "attention.h"
 #include "gemm.h"
 #include "kernels.h"
+#include "peer.h"
 
 namespace zp {
 namespace {
@@ -245,6 +250,13 @@ struct Runtime {
   ncclComm_t comm = nullptr;
   Layout lay;
   Arena arena;
+  // NVLink peer-memory collectives (peer.h): every rank's arena and flag block mapped here
+  PeerView pv;
+  bool peer = false;
+  uint32_t epoch = 0;
+  PeerFlags* flags = nullptr;
+  std::vector<void*> ipc_open;
+  int64_t off(const void* p) const { return static_cast<const char*>(p) - arena.base; }
   int stage = -1;
   size_t resident_mark = 0;
   int64_t adam_t = 0;
@@ -776,6 +788,78 @@ struct Runtime {
     tm.close(kComm, s0, st);
   }
 
+  // Map every rank's arena and flag block (CUDA IPC handles exchanged over NCCL). All ranks
+  // agree on the outcome; any failure leaves the NCCL path in place.
+  void setup_peers() {
+    const char* env = std::getenv("ZP_PEER");
+    if (n < 2 || n > kMaxPeers || (env && env[0] == '0')) return;
+    struct Handles {
+      cudaIpcMemHandle_t arena, flags;
+      int ok;
+    };
+    CK(cudaMalloc(&flags, sizeof(PeerFlags)));
+    CK(cudaMemset(flags, 0, sizeof(PeerFlags)));
+    Handles mine{};
+    mine.ok = cudaIpcGetMemHandle(&mine.arena, arena.base) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.flags, flags) == cudaSuccess;
+    cudaGetLastError();
+    std::vector<Handles> all(n);
+    void* dbuf = nullptr;
+    CK(cudaMalloc(&dbuf, sizeof(Handles) * (n + 1)));
+    char* dsrc = static_cast<char*>(dbuf) + sizeof(Handles) * n;
+    CK(cudaMemcpyAsync(dsrc, &mine, sizeof(Handles), cudaMemcpyHostToDevice, st));
+    NK(ncclAllGather(dsrc, dbuf, sizeof(Handles), ncclUint8, comm, st));
+    CK(cudaMemcpyAsync(all.data(), dbuf, sizeof(Handles) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaFree(dbuf));
+    int ok = 1;
+    pv.n = n;
+    pv.rank = rank;
+    for (int j = 0; j < n; ++j) {
+      ok &= all[j].ok;
+      if (j == rank) {
+        pv.base[j] = arena.base;
+        pv.flags[j] = flags;
+        continue;
+      }
+      if (!ok) break;
+      void* a = nullptr;
+      void* f = nullptr;
+      if (cudaIpcOpenMemHandle(&a, all[j].arena, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+          cudaIpcOpenMemHandle(&f, all[j].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        if (a) cudaIpcCloseMemHandle(a);
+        ok = 0;
+        break;
+      }
+      ipc_open.push_back(a);
+      ipc_open.push_back(f);
+      pv.base[j] = static_cast<char*>(a);
+      pv.flags[j] = static_cast<PeerFlags*>(f);
+    }
+    peer = agree(ok, ncclMin) == 1;
+    if (!peer) close_peers();
+  }
+  void close_peers() {
+    for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
+    ipc_open.clear();
+    peer = false;
+  }
+  // Z2 micro-step: acc (=|+=) sum over ranks of their bf16 gradients of this rank's shard.
+  void peer_reduce_accumulate(bool overwrite) {
+    const int s0 = tm.mark(st);
+    CK(peer_rs_accumulate(pv, off(g16), shard_begin(), acc, shard(), overwrite, ++epoch, ctas, st));
+    tm.close(kComm, s0, st);
+  }
+  // Synchronisation point: pull-reduce the shard (bf16 Z2 gradients or fp32 Z1 accumulators),
+  // AdamW, push the new bf16 shard into every rank's parameter buffer.
+  void peer_sync(const void* src, bool f32, const float* a, const AdamParams& ap) {
+    const int s0 = tm.mark(st);
+    CK(peer_rs_adam_ag(pv, off(src), f32, shard_begin(), a, p32, m32, v32, off(p16), gkeep, shard(), ap, ++epoch,
+                       ctas, st));
+    tm.close(kComm, s0, st);
+  }
+
   AdamParams adam_params() {
     ++adam_t;
     AdamParams a;
@@ -840,6 +924,8 @@ struct Runtime {
           accumulate_bf16(acc, g16, total, !any_local, ctas, st);
           any_local = true;
         }
+      } else if (stage == 2 && peer) {  // Z2 over NVLink: pull-reduce into the fp32 shard
+        if (!last) peer_reduce_accumulate(k == 0);
       } else if (stage == 2) {  // Z2: reduce-scatter every micro-step
         bf16* src = (n == 1) ? g16 : r16;
         reduce_scatter_bf16(g16, r16);
@@ -853,7 +939,14 @@ struct Runtime {
     // ---- synchronisation point + optimizer
     const AdamParams ap = adam_params();
     const int64_t L = state_len();
-    if (stage == 0) {
+    if (peer && (stage == 1 || stage == 2)) {
+      // one kernel: reduce-scatter (+ the fp32 accumulation of earlier micro-steps) + AdamW +
+      // all-gather; the optimizer time is inside this collective's span
+      if (stage == 1)
+        peer_sync(acc, true, nullptr, ap);
+      else
+        peer_sync(g16, false, steps.size() > 1 ? acc : nullptr, ap);
+    } else if (stage == 0) {
       if (n > 1) all_reduce_f32(acc, total);
       if (gkeep) CK(cudaMemcpyAsync(gkeep, acc, size_t(total) * 4, cudaMemcpyDeviceToDevice, st));
       const int o0 = tm.mark(st);
@@ -1171,6 +1264,7 @@ int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
         ncclUniqueId id;
         std::memcpy(id.internal, desc->nccl_id, 128);
         NK(ncclCommInitRank(&R.comm, R.n, id, R.rank));
+        R.setup_peers();
       }
       R.tm.init(8192);
     } catch (...) {
@@ -1186,6 +1280,8 @@ int zp_runtime_destroy(zp_runtime* h) {
   if (!h) return ZP_OK;
   zp::Runtime& R = h->rt;
   cudaStreamSynchronize(R.st);
+  R.close_peers();
+  if (R.flags) cudaFree(R.flags);
   if (R.comm) ncclCommDestroy(R.comm);
   R.tm.destroy();
   R.gtm.destroy();
@@ -1313,6 +1409,11 @@ int zp_runtime_owned_ranges(zp_runtime* h, int64_t* triples, int32_t cap, int32_
     }
     return ZP_OK;
   });
+}
+
+int zp_runtime_peer_collectives(zp_runtime* h, int32_t* on) {
+  *on = h->rt.peer ? 1 : 0;
+  return ZP_OK;
 }
 
 int zp_runtime_keep_grads(zp_runtime* h, int32_t on) {

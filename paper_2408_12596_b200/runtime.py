@@ -60,6 +60,7 @@ _SIGS = {
     "zp_runtime_get_params_bf16": ([_P, _P], C.c_int),
     "zp_runtime_set_params": ([_P, _P], C.c_int),
     "zp_runtime_keep_grads": ([_P, C.c_int32], C.c_int),
+    "zp_runtime_peer_collectives": ([_P, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_owned_ranges": ([_P, C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_tensor_info": ([_P, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)], C.c_int),
@@ -207,6 +208,12 @@ class Runtime:
     # ---- state
     def keep_grads(self, on=True):
         _check(lib.zp_runtime_keep_grads(self.h, 1 if on else 0))
+
+    def peer_collectives(self) -> bool:
+        """True when the ZeRO-1/2 collectives run over NVLink peer memory (peer.cu)."""
+        on = C.c_int32(0)
+        _check(lib.zp_runtime_peer_collectives(self.h, C.byref(on)))
+        return bool(on.value)
 
     def get_state(self, kind: int):
         """kind 0 master, 1 m, 2 v, 3 summed grad. Returns (begin, end, float32 array)."""

@@ -1,7 +1,11 @@
 """Two-rank heterogeneous ZeRO on 2 GPUs (NCCL over NVLink): unequal per-rank micro-batches
 with the b_i/B weighting must reproduce the single-device float64 oracle step on the union of
 the samples, for ZeRO-0 (all-reduce), ZeRO-1 (fp32 reduce-scatter + all-gather) and ZeRO-2
-(bf16 reduce-scatter every micro-step + all-gather). Skipped with fewer than 2 GPUs."""
+(bf16 reduce-scatter every micro-step + all-gather), ZeRO-3 (per-group gathers and
+reduce-scatters). ZeRO-1/2 run twice: over NVLink peer memory (pull reduce-scatter, and the
+fused reduce-scatter + AdamW + push all-gather kernel of peer.cu) and over NCCL (ZP_PEER=0).
+The updated fp32 master must equal one float64 AdamW step on the summed gradient. Skipped with
+fewer than 2 GPUs."""
 import numpy as np
 import pytest
 
@@ -17,8 +21,10 @@ def _plan(stage, devs, gas):
                 predicted_wall_time=0.0)
 
 
-def _worker(rank, world, q_in, q_out, stage, plan, tokens):
+def _worker(rank, world, q_in, q_out, stage, plan, tokens, peer=True):
     try:
+        import os
+        os.environ["ZP_PEER"] = "1" if peer else "0"
         from paper_2408_12596_b200.runtime import Runtime, GPT, nccl_unique_id, bf16_to_f32
         nid = nccl_unique_id() if rank == 0 else None
         if rank == 0:
@@ -37,16 +43,18 @@ def _worker(rank, world, q_in, q_out, stage, plan, tokens):
         t = rt.execute_iteration(plan, stage)
         g, mask = rt.state_flat(3)
         after = rt.state_flat(0)[0] if stage == 3 else rt.params_bf16()
+        master = rt.state_flat(0)[0]
         layout = {n: rt.tensor_info(n) for n in rt.tensor_names()}  # offsets depend on world size
-        q_out.put((rank, "ok", mask, layout, g, (m0, mask0), after, t["loss_sum"], len(t["coll_times"])))
+        q_out.put((rank, "ok", mask, layout, g, (m0, mask0), after, t["loss_sum"], len(t["coll_times"]),
+                   master, rt.peer_collectives()))
         rt.close()
     except Exception as ex:  # pragma: no cover
         import traceback
-        q_out.put((rank, traceback.format_exc(), None, None, None, None, None, None, None))
+        q_out.put((rank, traceback.format_exc(), None, None, None, None, None, None, None, None, None))
 
 
-@pytest.mark.parametrize("stage", [0, 1, 2, 3])
-def test_two_rank_hetero_step_matches_oracle(stage):
+@pytest.mark.parametrize("stage,peer", [(0, True), (1, True), (1, False), (2, True), (2, False), (3, True)])
+def test_two_rank_hetero_step_matches_oracle(stage, peer):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -62,7 +70,7 @@ def test_two_rank_hetero_step_matches_oracle(stage):
     tokens = np.random.default_rng(3).integers(0, TINY["vocab"], (B, TINY["seq_len"] + 1)).astype(np.int32)
     ctx = mp.get_context("spawn")
     q_in, q_out = ctx.Queue(), ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, q_in, q_out, stage, plan, tokens)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, q_in, q_out, stage, plan, tokens, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q_out.get(timeout=300) for _ in procs], key=lambda r: r[0])
@@ -90,6 +98,14 @@ def test_two_rank_hetero_step_matches_oracle(stage):
     # all ranks end the iteration with identical bf16 parameters (Z0-2, gathered)
     if stage < 3:
         assert np.array_equal(res[0][6], res[1][6])
+    # the fused optimizer: new master == one float64 AdamW step (t=1) on the summed gradient
+    m0 = np.where(k0a, m0a, m0b).astype(np.float64) if stage else m0a.astype(np.float64)
+    exp, _, _ = so.adamw(m0, 0.0, 0.0, g.astype(np.float64), 1, 1e-3, 0.9, 0.95, 1e-8, 0.0)
+    master = res[0][9] if stage == 0 else np.where(res[0][2], res[0][9], res[1][9])
+    assert so.rel_err(master, exp) < 1e-6
+    # the collective path that actually ran
+    if stage in (1, 2):
+        assert res[0][10] == res[1][10] == peer
 
 
 def _unflat(flat, layout):
