@@ -345,7 +345,7 @@ def main():
                                 "gmbs": [d["gmbs"] for d in plan["devices"]], "gas": plan["gas"]},
                        "mbs": [d["mbs"] for d in profile["devices"]],
                        "profile_seconds": t_profile, "parallelism": f"zero{stage}-dp{world}",
-                       "collectives": ("nvlink-peer (pull RS; fused RS+AdamW+AG)" if rt.peer_collectives() else "nccl") if world > 1 else "none",
+                       "collectives": (("nvlink-peer (pull RS/AG; fused RS+AdamW+AG at sync)" if stage in (1, 2) else "nvlink-peer (pull RS/AG)" if stage == 3 else "nccl (all-reduce)") if rt.peer_collectives() else "nccl") if world > 1 else "none",
                        "l2": "inputs larger than L2 (per-step activations are tens of GB)"},
             "sync_idle_pct": report["sync_idle_pct"],
             "uniform_split": {"value": uniform_value, "poplar_speedup": value / uniform_value,

@@ -103,8 +103,9 @@ int zp_runtime_get_state(zp_runtime* rt, int32_t kind, float* out, int64_t* begi
 int zp_runtime_get_params_bf16(zp_runtime* rt, uint16_t* out); /* full bf16 params (Z3: owned slices) */
 int zp_runtime_set_params(zp_runtime* rt, const float* full_fp32); /* resets master + bf16 copy */
 int zp_runtime_keep_grads(zp_runtime* rt, int32_t on);
-/* *on = 1 when the ZeRO-1/2 collectives run over NVLink peer memory (CUDA IPC mappings of every
- * rank's arena: pull reduce-scatter and the fused reduce-scatter + AdamW + all-gather kernel),
+/* *on = 1 when the ZeRO-1/2/3 collectives run over NVLink peer memory (CUDA IPC mappings of every
+ * rank's arena: pull reduce-scatter and all-gather, and the fused reduce-scatter + AdamW +
+ * all-gather kernel at the ZeRO-1/2 synchronisation point),
  * 0 when they run over NCCL (world size 1, ZP_PEER=0, or a rank that cannot map its peers). */
 int zp_runtime_peer_collectives(zp_runtime* rt, int32_t* on);
 /* Flat-layout ranges this rank owns, as (flat_begin, flat_end, shard_begin) triples: one range

@@ -569,16 +569,24 @@ struct Runtime {
     if (stage != 3 || n == 1) return;
     const Group& G = lay.groups[g];
     const int s0 = tm.mark(st);
-    NK(ncclAllGather(p16s + shoff[g], gather_dst(g), size_t(G.len / n), ncclBfloat16, comm, st));
+    if (peer)
+      CK(peer_all_gather(pv, off(p16s + shoff[g]), gather_dst(g), G.len / n, ++epoch, ctas, st));
+    else
+      NK(ncclAllGather(p16s + shoff[g], gather_dst(g), size_t(G.len / n), ncclBfloat16, comm, st));
     tm.close(kind, s0, st);
   }
   void z3_reduce(int g) {
     if (stage != 3 || n == 1) return;
     const Group& G = lay.groups[g];
     const int s0 = tm.mark(st);
-    NK(ncclReduceScatter(ggrp, r16 + shoff[g], size_t(G.len / n), ncclBfloat16, ncclSum, comm, st));
+    if (peer)  // pull-reduce straight into the fp32 shard accumulator (no bf16 round trip)
+      CK(peer_rs_accumulate(pv, off(ggrp), (G.len / n) * rank, acc + shoff[g], G.len / n, z3_first, ++epoch,
+                            ctas, st));
+    else
+      NK(ncclReduceScatter(ggrp, r16 + shoff[g], size_t(G.len / n), ncclBfloat16, ncclSum, comm, st));
     tm.close(kRs, s0, st);
   }
+  bool z3_first = true;  // ZeRO-3 peer path: the current micro-step is the iteration's first
   // Zero the reused group-gradient buffer so padding never carries another group's values.
   void z3_clear_group(int g) {
     if (stage != 3 || n == 1) return;
@@ -899,6 +907,7 @@ struct Runtime {
         }
       }
       const bool last = (k + 1 == steps.size());
+      z3_first = (k == 0);
       if (b > 0) {
         const int32_t* tok = tokens + sample * (c.seq_len + 1);
         const int f0 = tm.mark(st);
@@ -930,7 +939,7 @@ struct Runtime {
         bf16* src = (n == 1) ? g16 : r16;
         reduce_scatter_bf16(g16, r16);
         if (!last) accumulate_bf16(acc, src, sh, k == 0, ctas, st);
-      } else {  // Z3: the per-group reduce-scatters already landed in r16 during backward
+      } else if (!(peer && n > 1)) {  // Z3: the per-group reduce-scatters landed in r16 in backward
         if (!last) accumulate_bf16(acc, r16, sh, k == 0, ctas, st);
       }
     }
@@ -964,11 +973,16 @@ struct Runtime {
       tm.close(kOpt, o0, st);
       all_gather_params();
     } else {
-      const bf16* g = (stage == 2 && n == 1) ? g16 : r16;
-      const float* a = steps.size() > 1 ? acc : nullptr;
+      const bool z3peer = stage == 3 && peer;  // every micro-step already summed into acc (fp32)
+      const bf16* g = z3peer ? nullptr : ((stage == 2 && n == 1) ? g16 : r16);
+      const float* a = (steps.size() > 1 || z3peer) ? acc : nullptr;
       if (gkeep) {
-        accumulate_bf16(gkeep, g, L, true, ctas, st);
-        if (a) add_f32(gkeep, a, L, ctas, st);
+        if (g) {
+          accumulate_bf16(gkeep, g, L, true, ctas, st);
+          if (a) add_f32(gkeep, a, L, ctas, st);
+        } else {
+          CK(cudaMemcpyAsync(gkeep, a, size_t(L) * 4, cudaMemcpyDeviceToDevice, st));
+        }
       }
       const int o0 = tm.mark(st);
       adam_update(p32, m32, v32, stage == 3 ? p16s : p16 + shard_begin(), a, g, nullptr, L, ap, ctas, st);
