@@ -38,7 +38,7 @@ typedef struct zp_gemm_desc {
   const void* aux;
   void* aux_out;
   int32_t max_ctas;
-  int32_t split_k;  /* > 1 splits the K range across CTAs; needs epilogue 7 (fp32 atomic add) */
+  int32_t split_k;  /* > 1 splits the K range across CTAs, -1 picks the split for full waves; needs epilogue 7 (fp32 atomic add) */
 } zp_gemm_desc;
 
 int zp_gemm(const zp_gemm_desc* d, void* stream);

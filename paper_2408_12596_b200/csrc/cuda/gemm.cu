@@ -38,6 +38,8 @@ struct Cfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+constexpr int kGroupM = 8;
+
 struct TileInfo {
   int z1, z2, m0, n0, kb0, kb1;
   bool skip;
@@ -53,8 +55,14 @@ struct Sched {
     const int per_batch = m_tiles * n_tiles;
     const int z = t / per_batch;
     const int r = t - z * per_batch;
-    const int mb = r / n_tiles;
-    const int nb = r - mb * n_tiles;
+    // grouped raster: runs of kGroupM m-tiles sweep the n-tiles together, so the tiles in flight
+    // at any time share a few A row-blocks and B column-blocks (L2 reuse for large N, e.g. the
+    // LM head)
+    const int first_m = (r / (kGroupM * n_tiles)) * kGroupM;
+    const int gsize = min(kGroupM, m_tiles - first_m);
+    const int rr = r - first_m * n_tiles;
+    const int mb = first_m + rr % gsize;
+    const int nb = rr / gsize;
     ti.z1 = z % nb1;
     ti.z2 = z / nb1;
     ti.m0 = mb * tile_m;
@@ -584,9 +592,30 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   s.m_tiles = (a.M + s.tile_m - 1) / s.tile_m;
   s.n_tiles = (a.N + BN - 1) / BN;
   s.nb1 = a.nb1;
+  int ctas = num_sms();
+  if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
+  const int workers = ctas / CG;  // persistent CTAs (pairs)
+  const int tiles = s.m_tiles * s.n_tiles * a.nb1 * a.nb2;
   s.split_k = a.split_k > 1 ? a.split_k : 1;
+  if (a.split_k < 0) {
+    // auto split-K: the split count whose work units fill the persistent CTAs in the fewest,
+    // fullest waves (ties to the smaller split), keeping >= 8 k-blocks per unit
+    const int kblocks = (a.K + kBK - 1) / kBK;
+    const int max_split = kblocks / 8 < 64 ? kblocks / 8 : 64;
+    double best = -1.0;
+    for (int sp = 1; sp <= max_split; ++sp) {
+      const int u = tiles * sp;
+      const int waves = (u + workers - 1) / workers;
+      // efficiency of the last wave, discounted by a small per-split atomic overhead
+      const double eff = double(u) / double(waves * workers) - 0.004 * sp;
+      if (eff > best + 1e-9) {
+        best = eff;
+        s.split_k = sp;
+      }
+    }
+  }
   if (s.split_k > 1 && a.epilogue != kEpiAtomicF32) return cudaErrorInvalidValue;
-  s.total = s.m_tiles * s.n_tiles * a.nb1 * a.nb2 * s.split_k;
+  s.total = tiles * s.split_k;
   s.M = a.M;
   s.N = a.N;
   s.K = a.K;
@@ -603,9 +632,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.aux = static_cast<const __nv_bfloat16*>(a.aux);
   ep.aux_out = static_cast<__nv_bfloat16*>(a.aux_out);
   ep.tma_store = tma_store ? 1 : 0;
-  int ctas = num_sms();
-  if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
-  int units = ctas / CG;  // persistent CTAs (pairs)
+  int units = workers;
   if (s.total < units) units = s.total;
   if (units < 1) return cudaSuccess;
   if (CG == 1) {

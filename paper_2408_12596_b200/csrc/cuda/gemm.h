@@ -55,7 +55,7 @@ struct GemmArgs {
   const void* aux = nullptr;   // bf16, same layout as C (residual R or pre-activation U)
   void* aux_out = nullptr;     // bf16, same layout as C (U written by kEpiBiasGeluBf16)
   int max_ctas = 0;            // SM budget cap (0 = all SMs)
-  int split_k = 1;             // >1: K range split across CTAs; requires kEpiAtomicF32
+  int split_k = 1;             // >1: K range split across CTAs; -1: auto; requires kEpiAtomicF32
 };
 
 // Returns cudaSuccess or the launch/encode error.

@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace zp {
 namespace {
@@ -29,21 +30,24 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+__device__ __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
+  lo = __uint_as_float(w << 16);
+  hi = __uint_as_float(w & 0xffff0000u);
+}
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 t = __bfloat1622float2(h[i]);
-    f[2 * i] = t.x;
-    f[2 * i + 1] = t.y;
-  }
+  unpack2(u.x, f[0], f[1]);
+  unpack2(u.y, f[2], f[3]);
+  unpack2(u.z, f[4], f[5]);
+  unpack2(u.w, f[6], f[7]);
+}
+// (lo, hi) -> bf16x2 in one cvt, kept in registers (no address-taken temporaries)
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
-  uint4 u;
-  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
-  return u;
+  return make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
 }
 
 int grid_for(int64_t work_items, int per_block, int ctas, int per_sm = 4) {
@@ -303,6 +307,12 @@ __device__ __forceinline__ float block_reduce(float v, float* sh, bool is_max) {
 }
 
 // Combines two (max, sum-of-exp2) pairs of an online softmax in the log2 domain.
+__device__ __forceinline__ float ex2_fast(float x) {  // MUFU.EX2 (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
   const float mx = fmaxf(m, m2);
   s = (m == -INFINITY ? 0.f : s * exp2f(m - mx)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mx));
@@ -382,6 +392,117 @@ __global__ void __launch_bounds__(kThreads) ce_k(bf16* logits, const int32_t* to
       *reinterpret_cast<uint4*>(lg + i * 8) = pack8(f);
     }
     if (threadIdx.x == 0) row_loss[r] = lse - tl;
+  }
+}
+
+// Rows that fit twice in shared memory (vocab up to ~56K): one persistent CTA per SM streams
+// rows through two smem buffers with bulk copies (the next row loads while this one is
+// processed), so the logits are read from HBM once and the gradient written once. Pass 1 (online
+// max / sum of exp2) and pass 2 (gradient) both read the row from shared memory.
+constexpr int kCeThreads = 512;
+__global__ void __launch_bounds__(kCeThreads, 1) ce_smem_k(bf16* logits, const int32_t* tok, int seq, int64_t rows,
+                                                           int vocab, int ldv, float gscale, float* row_loss) {
+  constexpr float kL2e = 1.4426950408889634f;
+  extern __shared__ __align__(128) uint8_t ce_smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ float shm[kCeThreads / 32], shs[kCeThreads / 32];
+  const uint32_t row_bytes = uint32_t(ldv) * 2;
+  const uint32_t stride = (row_bytes + 127) & ~127u;
+  const int nvec = ldv / 8, nfull = vocab / 8;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t r, int buf) {
+    ptx::mbar_arrive_expect_tx(&bar[buf], row_bytes);
+    ptx::bulk_load(ce_smem + buf * stride, logits + r * ldv, row_bytes, &bar[buf]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < rows) issue(blockIdx.x, 0);
+  uint32_t it = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+    const int buf = it & 1;
+    if (threadIdx.x == 0 && r + gridDim.x < rows) issue(r + gridDim.x, buf ^ 1);
+    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
+    const uint4* row = reinterpret_cast<const uint4*>(ce_smem + buf * stride);
+    const int64_t smp = r / seq;
+    const int pos = int(r % seq);
+    const int target = tok[smp * (seq + 1) + pos + 1];
+    // One MUFU exp2 per element: pass 1 takes the row max (packed bf16x2 max, order-preserving
+    // under the positive log2(e) scale); pass 2 computes e = exp2(x*log2e - max), sums it and
+    // stores it in place as bf16; pass 3 writes (e / sum - onehot) * gscale.
+    float tl = 0.f;
+    if (threadIdx.x == 0) tl = __bfloat162float(reinterpret_cast<const bf16*>(row)[target]);
+    __nv_bfloat162 mx2 = __float2bfloat162_rn(-INFINITY);
+    for (int i = threadIdx.x; i < nfull; i += kCeThreads) {
+      const uint4 u = row[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+      mx2 = __hmax2(mx2, __hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])));
+    }
+    float m = fmaxf(__low2float(mx2), __high2float(mx2));
+    if (nfull < nvec && threadIdx.x == (nfull % kCeThreads)) {  // ragged tail chunk (vocab % 8)
+      const bf16* t = reinterpret_cast<const bf16*>(row) + nfull * 8;
+      for (int k = 0; k < vocab - nfull * 8; ++k) m = fmaxf(m, __bfloat162float(t[k]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) shm[w] = m;
+    __syncthreads();
+    m = shm[0];
+#pragma unroll
+    for (int k = 1; k < kCeThreads / 32; ++k) m = fmaxf(m, shm[k]);
+    m *= kL2e;
+    uint4* rw = reinterpret_cast<uint4*>(ce_smem + buf * stride);
+    float s0 = 0.f, s1 = 0.f;
+    for (int i = threadIdx.x; i < nvec; i += kCeThreads) {
+      const uint4 u = rw[i];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+      float f[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 t = __bfloat1622float2(h[k]);
+        f[2 * k] = ex2_fast(fmaf(t.x, kL2e, -m));
+        f[2 * k + 1] = ex2_fast(fmaf(t.y, kL2e, -m));
+      }
+      if (i >= nfull) {
+        const int valid = vocab - i * 8;  // < 8 on the ragged tail chunk
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = k < valid ? f[k] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        s0 += f[k];
+        s1 += f[k + 1];
+      }
+      rw[i] = pack8(f);
+    }
+    float sum = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) shs[w] = sum;
+    __syncthreads();
+    sum = shs[0];
+#pragma unroll
+    for (int k = 1; k < kCeThreads / 32; ++k) sum += shs[k];
+    const float coef = gscale / sum;
+    uint4* out = reinterpret_cast<uint4*>(logits + r * ldv);
+    for (int i = threadIdx.x; i < nvec; i += kCeThreads) {
+      float f[8];
+      unpack8(rw[i], f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] *= coef;
+      out[i] = pack8(f);
+    }
+    // one-hot term: the thread that wrote the target's chunk rewrites that element (program
+    // order on the same address)
+    if (threadIdx.x == (target / 8) % kCeThreads) {
+      const float e = __bfloat162float(reinterpret_cast<const bf16*>(rw)[target]);
+      logits[r * ldv + target] = __float2bfloat16_rn(e * coef - gscale);
+    }
+    if (threadIdx.x == 0) row_loss[r] = (m + __log2f(sum)) / kL2e - tl;
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
   }
 }
 
@@ -693,6 +814,18 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
 
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
                            int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s) {
+  const size_t stride = (size_t(ldv) * 2 + 127) & ~size_t(127);
+  if (2 * stride <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ce_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int grid = int(rows < ctas ? rows : ctas);
+    ce_smem_k<<<grid, kCeThreads, 2 * stride, s>>>(logits, tokens, seq, rows, vocab, ldv, grad_scale, row_loss);
+    note_launch();
+    return;
+  }
   ce_k<<<grid_for(rows, 1, ctas, 8), kThreads, 0, s>>>(logits, tokens, seq, rows, vocab, ldv,
                                                       grad_scale, row_loss); note_launch();
 }

@@ -380,7 +380,7 @@ struct Runtime {
     }
     CK(cudaMemsetAsync(wgrad32, 0, size_t(M) * N * 4, st));
     mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, wgrad32, N, kEpiAtomicF32, 1.f, nullptr, nullptr,
-       nullptr, split);
+       nullptr, -1);  // split count chosen by the launcher for full waves of its tile shape
     cast_f32_bf16(wgrad32, dst, int64_t(M) * N, ctas, st);
   }
 

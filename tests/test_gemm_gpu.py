@@ -171,7 +171,7 @@ def test_gemm_causal_modes(cuda):
     assert relerr(dV, P.float().t() @ G.float()) < 1e-5
 
 
-@pytest.mark.parametrize("split", [2, 5, 16])
+@pytest.mark.parametrize("split", [2, 5, 16, -1])
 def test_gemm_split_k_weight_grad(cuda, split):
     # dW = dY^T X with both operands MN-major, K = tokens (long), fp32 atomics across splits.
     T, M, N = 8192, 768, 3072

@@ -12,6 +12,8 @@ WANT = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe % active"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % of peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 % of peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
     ("launch__registers_per_thread", "regs/thread"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
@@ -19,7 +21,10 @@ WANT = [
 
 
 def summarise(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         return None

@@ -3,7 +3,7 @@
 # (single launch each, inside the cudaProfilerStart/Stop range). Run under gpurun on 1 GPU.
 set -u
 B=${1:-16}
-OUT=gpurun_out/prof_r1
+OUT=${2:-gpurun_out/prof_r1}
 mkdir -p $OUT
 python tools/profile_step.py --b $B > $OUT/plain.log 2>&1 || { echo "plain run failed"; tail $OUT/plain.log; exit 1; }
 cap() {  # name regex skip
@@ -18,5 +18,5 @@ cap attn_fwd "attn_fwd_kernel" 0
 cap attn_bwd "attn_bwd_kernel" 0
 cap adam "adam_k" 0
 cap ce "ce_k" 0
-cap ln_bwd "ln_bwd_k" 0
+cap ln_bwd "ln_bwd_rows_k" 0
 ls -la $OUT
