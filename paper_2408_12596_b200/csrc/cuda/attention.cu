@@ -1,9 +1,9 @@
 // Fused causal attention for head_dim 64 on sm_100a tensor cores (tcgen05 + TMEM + TMA).
 //
 // Forward (one CTA task = 128 queries of one (head, sample)): for every 128-key tile at or
-// below the diagonal, S = Q K^T lands in TMEM, four softmax warps read it row-per-thread,
-// run the online softmax in registers, write P (bf16) into a SWIZZLE_128B shared tile and the
-// MMA warp computes P V into TMEM; the softmax warps fold it into a register accumulator.
+// below the diagonal, S = Q K^T lands in one of two TMEM buffers, eight softmax warps read it
+// (one row half per thread), run the online softmax, write P (bf16) into one of two SWIZZLE_128B
+// shared tiles, and the MMA warp accumulates P V into a TMEM-resident O.
 // Nothing of size s x s ever reaches HBM: the kernel reads Q, K, V once per query tile and
 // writes O and the row log-sum-exp.
 //
@@ -55,9 +55,10 @@ __device__ __forceinline__ uint32_t p_off(int r, int k) {
   return blk * kTile + r * 128 + ((chunk ^ (r & 7)) << 4);
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {  // a -> low half, b -> high half
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -69,75 +70,178 @@ struct AttnTask {
   int tile, z;  // tile index (query tile in fwd, key tile in bwd) and z = sample * H + head
 };
 
-// Longest tasks first: forward query tile qt needs qt+1 key tiles; backward key tile kt needs
-// nt-kt query tiles.
-__device__ __forceinline__ AttnTask fwd_task(int t, int nz, int nt) {
-  return {nt - 1 - t / nz, t % nz};
+// Dynamic task scheduling. Forward tasks are numbered in groups of kGroupZ (sample, head) pairs;
+// within a group the longest tiles come first (forward query tile qt needs qt+1 key tiles, backward key
+// tile kt needs nt-kt query tiles). CTAs grab task numbers from a global counter, so the tiles
+// of a few (sample, head) pairs are in flight together (their K/V, resp. Q/dO, tiles are read
+// from HBM once and served from L2) and the longest-first order balances the CTAs.
+constexpr int kGroupZ = 16;
+__device__ unsigned int g_sched[4];  // [fwd counter, fwd done, bwd counter, bwd done]
+
+__device__ __forceinline__ AttnTask group_task(int t, int nz, int nt, bool longest_is_last_tile) {
+  const int per = kGroupZ * nt;
+  const int g = t / per;
+  const int rem = t - g * per;
+  const int gz = min(kGroupZ, nz - g * kGroupZ);
+  const int rank = rem / gz;  // 0 = longest
+  return {longest_is_last_tile ? nt - 1 - rank : rank, g * kGroupZ + rem % gz};
 }
-__device__ __forceinline__ AttnTask bwd_task(int t, int nz) { return {t / nz, t % nz}; }
+__device__ __forceinline__ AttnTask fwd_task(int t, int nz, int nt) { return group_task(t, nz, nt, true); }
+// Backward: static round-robin, tile-major (longest key tiles first) over all (sample, head)
+// pairs: concurrent key tiles of the same (sample, head) would contend on the same dQ rows'
+// atomics.
+__device__ __forceinline__ AttnTask bwd_task_static(int t, int nz) { return {t / nz, t % nz}; }
+
+__device__ __forceinline__ int lds_s32(const int* p) {
+  int v;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ float lds_f32(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(ptx::smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_f32(float* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(ptx::smem_u32(p)), "f"(v) : "memory");
+}
+
+// Four-slot ring carrying the grabbed task numbers from the producer to the other warp roles.
+struct TaskRing {
+  int* slot;        // [4]
+  uint64_t* full;   // [4], count 1 (producer)
+  uint64_t* empty;  // [4], count = number of consumer warps
+  // producer: next task number (>= ntasks when the launch is exhausted; consumers see it too)
+  __device__ int produce(uint32_t item, unsigned int* ctr) const {
+    const int k = item & 3;
+    ptx::mbar_wait(&empty[k], ((item >> 2) & 1) ^ 1);
+    const int t = int(atomicAdd(ctr, 1u));
+    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(ptx::smem_u32(&slot[k])), "r"(t) : "memory");
+    ptx::mbar_arrive(&full[k]);
+    return t;
+  }
+  // consumer warp (all lanes call): the item's task number; lane 0 releases the slot
+  __device__ int consume(uint32_t item) const {
+    const int k = item & 3;
+    ptx::mbar_wait(&full[k], (item >> 2) & 1);
+    const int t = lds_s32(&slot[k]);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(&empty[k]);
+    return t;
+  }
+  // single-thread consumer
+  __device__ int consume1(uint32_t item) const {
+    const int k = item & 3;
+    ptx::mbar_wait(&full[k], (item >> 2) & 1);
+    const int t = lds_s32(&slot[k]);
+    ptx::mbar_arrive(&empty[k]);
+    return t;
+  }
+};
+
+// Called once per CTA by the producer after its last grab: the last CTA resets the counter for
+// the next launch on the stream.
+__device__ __forceinline__ void sched_finish(unsigned int* sched, unsigned int producers_per_cta) {
+  __threadfence();
+  if (atomicAdd(&sched[1], 1u) == gridDim.x * producers_per_cta - 1) {
+    atomicExch(&sched[0], 0u);
+    atomicExch(&sched[1], 0u);
+  }
+}
 
 // ============================================================================ forward
-// Warp roles: 0-7 softmax (TMEM lane quarter w % 4, key half w / 4), 8 TMA producer, 9 MMA.
-constexpr int kFwdThreads = 320;
+// One CTA per SM running two independent pipelines (warps 10p .. 10p+9 for pipeline p), each
+// with its own tasks, shared-memory stages, barriers and 256 TMEM columns: warps 0-7 softmax
+// (TMEM lane quarter w % 4, key half w / 4), warp 8 TMA producer, warp 9 MMA issuer. TMEM per
+// pipeline: S [0,128), P [128,192) as packed bf16 pairs, O [192,256). S = Q K^T lands in TMEM; the softmax warps read it, write P back into TMEM
+// (tcgen05.st) and the MMA warp accumulates O += P V with P as a TMEM operand. O stays in TMEM
+// for the whole query tile; the max used for the exponentials is only raised when the row max
+// grows by more than 2^8 (lazy rescale of O and the row sum, in place). The two pipelines
+// overlap one's softmax with the other's MMAs and barrier waits.
+constexpr int kFwdPipes = 2;
+constexpr int kFwdThreads = 320 * kFwdPipes;
+constexpr int kFwdProducer = 8, kFwdMma = 9;
+constexpr int kFwdKV = 2;              // K/V stages
+constexpr float kRescaleLog2 = 8.0f;   // rescale O only when the max grows by more than 2^8
+constexpr int kFwdTmemS = 0, kFwdTmemP = 128, kFwdTmemO = 192;
 
 struct FwdSmem {
   static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kTile;           // 2 stages
-  static constexpr int kV = kK + 2 * kTile;       // 2 stages
-  static constexpr int kP = kV + 2 * kTile;       // [128, 128] = 2 tiles
-  static constexpr int kRed = kP + 2 * kTile;   // [2 halves][128 rows] fp32 exchange
+  static constexpr int kK = kQ + kTile;                // kFwdKV stages
+  static constexpr int kV = kK + kFwdKV * kTile;       // kFwdKV stages
+  static constexpr int kRed = kV + kFwdKV * kTile;     // [2 halves][128 rows] fp32 exchange
   static constexpr int kBar = kRed + 2 * 128 * 4;
-  static constexpr int kBytes = kBar + 256 + 1024;
+  static constexpr int kPipe = (kBar + 256 + 1023) / 1024 * 1024;  // one pipeline (1 KiB multiple)
+  static constexpr int kBytes = kFwdPipes * kPipe + 1024;
 };
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+static_assert(FwdSmem::kPipe % 1024 == 0, "pipeline regions keep the 1 KiB swizzle alignment");
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap map_qkv, bf16* __restrict__ out,
                     float* __restrict__ lse, int seq, int heads, int nz, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int pipe = int(ptx::warp_id()) / 10;
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023)) +
+                pipe * FwdSmem::kPipe;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FwdSmem::kBar);
   uint64_t* q_full = bar + 0;
   uint64_t* q_empty = bar + 1;
-  uint64_t* kv_full = bar + 2;   // [2]
-  uint64_t* kv_empty = bar + 4;  // [2]
-  uint64_t* s_full = bar + 6;
-  uint64_t* s_free = bar + 7;
-  uint64_t* p_full = bar + 8;
-  uint64_t* o_full = bar + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar + 2;            // [kFwdKV]
+  uint64_t* kv_empty = bar + 2 + kFwdKV;  // [kFwdKV]
+  uint64_t* s_full = bar + 2 + 2 * kFwdKV;  // S ready (MMA -> softmax)
+  uint64_t* s_free = s_full + 1;   // S read out (softmax -> MMA)
+  uint64_t* p_full = s_full + 2;   // P written to TMEM, O rescaled (softmax -> MMA)
+  uint64_t* pv_done = s_full + 3;  // P.V complete: P free, O updated (MMA -> softmax)
+  uint64_t* o_free = s_full + 4;   // O read out by the epilogue (softmax -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 5);
+  const TaskRing ring{reinterpret_cast<int*>(s_full + 6), s_full + 8, s_full + 12};
 
-  const int warp = int(ptx::warp_id());
+  const int warp = int(ptx::warp_id()) % 10;  // role within the pipeline
   const int lane = threadIdx.x & 31;
   const int nt = seq / kT;
   const int ntasks = nt * nz;
   const int h = heads * kD;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == kFwdProducer && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kFwdKV; ++i) {
       ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_free, 256);
     ptx::mbar_init(p_full, 256);
-    ptx::mbar_init(o_full, 1);
+    ptx::mbar_init(pv_done, 1);
+    ptx::mbar_init(o_free, 256);
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&ring.full[i], 1);
+      ptx::mbar_init(&ring.empty[i], 9);  // MMA thread + 8 softmax warps
+    }
     ptx::fence_barrier_init();
   }
-  if (warp == 8) ptx::tmem_alloc(tmem_slot, 256);
+  uint32_t* tmem_slot0 = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tmem_slot) - pipe * FwdSmem::kPipe);
+  if (pipe == 0 && warp == kFwdProducer) ptx::tmem_alloc(tmem_slot0, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_o = tmem + 128;
+  const uint32_t tmem = *tmem_slot0 + 256 * pipe;
 
-  if (warp == 8) {
+  if (warp == kFwdProducer) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       int stage = 0;
-      uint32_t phase = 0, item = 0;
-      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+      uint32_t phase = 0;
+      for (uint32_t item = 0;; ++item) {
+        const int t = ring.produce(item, &g_sched[0]);
+        if (t >= ntasks) break;
         const AttnTask tk = fwd_task(t, nz, nt);
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
@@ -151,85 +255,96 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                            row0 + j * kT, 0, 0);
           ptx::tma_load_4d(sm + FwdSmem::kV + stage * kTile, &map_qkv, &kv_full[stage], 2 * h + head * kD,
                            row0 + j * kT, 0, 0);
-          if (++stage == 2) {
+          if (++stage == kFwdKV) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      sched_finish(&g_sched[0], kFwdPipes);
     }
-  } else if (warp == 9) {
+  } else if (warp == kFwdMma) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      // S(j+1) is issued as soon as the softmax warps have pulled S(j) out of TMEM, before P V(j):
-      // the tensor pipe computes the next scores while the softmax of tile j runs.
+      // Per task: S(0); then for each j: S(j+1) (after the softmax has read S(j)), P.V(j).
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, 64, 0, 1);
       const uint32_t sq = ptx::smem_u32(sm + FwdSmem::kQ);
-      const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
-      int ks = 0, kp = 0;              // K/V stage of the next S issue and of the next P V issue
-      uint32_t ks_ph = 0, item = 0, it = 0;
-      auto issue_s = [&](uint32_t s_parity) {
+      int ks = 0, kp = 0;  // K/V stage of the next S issue and of the next P.V issue
+      uint32_t ks_ph = 0;
+      uint32_t gs = 0, gp = 0;  // S and P.V issues so far (barrier phases)
+      auto issue_s = [&]() {
         ptx::mbar_wait(&kv_full[ks], ks_ph);
-        ptx::mbar_wait(s_free, s_parity);
+        ptx::mbar_wait(s_free, (gs & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t sk = ptx::smem_u32(sm + FwdSmem::kK + ks * kTile);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_s, k > 0);
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kFwdTmemS, kdesc(sq, k), kdesc(sk, k), id_s, k > 0);
         ptx::umma_commit(s_full);
-        if (++ks == 2) {
+        if (++ks == kFwdKV) {
           ks = 0;
           ks_ph ^= 1;
         }
+        ++gs;
       };
-      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+      for (uint32_t item = 0;; ++item) {
+        const int t = ring.consume1(item);
+        if (t >= ntasks) break;
         const AttnTask tk = fwd_task(t, nz, nt);
         const int nj = tk.tile + 1;
         ptx::mbar_wait(q_full, item & 1);
-        issue_s((it & 1) ^ 1);  // S(0): softmax finished reading the previous task's last S
-        if (nj == 1) ptx::umma_commit(q_empty);
-        for (int j = 0; j < nj; ++j, ++it) {
+        issue_s();
+        for (int j = 0; j < nj; ++j) {
           if (j + 1 < nj) {
-            issue_s(it & 1);  // S(j) has been read out of TMEM
-            if (j + 2 == nj) ptx::umma_commit(q_empty);
+            issue_s();
+            if (j + 2 == nj) ptx::umma_commit(q_empty);  // the task's last S has been issued
+          } else if (nj == 1) {
+            ptx::umma_commit(q_empty);
           }
-          ptx::mbar_wait(p_full, it & 1);
+          if (j == 0) ptx::mbar_wait(o_free, (item & 1) ^ 1);  // previous task's epilogue read O
+          ptx::mbar_wait(p_full, gp & 1);
           ptx::tc_fence_after();
           const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + kp * kTile);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_o, kdesc2(sp, k), mndesc(sv, k), id_o, k > 0);
-          ptx::umma_commit(o_full);
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_ts(tmem + kFwdTmemO, tmem + kFwdTmemP + 8 * k, mndesc(sv, k), id_o, (j > 0 || k > 0));
+          ptx::umma_commit(pv_done);
           ptx::umma_commit(&kv_empty[kp]);
-          kp ^= 1;
+          if (++kp == kFwdKV) kp = 0;
+          ++gp;
         }
       }
     }
   } else {  // -------------------------------------------------------------- softmax warps 0-7
-    // Warp (q4, kh) owns query rows 32*q4..+31 and keys 64*kh..+63 of every S tile, and O columns
-    // 32*kh..+31. The two halves of a row exchange their maxima through shared memory.
-    const int q4 = warp & 3, kh = warp >> 2;
+    // Warp (q4, kh) owns query rows 32*q4..+31, keys 64*kh..+63 of every S tile (P columns
+    // 32*kh..+31) and O columns 32*kh..+31. The two halves of a row exchange their maxima and
+    // row sums through shared memory.
+    // a warp may only touch the TMEM lane quarter (hardware warp index % 4)
+    const int q4 = int(ptx::warp_id()) & 3, kh = warp >> 2;
+    const int nb = 1 + 4 * pipe + q4;  // named barrier of the row quarter's two halves
     const int r = q4 * 32 + lane;  // query row within the tile == TMEM lane
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
-    const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
     float* red = reinterpret_cast<float*>(sm + FwdSmem::kRed);  // [2][128]
-    uint32_t it = 0;
-    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const uint32_t t_s = tmem + kFwdTmemS + lane_off + kh * 64;
+    const uint32_t t_p = tmem + kFwdTmemP + lane_off + kh * 32;
+    const uint32_t t_o = tmem + kFwdTmemO + lane_off + kh * 32;
+    uint32_t g = 0;  // tiles processed (S / P.V barrier phases)
+    for (uint32_t item = 0;; ++item) {
+      const int t = ring.consume(item);
+      if (t >= ntasks) break;
       const AttnTask tk = fwd_task(t, nz, nt);
       const int smp = tk.z / heads, head = tk.z % heads;
-      float o[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = 0.f;
-      float m = -INFINITY, l = 0.f;
-      for (int j = 0; j <= tk.tile; ++j, ++it) {
-        ptx::mbar_wait(s_full, it & 1);
+      float m = -INFINITY, l = 0.f;  // m: max used for the exponentials (log2 domain)
+      for (int j = 0; j <= tk.tile; ++j, ++g) {
+        ptx::mbar_wait(s_full, g & 1);
         ptx::tc_fence_after();
         float sv[64];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_s + lane_off + kh * 64 + c * 32, v);
+          ptx::tmem_ld_32x32b_x32(t_s + c * 32, v);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]) * scale_log2;
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
@@ -238,58 +353,74 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 64; ++i)
             if (kh * 64 + i > r) sv[i] = -INFINITY;
         }
-        float lm = -INFINITY;
+        float pm[8];  // independent partial maxima (short dependency chains)
 #pragma unroll
-        for (int i = 0; i < 64; ++i) lm = fmaxf(lm, sv[i]);
-        red[kh * 128 + r] = lm;
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");  // the row's two halves
-        const float mx = fmaxf(m, fmaxf(red[r], red[128 + r]));
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");  // red reusable next tile
-        const float alpha = exp2f(m - mx);
-        m = mx;
-        float sum = 0.f;
+        for (int i = 0; i < 8; ++i) pm[i] = fmaxf(sv[i], sv[i + 8]);
 #pragma unroll
-        for (int c = 0; c < 64; c += 8) {
-          float p[8];
+        for (int i = 16; i < 64; i += 8) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            p[i] = exp2f(sv[c + i] - mx);
-            sum += p[i];
+          for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], sv[i + k]);
+        }
+        sts_f32(&red[kh * 128 + r], fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                          fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))));
+        asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // the row's two halves
+        const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
+        asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // red reusable next tile
+        // lazy rescale: raise m only when the row max outgrows it by more than 2^8
+        const bool raise = mx > m + kRescaleLog2;
+        const float alpha = raise ? ex2(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
+        if (raise) m = mx;
+        // exponentials and row sum (registers), packed bf16 pairs for the TMEM P tile
+        uint32_t pk[32];
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const float p0 = ex2(fmaf(sv[i], scale_log2, -m));
+          const float p1 = ex2(fmaf(sv[i + 1], scale_log2, -m));
+          ps[(i >> 1) & 7] += p0 + p1;
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
+        // P.V(j-1) must have finished reading P and accumulating into O
+        if (j > 0) {
+          ptx::mbar_wait(pv_done, (g - 1) & 1);
+          ptx::tc_fence_after();
+          if (__any_sync(0xffffffffu, raise)) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(t_o, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            ptx::tmem_st_32x32b_x32(t_o, v);
           }
-          st_shared_v4(sp + p_off(r, kh * 64 + c), pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]),
-                       pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
         }
-        l = l * alpha + sum;
-        fence_proxy_async();
-        ptx::mbar_arrive(p_full);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] *= alpha;
-        ptx::mbar_wait(o_full, it & 1);
-        ptx::tc_fence_after();
-        {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_o + lane_off + kh * 32, v);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] += __uint_as_float(v[i]);
-        }
+        l = l * alpha + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
+        ptx::tmem_st_32x32b_x32(t_p, pk);
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full);
       }
-      // combine the two halves' row sums, then O / l -> bf16 (this warp's 32 columns), LSE
-      red[kh * 128 + r] = l;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
-      const float lt = red[r] + red[128 + r];
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+      // epilogue: wait for the last P.V, combine the halves' row sums, O / l -> bf16, LSE
+      ptx::mbar_wait(pv_done, (g - 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t v[32];
+      ptx::tmem_ld_32x32b_x32(t_o, v);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(o_free);
+      sts_f32(&red[kh * 128 + r], l);
+      asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");
+      const float lt = lds_f32(&red[r]) + lds_f32(&red[128 + r]);
+      asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");
       const float inv = 1.f / lt;
       const int64_t row = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
       bf16* dst = out + row * h + head * kD + kh * 32;
 #pragma unroll
       for (int c = 0; c < 32; c += 8) {
         uint4 u;
-        u.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
-        u.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
-        u.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
-        u.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+        u.x = pack_bf16(__uint_as_float(v[c]) * inv, __uint_as_float(v[c + 1]) * inv);
+        u.y = pack_bf16(__uint_as_float(v[c + 2]) * inv, __uint_as_float(v[c + 3]) * inv);
+        u.z = pack_bf16(__uint_as_float(v[c + 4]) * inv, __uint_as_float(v[c + 5]) * inv);
+        u.w = pack_bf16(__uint_as_float(v[c + 6]) * inv, __uint_as_float(v[c + 7]) * inv);
         *reinterpret_cast<uint4*>(dst + c) = u;
       }
       if (kh == 0) lse[int64_t(tk.z) * seq + int64_t(tk.tile) * kT + r] = (m + log2f(lt)) / kLog2e;
@@ -297,9 +428,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (pipe == 0 && warp == kFwdProducer) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 256);
+    ptx::tmem_dealloc(*tmem_slot0, 512);
   }
 }
 
@@ -375,7 +506,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int stage = 0;
       uint32_t phase = 0, item = 0;
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
-        const AttnTask tk = bwd_task(t, nz);
+        const AttnTask tk = bwd_task_static(t, nz);
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
         ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
@@ -426,7 +557,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
-        const AttnTask tk = bwd_task(t, nz);
+        const AttnTask tk = bwd_task_static(t, nz);
         ptx::mbar_wait(kv_full, item & 1);
         ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // epilogue of the previous task read dK/dV
         issue_sdp((it & 1) ^ 1);
@@ -459,7 +590,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-      const AttnTask tk = bwd_task(t, nz);
+      const AttnTask tk = bwd_task_static(t, nz);
       for (int i = tk.tile; i < nt; ++i, ++it) {
         const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
         const float lse2 = lse[qrow] * kLog2e;
@@ -510,7 +641,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-      const AttnTask tk = bwd_task(t, nz);
+      const AttnTask tk = bwd_task_static(t, nz);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
         ptx::mbar_wait(mm_done, it & 1);
@@ -671,7 +802,7 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
   if (!map_rows(&m, qkv, batch * seq, 3 * h)) return cudaErrorInvalidValue;
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
-  int grid = std::min(ntasks, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
+  int grid = std::min((ntasks + kFwdPipes - 1) / kFwdPipes, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
   const float scale_log2 = (1.0f / std::sqrt(float(kD))) * kLog2e;
   attn_fwd_kernel<<<grid, kFwdThreads, FwdSmem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
   note_launch();
