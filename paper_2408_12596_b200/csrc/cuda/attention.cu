@@ -24,6 +24,25 @@
 namespace zp {
 namespace {
 
+#ifdef ZP_ATTN_TRACE
+// Debug timeline (tools/debug/attn_trace.cu): CTA 0 records (tag, clock64) per warp role.
+__device__ unsigned long long g_trace[4][8192];
+__device__ unsigned int g_trace_n[4];
+// One writer thread per role; the event index lives in a register (zp_tn) of that thread and
+// the stores are fire-and-forget, so tracing does not perturb the timeline.
+__device__ __forceinline__ void trace(int role, int tag, uint32_t& n) {
+  if (blockIdx.x != 0) return;
+  if (n < 8192) g_trace[role][n] = (static_cast<unsigned long long>(tag) << 56) | (clock64() & ((1ull << 56) - 1));
+  ++n;
+  g_trace_n[role] = n;
+}
+#define ZP_TRACE(role, tag) trace(role, tag, zp_tn)
+#define ZP_TRACE_INIT uint32_t zp_tn = 0
+#else
+#define ZP_TRACE(role, tag) ((void)0)
+#define ZP_TRACE_INIT ((void)0)
+#endif
+
 constexpr int kT = 128;          // query / key tile
 constexpr int kD = 64;           // head dim
 constexpr int kTile = kT * kD * 2;  // one [128, 64] bf16 tile = 16 KiB
@@ -439,20 +458,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // dK/dV epilogue (lane quarter w % 4), 12 TMA producer, 13 MMA issuer. The dQ atomics of query
 // tile i overlap the P/dS construction of tile i+1.
 constexpr int kBwdThreads = 448;
+constexpr int kBwdQD = 3;  // Q/dO stages: a stage is held from its load until dV/dK/dQ of its tile
+constexpr int kBwdPS = 1;  // P/dS shared-memory buffers
 
 struct BwdSmem {
   static constexpr int kK = 0;
   static constexpr int kV = kK + kTile;
-  static constexpr int kQ = kV + kTile;     // 2 stages
-  static constexpr int kDO = kQ + 2 * kTile;  // 2 stages
-  static constexpr int kP = kDO + 2 * kTile;  // [128, 128]
-  static constexpr int kDS = kP + 2 * kTile;  // [128, 128]
-  static constexpr int kBar = kDS + 2 * kTile;
+  static constexpr int kQ = kV + kTile;               // kBwdQD stages
+  static constexpr int kDO = kQ + kBwdQD * kTile;      // kBwdQD stages
+  static constexpr int kP = kDO + kBwdQD * kTile;      // kBwdPS buffers of [128, 128]
+  static constexpr int kDS = kP + kBwdPS * 2 * kTile;  // kBwdPS buffers of [128, 128]
+  static constexpr int kDQ = kDS + kBwdPS * 2 * kTile;  // dQ staging: 4 warps x [32 rows x 64] fp32
+  static constexpr int kBar = kDQ + 4 * 32 * 64 * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                    const __grid_constant__ CUtensorMap map_dq,
                     const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
                     bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale) {
   extern __shared__ uint8_t smem_raw[];
@@ -460,15 +483,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::kBar);
   uint64_t* kv_full = bar + 0;
   uint64_t* kv_empty = bar + 1;
-  uint64_t* qd_full = bar + 2;   // [2]
-  uint64_t* qd_empty = bar + 4;  // [2]
-  uint64_t* sp_full = bar + 6;
-  uint64_t* s_free = bar + 7;
-  uint64_t* ps_full = bar + 8;
-  uint64_t* mm_done = bar + 9;
-  uint64_t* acc_free = bar + 10;
-  uint64_t* dq_free = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* qd_full = bar + 2;            // [kBwdQD]
+  uint64_t* qd_empty = bar + 2 + kBwdQD;  // [kBwdQD]
+  uint64_t* sp_full = bar + 2 + 2 * kBwdQD;
+  uint64_t* s_free = sp_full + 1;
+  uint64_t* ps_full = sp_full + 2;   // [kBwdPS] P/dS buffer written (builders -> MMA)
+  uint64_t* mm_done = sp_full + 4;   // [kBwdPS] dV/dK/dQ products of the buffer's tile done
+  uint64_t* acc_free = sp_full + 6;
+  uint64_t* dq_free = sp_full + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sp_full + 8);
 
   const int warp = int(ptx::warp_id());
   const int lane = threadIdx.x & 31;
@@ -482,14 +505,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::tma_prefetch_desc(&map_do);
     ptx::mbar_init(kv_full, 1);
     ptx::mbar_init(kv_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kBwdQD; ++i) {
       ptx::mbar_init(&qd_full[i], 1);
       ptx::mbar_init(&qd_empty[i], 1);
     }
     ptx::mbar_init(sp_full, 1);
     ptx::mbar_init(s_free, 256);
-    ptx::mbar_init(ps_full, 256);
-    ptx::mbar_init(mm_done, 1);
+    for (int i = 0; i < kBwdPS; ++i) {
+      ptx::mbar_init(&ps_full[i], 256);
+      ptx::mbar_init(&mm_done[i], 1);
+    }
     ptx::mbar_init(acc_free, 128);
     ptx::mbar_init(dq_free, 128);
     ptx::fence_barrier_init();
@@ -503,24 +528,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 12) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
+      ZP_TRACE_INIT;
       int stage = 0;
       uint32_t phase = 0, item = 0;
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task_static(t, nz);
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
+        ZP_TRACE(3, 7);
         ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
+        ZP_TRACE(3, 8);
         ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile);
         ptx::tma_load_4d(sm + BwdSmem::kK, &map_qkv, kv_full, h + head * kD, row0 + tk.tile * kT, 0, 0);
         ptx::tma_load_4d(sm + BwdSmem::kV, &map_qkv, kv_full, 2 * h + head * kD, row0 + tk.tile * kT, 0, 0);
         for (int i = tk.tile; i < nt; ++i) {
+          ZP_TRACE(3, 1);
           ptx::mbar_wait(&qd_empty[stage], phase ^ 1);
+          ZP_TRACE(3, 2);
           ptx::mbar_arrive_expect_tx(&qd_full[stage], 2 * kTile);
           ptx::tma_load_4d(sm + BwdSmem::kQ + stage * kTile, &map_qkv, &qd_full[stage], head * kD,
                            row0 + i * kT, 0, 0);
           ptx::tma_load_4d(sm + BwdSmem::kDO + stage * kTile, &map_do, &qd_full[stage], head * kD,
                            row0 + i * kT, 0, 0);
-          if (++stage == 2) {
+          if (++stage == kBwdQD) {
             stage = 0;
             phase ^= 1;
           }
@@ -529,6 +559,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 13) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      ZP_TRACE_INIT;
       // S/dP of query tile i+1 are issued before the dV/dK/dQ products of tile i, so the builders
       // compute P/dS(i+1) while the tensor pipe works on tile i.
       constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
@@ -541,17 +572,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int ss = 0, sm2 = 0;  // Q/dO stage of the next S/dP issue and of the next dV/dK/dQ issue
       uint32_t ss_ph = 0, item = 0, it = 0;
       auto issue_sdp = [&](uint32_t s_parity) {
+        ZP_TRACE(0, 1);
         ptx::mbar_wait(&qd_full[ss], ss_ph);
+        ZP_TRACE(0, 2);
         ptx::mbar_wait(s_free, s_parity);
+        ZP_TRACE(0, 3);
         ptx::tc_fence_after();
         const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
         const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
+        for (int k = 0; k < 4; ++k) {
+          ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
+          ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
+        }
         ptx::umma_commit(sp_full);
-        if (++ss == 2) {
+        if (++ss == kBwdQD) {
           ss = 0;
           ss_ph ^= 1;
         }
@@ -563,26 +598,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         issue_sdp((it & 1) ^ 1);
         for (int i = tk.tile; i < nt; ++i, ++it) {
           if (i + 1 < nt) issue_sdp(it & 1);  // builders have pulled S/dP(i) out of TMEM
-          ptx::mbar_wait(ps_full, it & 1);
+          const int pb = it % kBwdPS;  // P/dS buffer of this tile
+          ZP_TRACE(0, 4);
+          ptx::mbar_wait(&ps_full[pb], (it / kBwdPS) & 1);
+          ZP_TRACE(0, 5);
           ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
+          ZP_TRACE(0, 6);
           ptx::tc_fence_after();
           const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + sm2 * kTile);
           const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + sm2 * kTile);
           const bool first = (i == tk.tile);
+          // interleaved by k step so consecutive MMAs target different accumulators
 #pragma unroll
-          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dv, mndesc(spp, k), mndesc(sdo, k), id_t, (!first || k > 0));
-#pragma unroll
-          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dk, mndesc(sds, k), mndesc(sq, k), id_t, (!first || k > 0));
-#pragma unroll
-          for (int k = 0; k < 8; ++k) ptx::umma_bf16(t_dq, kdesc2(sds, k), mndesc(sk, k), id_q, k > 0);
-          ptx::umma_commit(mm_done);
+          for (int k = 0; k < 8; ++k) {
+            ptx::umma_bf16(t_dv, mndesc(spp + pb * 2 * kTile, k), mndesc(sdo, k), id_t, (!first || k > 0));
+            ptx::umma_bf16(t_dk, mndesc(sds + pb * 2 * kTile, k), mndesc(sq, k), id_t, (!first || k > 0));
+            ptx::umma_bf16(t_dq, kdesc2(sds + pb * 2 * kTile, k), mndesc(sk, k), id_q, k > 0);
+          }
+          ptx::umma_commit(&mm_done[pb]);
           ptx::umma_commit(&qd_empty[sm2]);
           if (i == nt - 1) ptx::umma_commit(kv_empty);
-          sm2 ^= 1;
+          if (++sm2 == kBwdQD) sm2 = 0;
         }
       }
     }
   } else if (warp < 8) {  // ------------------------------------------ P / dS builders
+    ZP_TRACE_INIT;
     const int q4 = warp & 3, kh = warp >> 2;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
@@ -595,7 +636,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
         const float lse2 = lse[qrow] * kLog2e;
         const float dd = dvec[qrow];
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 1);
         ptx::mbar_wait(sp_full, it & 1);
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 2);
         ptx::tc_fence_after();
         uint32_t vs[2][32], vp[2][32];
 #pragma unroll
@@ -606,7 +649,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
-        uint32_t pk[32], dk[32];  // packed bf16 pairs of this thread's 64 P and dS values
+        // P = exp2(S*scale*log2e - LSE*log2e); dS' = P (dP - D) (the softmax scale of dS is
+        // applied once to dK and dQ at the end). Only the diagonal tile is masked.
+        uint32_t pk[32], dk[32];  // packed bf16 pairs of this thread's 64 P and dS' values
+        const bool diag = (i == tk.tile);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
 #pragma unroll
@@ -614,28 +660,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float pv[2], dv[2];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const int key = kh * 64 + c * 32 + e + u;
-              const bool masked = (i == tk.tile) && (key > r);
-              pv[u] = masked ? 0.f : exp2f(__uint_as_float(vs[c][e + u]) * scale_log2 - lse2);
-              dv[u] = pv[u] * (__uint_as_float(vp[c][e + u]) - dd) * scale;
+              pv[u] = ex2(fmaf(__uint_as_float(vs[c][e + u]), scale_log2, -lse2));
+              dv[u] = pv[u] * (__uint_as_float(vp[c][e + u]) - dd);
             }
             pk[c * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
             dk[c * 16 + e / 2] = pack_bf16(dv[0], dv[1]);
           }
         }
+        if (diag) {  // key > query: P = dS = 0 (zero the packed halves)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int key0 = kh * 64 + 2 * e;
+            const uint32_t keep = (key0 > r ? 0u : 0xffffu) | (key0 + 1 > r ? 0u : 0xffff0000u);
+            pk[e] &= keep;
+            dk[e] &= keep;
+          }
+        }
         // P/dS smem is free once the dV/dK/dQ products of the previous tile completed
-        ptx::mbar_wait(mm_done, (it & 1) ^ 1);
+        // the P/dS buffer is free once the products of tile it - kBwdPS completed
+        const int pb = it % kBwdPS;
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 3);
+        ptx::mbar_wait(&mm_done[pb], ((it / kBwdPS) & 1) ^ 1);
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 4);
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           const uint32_t off = p_off(r, kh * 64 + g * 8);
-          st_shared_v4(spp + off, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-          st_shared_v4(sds + off, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+          st_shared_v4(spp + pb * 2 * kTile + off, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          st_shared_v4(sds + pb * 2 * kTile + off, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
         }
         fence_proxy_async();
-        ptx::mbar_arrive(ps_full);
+        ptx::mbar_arrive(&ps_full[pb]);
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 5);
       }
     }
   } else {  // --------------------------------------------------------- warps 8-11: dQ + dK/dV out
+    ZP_TRACE_INIT;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
@@ -644,7 +703,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const AttnTask tk = bwd_task_static(t, nz);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        ptx::mbar_wait(mm_done, it & 1);
+        if (warp == 8 && lane == 0) ZP_TRACE(2, 1);
+        ptx::mbar_wait_sleep(&mm_done[it % kBwdPS], (it / kBwdPS) & 1, 1000);
+        if (warp == 8 && lane == 0) ZP_TRACE(2, 2);
         ptx::tc_fence_after();
         uint32_t v[2][32];
         ptx::tmem_ld_32x32b_x32(t_dq + lane_off, v[0]);
@@ -652,14 +713,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(dq_free);
-        float* dq = dq32 + (int64_t(smp) * seq + int64_t(i) * kT + r) * h + head * kD;
+        // dQ tile rows of this warp -> swizzled fp32 staging -> TMA reduce-add into dq32 (the
+        // reduction happens in L2 in whole lines; no per-thread atomics)
+        uint8_t* stg = sm + BwdSmem::kDQ + q4 * (32 * 64 * 4);
+        if (lane == 0) ptx::bulk_wait_read<0>();  // the previous tile's reduce has read the staging
+        __syncwarp();
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c) {
+          const uint32_t rowa = ptx::smem_u32(stg + c * 4096) + lane * 128;
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            atomicAdd(reinterpret_cast<float4*>(dq + c * 32 + e),
-                      make_float4(__uint_as_float(v[c][e]), __uint_as_float(v[c][e + 1]),
-                                  __uint_as_float(v[c][e + 2]), __uint_as_float(v[c][e + 3])));
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + ((j ^ (lane & 7)) << 4)),
+                         "r"(v[c][4 * j]), "r"(v[c][4 * j + 1]), "r"(v[c][4 * j + 2]), "r"(v[c][4 * j + 3])
+                         : "memory");
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int row = smp * seq + i * kT + q4 * 32;
+          ptx::tma_reduce_add_2d(&map_dq, stg, head * kD, row);
+          ptx::tma_reduce_add_2d(&map_dq, stg + 4096, head * kD + 32, row);
+          ptx::bulk_commit();
+        }
       }
       // epilogue: dK, dV rows of this key tile -> bf16 into dqkv (all MMAs of the task are done)
       const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
@@ -672,13 +747,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(src + c * 32, v);
           ptx::tmem_ld_wait();
+          const float f = which == 0 ? scale : 1.f;  // dK = scale * dS'^T Q
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             uint4 u;
-            u.x = pack_bf16(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
-            u.y = pack_bf16(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-            u.z = pack_bf16(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5]));
-            u.w = pack_bf16(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7]));
+            u.x = pack_bf16(__uint_as_float(v[e]) * f, __uint_as_float(v[e + 1]) * f);
+            u.y = pack_bf16(__uint_as_float(v[e + 2]) * f, __uint_as_float(v[e + 3]) * f);
+            u.z = pack_bf16(__uint_as_float(v[e + 4]) * f, __uint_as_float(v[e + 5]) * f);
+            u.w = pack_bf16(__uint_as_float(v[e + 6]) * f, __uint_as_float(v[e + 7]) * f);
             *reinterpret_cast<uint4*>(dst + c * 32 + e) = u;
           }
         }
@@ -686,6 +762,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(acc_free);
     }
+    if (lane == 0) ptx::bulk_wait<0>();  // dQ reductions complete before the kernel ends
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -732,7 +809,8 @@ __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __rest
 }
 
 // dqkv[:, 0:h] (bf16, row stride 3h) = dq32 [T, h]
-__global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __restrict__ dqkv, int64_t tokens, int h) {
+__global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __restrict__ dqkv, int64_t tokens, int h,
+                                    float scale) {
   const int64_t n4 = tokens * h / 4;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t e = i * 4;
@@ -740,8 +818,8 @@ __global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __rest
     const int col = int(e % h);
     const float4 v = reinterpret_cast<const float4*>(dq32)[i];
     uint2 o;
-    o.x = pack_bf16(v.x, v.y);
-    o.y = pack_bf16(v.z, v.w);
+    o.x = pack_bf16(v.x * scale, v.y * scale);  // dQ = scale * dS' K
+    o.y = pack_bf16(v.z * scale, v.w * scale);
     *reinterpret_cast<uint2*>(dqkv + tok * 3 * h + col) = o;
   }
 }
@@ -771,6 +849,20 @@ bool map_rows(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
   cuuint32_t box[4] = {64, 128, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D map over a row-major [rows, cols] fp32 matrix, box = 32 columns (128 B) x 32 rows,
+// SWIZZLE_128B (the dQ reduce-add target).
+bool map_f32_rows(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(cols * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -821,8 +913,9 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   }
   const int h = heads * kD;
   const int64_t T = batch * seq;
-  CUtensorMap mq, md;
-  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
+  CUtensorMap mq, md, mdq;
+  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h) || !map_f32_rows(&mdq, dq32, T, h))
+    return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
   attn_dvec_kernel<<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
   note_launch();
@@ -830,10 +923,11 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   if (e != cudaSuccess) return e;
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
-  attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
+  attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, mdq, lse, dvec, dq32, dqkv, seq,
                                                                           heads, nz, 1.0f / std::sqrt(float(kD)));
   note_launch();
-  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h);
+  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h,
+                                                                                       1.0f / std::sqrt(float(kD)));
   note_launch();
   return cudaGetLastError();
 }
