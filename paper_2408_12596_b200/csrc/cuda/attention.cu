@@ -459,12 +459,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // tile i overlap the P/dS construction of tile i+1.
 constexpr int kBwdThreads = 448;
 constexpr int kBwdQD = 3;  // Q/dO stages: a stage is held from its load until dV/dK/dQ of its tile
+constexpr int kBwdKV = 1;  // K/V stages (2 would let the next task's key tile load early; smem-bound)
 constexpr int kBwdPS = 1;  // P/dS shared-memory buffers
 
 struct BwdSmem {
-  static constexpr int kK = 0;
-  static constexpr int kV = kK + kTile;
-  static constexpr int kQ = kV + kTile;               // kBwdQD stages
+  static constexpr int kK = 0;                        // kBwdKV stages
+  static constexpr int kV = kK + kBwdKV * kTile;      // kBwdKV stages
+  static constexpr int kQ = kV + kBwdKV * kTile;      // kBwdQD stages
   static constexpr int kDO = kQ + kBwdQD * kTile;      // kBwdQD stages
   static constexpr int kP = kDO + kBwdQD * kTile;      // kBwdPS buffers of [128, 128]
   static constexpr int kDS = kP + kBwdPS * 2 * kTile;  // kBwdPS buffers of [128, 128]
@@ -481,11 +482,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::kBar);
-  uint64_t* kv_full = bar + 0;
-  uint64_t* kv_empty = bar + 1;
-  uint64_t* qd_full = bar + 2;            // [kBwdQD]
-  uint64_t* qd_empty = bar + 2 + kBwdQD;  // [kBwdQD]
-  uint64_t* sp_full = bar + 2 + 2 * kBwdQD;
+  uint64_t* kv_full = bar + 0;                          // [kBwdKV]
+  uint64_t* kv_empty = bar + kBwdKV;                    // [kBwdKV]
+  uint64_t* qd_full = bar + 2 * kBwdKV;                 // [kBwdQD]
+  uint64_t* qd_empty = bar + 2 * kBwdKV + kBwdQD;       // [kBwdQD]
+  uint64_t* sp_full = bar + 2 * kBwdKV + 2 * kBwdQD;
   uint64_t* s_free = sp_full + 1;
   uint64_t* ps_full = sp_full + 2;   // [kBwdPS] P/dS buffer written (builders -> MMA)
   uint64_t* mm_done = sp_full + 4;   // [kBwdPS] dV/dK/dQ products of the buffer's tile done
@@ -503,8 +504,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 12 && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::tma_prefetch_desc(&map_do);
-    ptx::mbar_init(kv_full, 1);
-    ptx::mbar_init(kv_empty, 1);
+    for (int i = 0; i < kBwdKV; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < kBwdQD; ++i) {
       ptx::mbar_init(&qd_full[i], 1);
       ptx::mbar_init(&qd_empty[i], 1);
@@ -536,11 +539,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
         ZP_TRACE(3, 7);
-        ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
+        const int kvs = item % kBwdKV;
+        ptx::mbar_wait(&kv_empty[kvs], ((item / kBwdKV) & 1) ^ 1);
         ZP_TRACE(3, 8);
-        ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile);
-        ptx::tma_load_4d(sm + BwdSmem::kK, &map_qkv, kv_full, h + head * kD, row0 + tk.tile * kT, 0, 0);
-        ptx::tma_load_4d(sm + BwdSmem::kV, &map_qkv, kv_full, 2 * h + head * kD, row0 + tk.tile * kT, 0, 0);
+        ptx::mbar_arrive_expect_tx(&kv_full[kvs], 2 * kTile);
+        ptx::tma_load_4d(sm + BwdSmem::kK + kvs * kTile, &map_qkv, &kv_full[kvs], h + head * kD,
+                         row0 + tk.tile * kT, 0, 0);
+        ptx::tma_load_4d(sm + BwdSmem::kV + kvs * kTile, &map_qkv, &kv_full[kvs], 2 * h + head * kD,
+                         row0 + tk.tile * kT, 0, 0);
         for (int i = tk.tile; i < nt; ++i) {
           ZP_TRACE(3, 1);
           ptx::mbar_wait(&qd_empty[stage], phase ^ 1);
@@ -565,8 +571,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
       constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dV, dK (A^T, B MN-major)
       constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dQ
-      const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK);
-      const uint32_t sv = ptx::smem_u32(sm + BwdSmem::kV);
+      uint32_t sk = 0, sv = 0;  // this task's K/V stage
       const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
       const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
       int ss = 0, sm2 = 0;  // Q/dO stage of the next S/dP issue and of the next dV/dK/dQ issue
@@ -593,7 +598,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task_static(t, nz);
-        ptx::mbar_wait(kv_full, item & 1);
+        const int kvs = item % kBwdKV;
+        ptx::mbar_wait(&kv_full[kvs], (item / kBwdKV) & 1);
+        sk = ptx::smem_u32(sm + BwdSmem::kK + kvs * kTile);
+        sv = ptx::smem_u32(sm + BwdSmem::kV + kvs * kTile);
         ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // epilogue of the previous task read dK/dV
         issue_sdp((it & 1) ^ 1);
         for (int i = tk.tile; i < nt; ++i, ++it) {
@@ -617,7 +625,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           ptx::umma_commit(&mm_done[pb]);
           ptx::umma_commit(&qd_empty[sm2]);
-          if (i == nt - 1) ptx::umma_commit(kv_empty);
+          if (i == nt - 1) ptx::umma_commit(&kv_empty[kvs]);
           if (++sm2 == kBwdQD) sm2 = 0;
         }
       }
