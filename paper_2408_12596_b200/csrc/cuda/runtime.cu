@@ -1082,6 +1082,8 @@ struct Runtime {
   }
 
   // ---------------------------------------------------------------- lockstep profiler (Alg. 1)
+  static constexpr double kSettleSeconds = 0.25;  // per-probe device time before the kept sample
+  static constexpr int64_t kSettleMaxReps = 24;
   int* dscratch = nullptr;  // small device buffer for rank-agreement collectives
   int64_t agree(int64_t v, ncclRedOp_t op) {
     if (n == 1) return v;
@@ -1118,7 +1120,15 @@ struct Runtime {
         if (b > tokens_count) load_tokens(nullptr, 0, b, uint64_t(adam_t), false);
         const int64_t gb = agree(b, ncclSum);
         zp_step_trace tr{};
-        const int rc = run_step(b, s, gb, &tr);
+        int rc = run_step(b, s, gb, &tr);
+        // Steady state: a single short probe runs at boost clocks that a long iteration under the
+        // power cap does not keep, which overstates small-batch speed. Every rank repeats the probe
+        // (same count on all ranks, agreed by max) until ~kSettleSeconds of device time and keeps
+        // the last measurement.
+        const double t1 = tr.forward_compute + tr.backward_compute;
+        const int64_t reps = agree(std::min<int64_t>(kSettleMaxReps, int64_t(std::ceil(kSettleSeconds / std::max(t1, 1e-3)))),
+                                   ncclMax);
+        for (int64_t r = 1; r < reps; ++r) rc = run_step(b, s, gb, &tr);
         if (!active) continue;
         if (rc == ZP_OOM) {
           search.record(b, std::nullopt, 0.0);
