@@ -33,9 +33,9 @@ struct Cfg {
   static constexpr int kBTileBytes = (BN / CG) * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
   static constexpr int kEpiBytes = kEpiWarps * 2 * kStageBufBytes;  // double-buffered per warp
-  static constexpr int kStages = (232448 - kEpiBytes - 1024 - 256) / kStageBytes;
+  static constexpr int kStages = (232448 - kEpiBytes - 1024 - 512) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 constexpr int kGroupM = 8;
@@ -99,20 +99,27 @@ struct EpiParams {
   const __nv_bfloat16* aux;
   __nv_bfloat16* aux_out;
   int tma_store;  // bf16 output written through swizzled smem boxes + TMA stores
+  int aux_tma;      // residual / GELU-input rows loaded by TMA into the staging boxes
+  int aux_out_tma;  // GELU pre-activation written by TMA stores
 };
 
 // GELU (tanh form) with the MUFU tanh approximation (rel. error ~2^-11, below bf16 output
 // rounding).
 __device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = ptx::tanh_approx(k0 * (x + k1 * x * x * x));
-  return 0.5f * x * (1.0f + t);
+  // 0.5 x (1 + tanh(k0 (x + k1 x^3))): 3 FMUL + 2 FFMA + 1 MUFU
+  constexpr float k0 = 0.7978845608028654f, k0k1 = 0.7978845608028654f * 0.044715f;
+  const float t = ptx::tanh_approx(x * fmaf(k0k1, x * x, k0));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = ptx::tanh_approx(k0 * (x + k1 * x * x * x));
-  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+  // 0.5 (1 + t) + 0.5 x (1 - t^2) k0 (1 + 3 k1 x^2), t = tanh(k0 (x + k1 x^3))
+  constexpr float k0 = 0.7978845608028654f, k0k1 = 0.7978845608028654f * 0.044715f;
+  const float x2 = x * x;
+  const float t = ptx::tanh_approx(x * fmaf(k0k1, x2, k0));
+  const float hd = x * fmaf(1.5f * k0k1, x2, 0.5f * k0);  // 0.5 x d(inner)/dx
+  return fmaf(hd, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
 }
 
 // bf16-output epilogue math on 32 consecutive columns [n, n+32) of one row; leaves the final
@@ -196,6 +203,40 @@ __device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32
   }
 }
 
+__device__ __forceinline__ void epi_bias(const EpiParams& ep, float (&v)[32], int n, int N, bool valid) {
+  if (valid && n + 32 <= N) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      const uint4 braw = *reinterpret_cast<const uint4*>(ep.bias + n + i);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 bf = __bfloat1622float2(b2[j]);
+        v[i + 2 * j] += bf.x;
+        v[i + 2 * j + 1] += bf.y;
+      }
+    }
+  } else if (valid) {
+    _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] += __bfloat162float(ep.bias[n + i]);
+  }
+}
+
+// One lane's row of a warp's [32 rows x 64 cols] bf16 staging box (SWIZZLE_128B).
+__device__ __forceinline__ void stage_row_bf16(uint8_t* sb, int lane, const float (&v)[2][32]) {
+  const uint32_t srow = ptx::smem_u32(sb) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float* w = &v[j >> 2][(j & 3) * 8];
+    uint32_t p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p[k]) : "f"(w[2 * k + 1]), "f"(w[2 * k]));
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(srow + ((j ^ (lane & 7)) << 4)), "r"(p[0]),
+                 "r"(p[1]), "r"(p[2]), "r"(p[3])
+                 : "memory");
+  }
+}
+
 // Writes 32 consecutive columns [n, n+32) of one row.
 __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32_t (&acc)[32],
                                                int64_t off, int n, int N) {
@@ -260,7 +301,8 @@ template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, Sched sched, EpiParams ep) {
+                   const __grid_constant__ CUtensorMap map_c,
+                   const __grid_constant__ CUtensorMap map_x, Sched sched, EpiParams ep) {
   using C = Cfg<BN, CG>;
   constexpr int BNL = BN / CG;  // B rows staged by this CTA
   extern __shared__ uint8_t smem_raw[];
@@ -274,7 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + C::kStages;
   uint64_t* tfull = bars + 2 * C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* auxbar = tempty + 2;  // [8 epilogue warps][2 staging buffers]: aux tile TMA loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + 2 * kEpiWarps);
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -293,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 32 * kEpiWarps * CG);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) ptx::mbar_init(&auxbar[i], 1);
     ptx::fence_barrier_init();
   }
   if (CG == 2) ptx::cluster_sync();  // both CTAs' barriers exist before any remote arrive / TMA
@@ -409,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_begin = BN >= 128 ? half * (BN / 2) : 0;
     uint8_t* stage_buf = smem_epi + (warp - 4) * 2 * kStageBufBytes;
     int buf = 0;
+    uint32_t aux_ph[2] = {0, 0};  // phases of this warp's two aux-load barriers
     int local = 0;
     const uint32_t tempty_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
     for (int t = unit0; t < sched.total; t += units) {
@@ -434,31 +479,76 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[g][i] = __uint_as_float(r[i]);
           }
+          const int n0 = ti.n0 + c, r0 = mrow0 + q * 32;
+          if (ep.aux_tma) {
+            // aux rows (residual / GELU input) arrive by TMA into this warp's staging box
+            // instead of 32 uncoalesced per-row loads; bias and GELU' applied in registers
+            uint8_t* sb = stage_buf + buf * kStageBufBytes;
+            uint64_t* ab = &auxbar[(warp - 4) * 2 + buf];
+            if (lane == 0) {
+              ptx::bulk_wait_read<1>();  // the store issued from this box two chunks ago has read it
+              ptx::mbar_arrive_expect_tx(ab, kStageBufBytes);
+              ptx::tma_load_2d(sb, &map_x, ab, n0, r0);
+            }
+            ptx::mbar_wait(ab, aux_ph[buf]);
+            aux_ph[buf] ^= 1;
+            const uint32_t srow = ptx::smem_u32(sb) + lane * 128;
 #pragma unroll
-          for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + ti.n0 + c + 32 * g, ti.n0 + c + 32 * g,
-                                                    sched.N, valid);
-          // this warp's staging box was last handed to TMA two chunks ago: wait until read
+            for (int j = 0; j < 8; ++j) {
+              uint32_t p[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3])
+                           : "r"(srow + ((j ^ (lane & 7)) << 4)));
+              float* w = &v[j >> 2][(j & 3) * 8];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float a0 = __uint_as_float(p[k] << 16), a1 = __uint_as_float(p[k] & 0xffff0000u);
+                if (ep.epilogue == kEpiGeluBwdBf16) {
+                  w[2 * k] *= gelu_tanh_grad(a0);
+                  w[2 * k + 1] *= gelu_tanh_grad(a1);
+                } else {  // residual
+                  w[2 * k] += a0;
+                  w[2 * k + 1] += a1;
+                }
+              }
+            }
+            __syncwarp();  // every lane has read the aux box before it is overwritten
+            if (ep.epilogue == kEpiBiasResidBf16 && ep.bias) {
+#pragma unroll
+              for (int g = 0; g < 2; ++g) epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
+            }
+          } else if (ep.epilogue == kEpiBiasGeluBf16 && ep.aux_out_tma) {
+            // U = pre-activation (bias added) -> staging box -> TMA store; then GELU
+#pragma unroll
+            for (int g = 0; g < 2; ++g) epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
+            if (lane == 0) ptx::bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* sb = stage_buf + buf * kStageBufBytes;
+            stage_row_bf16(sb, lane, v);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&map_x, sb, n0, r0);
+              ptx::bulk_commit();
+            }
+            buf ^= 1;
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[g][i] = gelu_tanh(v[g][i]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + n0 + 32 * g, n0 + 32 * g, sched.N, valid);
+          }
+          // this warp's staging box was last handed to TMA two bulk groups ago: wait until read
           if (lane == 0) ptx::bulk_wait_read<1>();
           __syncwarp();
           uint8_t* sb = stage_buf + buf * kStageBufBytes;
-          const uint32_t srow = ptx::smem_u32(sb) + lane * 128;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float* w = &v[j >> 2][(j & 3) * 8];
-            uint32_t p[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(w[2 * k], w[2 * k + 1]);
-              p[k] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(srow + ((j ^ (lane & 7)) << 4)),
-                         "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3])
-                         : "memory");
-          }
+          stage_row_bf16(sb, lane, v);
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&map_c, sb, ti.n0 + c, mrow0 + q * 32);
+            ptx::tma_store_2d(&map_c, sb, n0, r0);
             ptx::bulk_commit();
           }
           buf ^= 1;
@@ -587,6 +677,14 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
   if (!tma_store) mc = ma;  // unused placeholder
+  // aux tiles share C's layout (ldc): residual / GELU input loaded, pre-activation stored by TMA
+  CUtensorMap mx = mc;
+  bool aux_tma = false, aux_out_tma = false;
+  if (tma_store && (a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiGeluBwdBf16) && a.aux &&
+      (reinterpret_cast<uintptr_t>(a.aux) % 16) == 0)
+    aux_tma = make_store_map(&mx, const_cast<void*>(a.aux), a.M, a.N, a.ldc);
+  if (tma_store && a.epilogue == kEpiBiasGeluBf16 && a.aux_out && (reinterpret_cast<uintptr_t>(a.aux_out) % 16) == 0)
+    aux_out_tma = make_store_map(&mx, a.aux_out, a.M, a.N, a.ldc);
   Sched s;
   s.tile_m = kBM * CG;
   s.m_tiles = (a.M + s.tile_m - 1) / s.tile_m;
@@ -632,11 +730,13 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.aux = static_cast<const __nv_bfloat16*>(a.aux);
   ep.aux_out = static_cast<__nv_bfloat16*>(a.aux_out);
   ep.tma_store = tma_store ? 1 : 0;
+  ep.aux_tma = aux_tma ? 1 : 0;
+  ep.aux_out_tma = aux_out_tma ? 1 : 0;
   int units = workers;
   if (s.total < units) units = s.total;
   if (units < 1) return cudaSuccess;
   if (CG == 1) {
-    kern<<<units, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, s, ep);
+    kern<<<units, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, mx, s, ep);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(units * CG);
@@ -650,7 +750,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, s, ep);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, s, ep);
     if (e != cudaSuccess) return e;
   }
   note_launch();

@@ -96,8 +96,10 @@ def test_gemm_accumulate(cuda):
     assert relerr(C.view(M, N), ref) < 1e-5
 
 
-def test_gemm_bias_resid_gelu(cuda):
-    M, N, K = 256, 768, 256
+@pytest.mark.parametrize("M,N,K", [(256, 768, 256), (200, 200, 96), (640, 3072, 768)])
+def test_gemm_bias_resid_gelu(cuda, M, N, K):
+    # fused epilogues; residual / GELU input / pre-activation tiles move by TMA through the
+    # epilogue staging boxes (edge tiles clipped)
     A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
     B = (0.1 * torch.randn(N, K, device=cuda)).to(torch.bfloat16)
     bias = torch.randn(N, device=cuda).to(torch.bfloat16)

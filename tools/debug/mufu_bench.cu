@@ -1,0 +1,44 @@
+// MUFU throughput: tanh.approx.f32, ex2.approx.f32, tanh.approx.bf16x2, rcp.approx (ops/clk/SM).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_bf16.h>
+template <int MODE>
+__global__ void k(float* out, int iters) {
+  float x0 = threadIdx.x * 1e-3f, x1 = x0 + 0.1f, x2 = x0 + 0.2f, x3 = x0 + 0.3f;
+  uint32_t h0 = 0x3f003f00u + threadIdx.x, h1 = h0 + 7, h2 = h0 + 11, h3 = h0 + 13;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    if (MODE == 0) {
+      asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x0)); asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x1));
+      asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x2)); asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x3));
+    } else if (MODE == 1) {
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x0)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x1));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x2)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x3));
+    } else if (MODE == 2) {
+      asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h0)); asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h1));
+      asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h2)); asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h3));
+    } else {
+      asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x0)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x1));
+      asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x2)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x3));
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[MODE] = float(t1 - t0);
+  if (x0 + x1 + x2 + x3 == 12345.f || (h0 ^ h1 ^ h2 ^ h3) == 1u) out[8] = 1;
+}
+int main() {
+  float* d; cudaMalloc(&d, 64);
+  const int iters = 4096, threads = 1024;
+  const char* n[4] = {"tanh.f32", "ex2.f32", "tanh.bf16x2", "rcp.f32"};
+  for (int m = 0; m < 4; ++m) {
+    for (int r = 0; r < 2; ++r) {
+      if (m == 0) k<0><<<148, threads>>>(d, iters);
+      if (m == 1) k<1><<<148, threads>>>(d, iters);
+      if (m == 2) k<2><<<148, threads>>>(d, iters);
+      if (m == 3) k<3><<<148, threads>>>(d, iters);
+    }
+    cudaDeviceSynchronize();
+    float c; cudaMemcpy(&c, d + m, 4, cudaMemcpyDeviceToHost);
+    printf("%-12s %.2f instr/clk/SM (%s)\n", n[m], 4.0 * iters * threads / c, cudaGetErrorString(cudaGetLastError()));
+  }
+}

@@ -35,6 +35,8 @@ def main():
     torch.manual_seed(0)
     # name, M, N, K, a_major, b_major, epilogue
     shapes = [("fwd qkv", T, 3 * h, h, 0, 0, 0), ("fwd fc", T, f, h, 0, 0, 0), ("fwd proj", T, h, f, 0, 0, 0),
+              ("fwd fc +bias+GELU(+U)", T, f, h, 0, 0, 5), ("fwd proj +bias+resid", T, h, f, 0, 0, 4),
+              ("dgrad fc +GELU'", T, f, h, 0, 1, 6),
               ("lm head", T, V, h, 0, 0, 0), ("dgrad proj", T, f, h, 0, 1, 0), ("dgrad fc", T, h, f, 0, 1, 0),
               ("wgrad fc", f, h, T, 1, 1, 7), ("wgrad qkv", 3 * h, h, T, 1, 1, 7)]
     print(f"| shape | M | N | K | ours 148 SM TF/s | ours 132 SM TF/s | cuBLAS 148 SM TF/s |")
@@ -48,8 +50,16 @@ def main():
             C = torch.empty(M * N, device=dev, dtype=torch.bfloat16)
         fl = 2.0 * M * N * K
         res = []
+        extra = {}
+        if epi in (4, 5, 6):
+            extra["bias"] = (torch.randn(N, device=dev) * 0.1).to(torch.bfloat16) if epi in (4, 5) else None
+            aux = (torch.randn(M * N, device=dev) * 0.1).to(torch.bfloat16)
+            if epi == 5:
+                extra["aux_out"] = aux
+            else:
+                extra["aux"] = aux
         for cap in (0, 132):
-            kw = dict(c=C, ldc=N, epilogue=epi, sync=False, max_ctas=cap, split_k=-1 if epi == 7 else 1)
+            kw = dict(c=C, ldc=N, epilogue=epi, sync=False, max_ctas=cap, split_k=-1 if epi == 7 else 1, **extra)
             ms = timeit(lambda: run_gemm(A, am, B, bm, M, N, K, **kw))
             res.append(fl / ms / 1e9)
         At = A.view(M, K) if am == 0 else A.view(K, M).t()
