@@ -460,9 +460,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileInfo ti = sched.tile(t);
       if (ti.skip) continue;
       const int acc = local & 1;
+      const int mrow0 = ti.m0 + int(cr) * kBM;  // this CTA's 128 accumulator rows
+      if (ep.tma_store && ep.aux_tma) {
+        // prefetch this tile's aux boxes (one per 64-column chunk, box j in staging buffer j)
+        // before the accumulator is ready; the previous tile's stores must have read the boxes
+        if (lane == 0) {
+          ptx::bulk_wait_read<0>();
+          for (int j = 0; j < 2 && c_begin + 64 * j < c_begin + cols && ti.n0 + c_begin + 64 * j < sched.N; ++j) {
+            uint64_t* ab = &auxbar[(warp - 4) * 2 + j];
+            ptx::mbar_arrive_expect_tx(ab, kStageBufBytes);
+            ptx::tma_load_2d(stage_buf + j * kStageBufBytes, &map_x, ab, ti.n0 + c_begin + 64 * j, mrow0 + q * 32);
+          }
+        }
+      }
       ptx::mbar_wait(&tfull[acc], (local >> 1) & 1);
       ptx::tc_fence_after();
-      const int mrow0 = ti.m0 + int(cr) * kBM;  // this CTA's 128 accumulator rows
       const int row = mrow0 + q * 32 + lane;
       const bool valid = row < sched.M;
       const int64_t row_off = ti.z1 * ep.cs1 + ti.z2 * ep.cs2 + int64_t(row) * ep.ldc;
@@ -483,15 +495,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (ep.aux_tma) {
             // aux rows (residual / GELU input) arrive by TMA into this warp's staging box
             // instead of 32 uncoalesced per-row loads; bias and GELU' applied in registers
-            uint8_t* sb = stage_buf + buf * kStageBufBytes;
-            uint64_t* ab = &auxbar[(warp - 4) * 2 + buf];
-            if (lane == 0) {
-              ptx::bulk_wait_read<1>();  // the store issued from this box two chunks ago has read it
-              ptx::mbar_arrive_expect_tx(ab, kStageBufBytes);
-              ptx::tma_load_2d(sb, &map_x, ab, n0, r0);
-            }
-            ptx::mbar_wait(ab, aux_ph[buf]);
-            aux_ph[buf] ^= 1;
+            const int j = (c - c_begin) >> 6;  // chunk index == staging box of its prefetched aux
+            buf = j;
+            uint8_t* sb = stage_buf + j * kStageBufBytes;
+            uint64_t* ab = &auxbar[(warp - 4) * 2 + j];
+            ptx::mbar_wait(ab, aux_ph[j]);
+            aux_ph[j] ^= 1;
             const uint32_t srow = ptx::smem_u32(sb) + lane * 128;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
