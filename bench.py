@@ -333,10 +333,11 @@ def main():
             peaks = json.load(f)
         fl, sec, nl, tr = g_all[0]
         achieved = fl / sec / 1e12 if sec > 0 else 0.0
-        # GEMMs are timed inside a long step under the power cap: the sustained bf16 figure is the
-        # denominator (the burst-figure fraction is reported beside it)
-        peak = peaks["bf16_tflops_sustained"] * tr / 148.0
-        peak_burst = peaks["bf16_tflops"] * tr / 148.0
+        # Denominator: the burst bf16 figure (conservative: the GEMMs of the larger models run
+        # above the 4-second sustained figure inside the step); the sustained fraction is
+        # reported beside it
+        peak = peaks["bf16_tflops"] * tr / 148.0
+        peak_sust = peaks["bf16_tflops_sustained"] * tr / 148.0
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
         if os.path.exists(tpath):
@@ -363,8 +364,9 @@ def main():
                          "frac": achieved / peak if peak else None,
                          "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                          "traffic_note": traffic["note"] if traffic else None,
-                         "peak_note": f"MEASURED_PEAKS bf16_tflops_sustained {peaks['bf16_tflops_sustained']} x {tr}/148 "
-                                      f"SM budget; vs burst {peaks['bf16_tflops']}: frac {achieved / peak_burst:.3f}",
+                         "frac_vs_sustained": achieved / peak_sust if peak_sust else None,
+                         "peak_note": f"MEASURED_PEAKS bf16_tflops (burst) {peaks['bf16_tflops']} x {tr}/148 SM budget; "
+                                      f"sustained {peaks['bf16_tflops_sustained']} x {tr}/148 for frac_vs_sustained",
                          "launches": nl},
             "roofline_hbm": {"kernel": "adam_k (fused accumulate + AdamW + bf16 cast), rank 0", "bound": "hbm",
                              "achieved": adam_all[0][0] / adam_all[0][1] / 1e9 if adam_all[0][1] else None,
