@@ -454,56 +454,72 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }
 
 // ============================================================================ backward
-// Warp roles: 0-7 P/dS builders (TMEM lane quarter w % 4, key half w / 4), 8-11 dQ reducers and
-// dK/dV epilogue (lane quarter w % 4), 12 TMA producer, 13 MMA issuer. The dQ atomics of query
-// tile i overlap the P/dS construction of tile i+1.
+// Transposed formulation: one CTA task = 128 keys of one (head, sample); for every query tile at
+// or above the diagonal the MMA warp computes S^T = K Q^T and dP^T = V dO^T into TMEM (keys on
+// the TMEM lanes). Eight builder warps turn them into P^T = exp2(S^T c - LSE) and
+// dS'^T = P^T (dP^T - D) (per-query LSE and D come with the Q/dO stage) and write them back into
+// TMEM as packed bf16 (P^T into its own columns, dS'^T in place over dP^T once both column halves
+// of a row have read it), and dS'^T also into shared memory. S^T of the next tile is issued as
+// soon as the builders have read this one, so it overlaps their work. Then dV += P^T dO and dK += dS'^T Q take P^T / dS'^T as
+// TMEM A operands (no shared-memory round trip), and dQ_tile = dS' K reads the shared dS'^T tile
+// as an MN-major operand. Four warps read dQ out of TMEM and add it into the fp32 dQ with TMA
+// bulk reduce-add; after a task's last tile they write dK (scaled) and dV.
+// Warp roles: 0-7 builders (TMEM lane quarter w % 4, query half w / 4), 8-11 dQ / dK dV out,
+// 12 TMA producer, 13 MMA issuer. K/V are double-buffered so the next task's key tile loads
+// while this one runs.
 constexpr int kBwdThreads = 448;
-constexpr int kBwdQD = 3;  // Q/dO stages: a stage is held from its load until dV/dK/dQ of its tile
-constexpr int kBwdKV = 1;  // K/V stages (2 would let the next task's key tile load early; smem-bound)
-constexpr int kBwdPS = 1;  // P/dS shared-memory buffers
+constexpr int kBwdQD = 3;  // Q/dO (+LSE, D) stages
+constexpr int kBwdKV = 2;  // K/V stages
+// TMEM columns: S^T, dP^T (-> dS'^T packed), dV, dK, dQ, P^T packed
+constexpr int kBwdTS = 0, kBwdTDP = 128, kBwdTDV = 256, kBwdTDK = 320, kBwdTDQ = 384, kBwdTP = 448;
 
 struct BwdSmem {
   static constexpr int kK = 0;                        // kBwdKV stages
   static constexpr int kV = kK + kBwdKV * kTile;      // kBwdKV stages
   static constexpr int kQ = kV + kBwdKV * kTile;      // kBwdQD stages
-  static constexpr int kDO = kQ + kBwdQD * kTile;      // kBwdQD stages
-  static constexpr int kP = kDO + kBwdQD * kTile;      // kBwdPS buffers of [128, 128]
-  static constexpr int kDS = kP + kBwdPS * 2 * kTile;  // kBwdPS buffers of [128, 128]
-  static constexpr int kDQ = kDS + kBwdPS * 2 * kTile;  // dQ staging: 4 warps x [32 rows x 64] fp32
-  static constexpr int kBar = kDQ + 4 * 32 * 64 * 4;
+  static constexpr int kDO = kQ + kBwdQD * kTile;     // kBwdQD stages
+  static constexpr int kDS = kDO + kBwdQD * kTile;    // dS'^T [128 keys, 128 queries]
+  static constexpr int kDQ = kDS + 2 * kTile;         // dQ staging: 4 warps x [32 rows x 32] fp32
+  static constexpr int kLD = kDQ + 4 * 32 * 32 * 4;   // kBwdQD stages x {LSE, D}[128] fp32
+  static constexpr int kBar = kLD + kBwdQD * 2 * 128 * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
+static_assert(BwdSmem::kBytes <= 232448, "backward shared memory");
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                     const __grid_constant__ CUtensorMap map_dq,
-                    const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
+                    const float* __restrict__ lse, const float* __restrict__ dvec,
                     bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::kBar);
-  uint64_t* kv_full = bar + 0;                          // [kBwdKV]
-  uint64_t* kv_empty = bar + kBwdKV;                    // [kBwdKV]
-  uint64_t* qd_full = bar + 2 * kBwdKV;                 // [kBwdQD]
-  uint64_t* qd_empty = bar + 2 * kBwdKV + kBwdQD;       // [kBwdQD]
-  uint64_t* sp_full = bar + 2 * kBwdKV + 2 * kBwdQD;
-  uint64_t* s_free = sp_full + 1;
-  uint64_t* ps_full = sp_full + 2;   // [kBwdPS] P/dS buffer written (builders -> MMA)
-  uint64_t* mm_done = sp_full + 4;   // [kBwdPS] dV/dK/dQ products of the buffer's tile done
-  uint64_t* acc_free = sp_full + 6;
-  uint64_t* dq_free = sp_full + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sp_full + 8);
+  uint64_t* kv_full = bar + 0;                     // [kBwdKV]
+  uint64_t* kv_empty = bar + kBwdKV;               // [kBwdKV]
+  uint64_t* qd_full = bar + 2 * kBwdKV;            // [kBwdQD]
+  uint64_t* qd_empty = qd_full + kBwdQD;           // [kBwdQD]
+  uint64_t* s_full = qd_full + 2 * kBwdQD;         // S^T in TMEM
+  uint64_t* s_free = s_full + 1;                   // S^T read by the builders
+  uint64_t* dp_full = s_full + 2;                  // dP^T in TMEM
+  uint64_t* pt_full = s_full + 3;                  // P^T, dS'^T in TMEM
+  uint64_t* dk_done = s_full + 4;                  // dK product done: dS'^T TMEM (dP^T columns) reusable
+  uint64_t* mm_done = s_full + 5;                  // dQ product done: dQ in TMEM, dS' smem free
+  uint64_t* acc_free = s_full + 6;                 // dK/dV read out by the epilogue
+  uint64_t* dq_free = s_full + 7;                  // dQ read out of TMEM
+  uint64_t* dv_done = s_full + 8;                  // dV product done: P^T TMEM reusable
+  uint64_t* ds_full = s_full + 9;                  // dS'^T in shared memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 10);
 
   const int warp = int(ptx::warp_id());
   const int lane = threadIdx.x & 31;
   const int nt = seq / kT;
   const int ntasks = nt * nz;
   const int h = heads * kD;
-  const float scale_log2 = scale * kLog2e;
 
   if (warp == 12 && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::tma_prefetch_desc(&map_do);
+    ptx::tma_prefetch_desc(&map_dq);
     for (int i = 0; i < kBwdKV; ++i) {
       ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
@@ -512,12 +528,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(&qd_full[i], 1);
       ptx::mbar_init(&qd_empty[i], 1);
     }
-    ptx::mbar_init(sp_full, 1);
+    ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_free, 256);
-    for (int i = 0; i < kBwdPS; ++i) {
-      ptx::mbar_init(&ps_full[i], 256);
-      ptx::mbar_init(&mm_done[i], 1);
-    }
+    ptx::mbar_init(dp_full, 1);
+    ptx::mbar_init(pt_full, 256);
+    ptx::mbar_init(ds_full, 256);
+    ptx::mbar_init(dk_done, 1);
+    ptx::mbar_init(dv_done, 1);
+    ptx::mbar_init(mm_done, 1);
     ptx::mbar_init(acc_free, 128);
     ptx::mbar_init(dq_free, 128);
     ptx::fence_barrier_init();
@@ -527,35 +545,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 320, t_dq = tmem + 384;
 
   if (warp == 12) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
-      ZP_TRACE_INIT;
       int stage = 0;
       uint32_t phase = 0, item = 0;
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task_static(t, nz);
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
-        ZP_TRACE(3, 7);
         const int kvs = item % kBwdKV;
         ptx::mbar_wait(&kv_empty[kvs], ((item / kBwdKV) & 1) ^ 1);
-        ZP_TRACE(3, 8);
         ptx::mbar_arrive_expect_tx(&kv_full[kvs], 2 * kTile);
         ptx::tma_load_4d(sm + BwdSmem::kK + kvs * kTile, &map_qkv, &kv_full[kvs], h + head * kD,
                          row0 + tk.tile * kT, 0, 0);
         ptx::tma_load_4d(sm + BwdSmem::kV + kvs * kTile, &map_qkv, &kv_full[kvs], 2 * h + head * kD,
                          row0 + tk.tile * kT, 0, 0);
         for (int i = tk.tile; i < nt; ++i) {
-          ZP_TRACE(3, 1);
           ptx::mbar_wait(&qd_empty[stage], phase ^ 1);
-          ZP_TRACE(3, 2);
-          ptx::mbar_arrive_expect_tx(&qd_full[stage], 2 * kTile);
+          ptx::mbar_arrive_expect_tx(&qd_full[stage], 2 * kTile + 2 * 128 * 4);
           ptx::tma_load_4d(sm + BwdSmem::kQ + stage * kTile, &map_qkv, &qd_full[stage], head * kD,
                            row0 + i * kT, 0, 0);
           ptx::tma_load_4d(sm + BwdSmem::kDO + stage * kTile, &map_do, &qd_full[stage], head * kD,
                            row0 + i * kT, 0, 0);
+          const int64_t q0 = int64_t(tk.z) * seq + int64_t(i) * kT;
+          ptx::bulk_load(sm + BwdSmem::kLD + stage * 1024, lse + q0, 512, &qd_full[stage]);
+          ptx::bulk_load(sm + BwdSmem::kLD + stage * 1024 + 512, dvec + q0, 512, &qd_full[stage]);
           if (++stage == kBwdQD) {
             stage = 0;
             phase ^= 1;
@@ -565,197 +580,234 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 13) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
+      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS' (MN-major), B = K
       ZP_TRACE_INIT;
-      // S/dP of query tile i+1 are issued before the dV/dK/dQ products of tile i, so the builders
-      // compute P/dS(i+1) while the tensor pipe works on tile i.
-      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S, dP
-      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dV, dK (A^T, B MN-major)
-      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dQ
-      uint32_t sk = 0, sv = 0;  // this task's K/V stage
-      const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
       const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
-      int ss = 0, sm2 = 0;  // Q/dO stage of the next S/dP issue and of the next dV/dK/dQ issue
+      int ss = 0;  // Q/dO stage of the tile whose products are issued next
       uint32_t ss_ph = 0, item = 0, it = 0;
-      auto issue_sdp = [&](uint32_t s_parity) {
-        ZP_TRACE(0, 1);
-        ptx::mbar_wait(&qd_full[ss], ss_ph);
-        ZP_TRACE(0, 2);
-        ptx::mbar_wait(s_free, s_parity);
-        ZP_TRACE(0, 3);
-        ptx::tc_fence_after();
-        const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
-        const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
+      // S^T / dP^T of the tile in Q/dO stage st
+      auto issue_s = [&](uint32_t sk, int st) {
+        const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + st * kTile);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          ptx::umma_bf16(t_s, kdesc(sq, k), kdesc(sk, k), id_ss, k > 0);
-          ptx::umma_bf16(t_dp, kdesc(sdo, k), kdesc(sv, k), id_ss, k > 0);
-        }
-        ptx::umma_commit(sp_full);
-        if (++ss == kBwdQD) {
-          ss = 0;
-          ss_ph ^= 1;
-        }
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTS, kdesc(sk, k), kdesc(sq, k), id_ss, k > 0);
+        ptx::umma_commit(s_full);
+      };
+      auto issue_dp = [&](uint32_t sv, int st) {
+        const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + st * kTile);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTDP, kdesc(sv, k), kdesc(sdo, k), id_ss, k > 0);
+        ptx::umma_commit(dp_full);
       };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task_static(t, nz);
         const int kvs = item % kBwdKV;
         ptx::mbar_wait(&kv_full[kvs], (item / kBwdKV) & 1);
-        sk = ptx::smem_u32(sm + BwdSmem::kK + kvs * kTile);
-        sv = ptx::smem_u32(sm + BwdSmem::kV + kvs * kTile);
-        ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // epilogue of the previous task read dK/dV
-        issue_sdp((it & 1) ^ 1);
+        const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK + kvs * kTile);
+        const uint32_t sv = ptx::smem_u32(sm + BwdSmem::kV + kvs * kTile);
+        // prologue: S^T / dP^T of the task's first tile
+        ptx::mbar_wait(&qd_full[ss], ss_ph);
+        ptx::mbar_wait(s_free, (it & 1) ^ 1);   // builders read the previous S^T
+        ptx::tc_fence_after();
+        issue_s(sk, ss);
+        ptx::mbar_wait(dk_done, (it & 1) ^ 1);  // previous dK read dS'^T out of the dP^T columns
+        ptx::tc_fence_after();
+        issue_dp(sv, ss);
+        int nx = ss + 1 == kBwdQD ? 0 : ss + 1;  // stage of the next tile
+        uint32_t nx_ph = ss + 1 == kBwdQD ? (ss_ph ^ 1) : ss_ph;
         for (int i = tk.tile; i < nt; ++i, ++it) {
-          if (i + 1 < nt) issue_sdp(it & 1);  // builders have pulled S/dP(i) out of TMEM
-          const int pb = it % kBwdPS;  // P/dS buffer of this tile
-          ZP_TRACE(0, 4);
-          ptx::mbar_wait(&ps_full[pb], (it / kBwdPS) & 1);
-          ZP_TRACE(0, 5);
-          ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
-          ZP_TRACE(0, 6);
-          ptx::tc_fence_after();
-          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + sm2 * kTile);
-          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + sm2 * kTile);
-          const bool first = (i == tk.tile);
-          // interleaved by k step so consecutive MMAs target different accumulators
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            ptx::umma_bf16(t_dv, mndesc(spp + pb * 2 * kTile, k), mndesc(sdo, k), id_t, (!first || k > 0));
-            ptx::umma_bf16(t_dk, mndesc(sds + pb * 2 * kTile, k), mndesc(sq, k), id_t, (!first || k > 0));
-            ptx::umma_bf16(t_dq, kdesc2(sds + pb * 2 * kTile, k), mndesc(sk, k), id_q, k > 0);
+          const bool more = i + 1 < nt;
+          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
+          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
+          ZP_TRACE(0, 1);
+          if (more) {  // S^T(i+1) as soon as the builders have read S^T(i)
+            ptx::mbar_wait(&qd_full[nx], nx_ph);
+            ZP_TRACE(0, 2);
+            ptx::mbar_wait(s_free, it & 1);
+            ZP_TRACE(0, 3);
+            ptx::tc_fence_after();
+            issue_s(sk, nx);
           }
-          ptx::umma_commit(&mm_done[pb]);
-          ptx::umma_commit(&qd_empty[sm2]);
+          const bool first = (i == tk.tile);
+          if (first) ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // previous task's dK/dV read out
+          ZP_TRACE(0, 4);
+          ptx::mbar_wait(pt_full, it & 1);
+          ZP_TRACE(0, 5);
+          ptx::tc_fence_after();
+          // dK first: its dS'^T operand sits in the dP^T columns, which dP^T(i+1) reuses
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_ts(tmem + kBwdTDK, tmem + kBwdTDP + 8 * k, mndesc(sq, k), id_t, (!first || k > 0));
+          ptx::umma_commit(dk_done);
+          if (more) {  // dP^T(i+1) overwrites dS'^T(i): after dK(i) has read it
+            ZP_TRACE(0, 6);
+            ptx::mbar_wait(dk_done, it & 1);
+            ZP_TRACE(0, 7);
+            ptx::tc_fence_after();
+            issue_dp(sv, nx);
+          }
+          // dV while the builders already work on tile i+1 (they wait for it before writing P^T)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_ts(tmem + kBwdTDV, tmem + kBwdTP + 8 * k, mndesc(sdo, k), id_t, (!first || k > 0));
+          ptx::umma_commit(dv_done);
+          ZP_TRACE(0, 8);
+          ptx::mbar_wait(ds_full, it & 1);         // dS'^T in shared memory
+          ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kBwdTDQ, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
+          ptx::umma_commit(mm_done);
+          ptx::umma_commit(&qd_empty[ss]);
           if (i == nt - 1) ptx::umma_commit(&kv_empty[kvs]);
-          if (++sm2 == kBwdQD) sm2 = 0;
+          ss = nx;
+          ss_ph = nx_ph;
+          if (++nx == kBwdQD) {
+            nx = 0;
+            nx_ph ^= 1;
+          }
         }
       }
     }
-  } else if (warp < 8) {  // ------------------------------------------ P / dS builders
+  } else if (warp < 8) {  // ------------------------------------------ P^T / dS'^T builders
     ZP_TRACE_INIT;
     const int q4 = warp & 3, kh = warp >> 2;
-    const int r = q4 * 32 + lane;
+    const int r = q4 * 32 + lane;  // key row of the tile == TMEM lane
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
-    const uint32_t spp = ptx::smem_u32(sm + BwdSmem::kP);
     const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
-    uint32_t it = 0;
+    int ss = 0;
+    uint32_t ss_ph = 0, it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
       const AttnTask tk = bwd_task_static(t, nz);
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        const int64_t qrow = int64_t(tk.z) * seq + int64_t(i) * kT + r;
-        const float lse2 = lse[qrow] * kLog2e;
-        const float dd = dvec[qrow];
+        ptx::mbar_wait(&qd_full[ss], ss_ph);  // this stage's LSE / D (already complete: S^T needed Q)
         if (warp == 0 && lane == 0) ZP_TRACE(1, 1);
-        ptx::mbar_wait(sp_full, it & 1);
+        ptx::mbar_wait(s_full, it & 1);
         if (warp == 0 && lane == 0) ZP_TRACE(1, 2);
         ptx::tc_fence_after();
-        uint32_t vs[2][32], vp[2][32];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          ptx::tmem_ld_32x32b_x32(t_s + lane_off + kh * 64 + c * 32, vs[c]);
-          ptx::tmem_ld_32x32b_x32(t_dp + lane_off + kh * 64 + c * 32, vp[c]);
-        }
-        ptx::tmem_ld_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(s_free);
-        // P = exp2(S*scale*log2e - LSE*log2e); dS' = P (dP - D) (the softmax scale of dS is
-        // applied once to dK and dQ at the end). Only the diagonal tile is masked.
-        uint32_t pk[32], dk[32];  // packed bf16 pairs of this thread's 64 P and dS' values
-        const bool diag = (i == tk.tile);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pv[2], dv[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              pv[u] = ex2(fmaf(__uint_as_float(vs[c][e + u]), scale_log2, -lse2));
-              dv[u] = pv[u] * (__uint_as_float(vp[c][e + u]) - dd);
-            }
-            pk[c * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
-            dk[c * 16 + e / 2] = pack_bf16(dv[0], dv[1]);
-          }
-        }
-        if (diag) {  // key > query: P = dS = 0 (zero the packed halves)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int key0 = kh * 64 + 2 * e;
-            const uint32_t keep = (key0 > r ? 0u : 0xffffu) | (key0 + 1 > r ? 0u : 0xffff0000u);
-            pk[e] &= keep;
-            dk[e] &= keep;
-          }
-        }
-        // P/dS smem is free once the dV/dK/dQ products of the previous tile completed
-        // the P/dS buffer is free once the products of tile it - kBwdPS completed
-        const int pb = it % kBwdPS;
+        ptx::mbar_wait(dp_full, it & 1);
         if (warp == 0 && lane == 0) ZP_TRACE(1, 3);
-        ptx::mbar_wait(&mm_done[pb], ((it / kBwdPS) & 1) ^ 1);
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 4);
+        ptx::tc_fence_after();
+        // per-query LSE and D of this stage (broadcast shared reads), indexed from the __shared__
+        // array itself so the compiler emits schedulable LDS
+        const float4* ld4 = reinterpret_cast<const float4*>(smem_raw + (sm - smem_raw) + BwdSmem::kLD + ss * 1024);
+        const float sl2 = scale * kLog2e;
+        uint32_t dk[32];  // packed bf16 pairs of this thread's 64 dS'^T values
+        // two passes of 32 query columns keep the live registers low
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const uint32_t off = p_off(r, kh * 64 + g * 8);
-          st_shared_v4(spp + pb * 2 * kTile + off, pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-          st_shared_v4(sds + pb * 2 * kTile + off, dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+        for (int c = 0; c < 2; ++c) {
+          uint32_t vs[32], vp[32], pk[16];
+          ptx::tmem_ld_32x32b_x32(tmem + kBwdTS + lane_off + kh * 64 + c * 32, vs);
+          ptx::tmem_ld_32x32b_x32(tmem + kBwdTDP + lane_off + kh * 64 + c * 32, vp);
+          ptx::tmem_ld_wait();
+          if (c == 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(s_free);  // S^T fully read: the MMA warp may issue the next one
+          }
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const int q = kh * 64 + c * 32 + e;
+            const float4 lq = ld4[q / 4], dq4 = ld4[32 + q / 4];
+            const float l4[4] = {lq.x, lq.y, lq.z, lq.w}, d4[4] = {dq4.x, dq4.y, dq4.z, dq4.w};
+            float pv[4], dv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              pv[u] = ex2(fmaf(__uint_as_float(vs[e + u]), sl2, -l4[u] * kLog2e));
+              dv[u] = pv[u] * (__uint_as_float(vp[e + u]) - d4[u]);
+            }
+            pk[e / 2] = pack_bf16(pv[0], pv[1]);
+            pk[e / 2 + 1] = pack_bf16(pv[2], pv[3]);
+            dk[c * 16 + e / 2] = pack_bf16(dv[0], dv[1]);
+            dk[c * 16 + e / 2 + 1] = pack_bf16(dv[2], dv[3]);
+          }
+          if (i == tk.tile) {  // diagonal tile: key (row r) > query (column) gives P = dS = 0
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int q0 = kh * 64 + c * 32 + 2 * e;
+              const uint32_t keep = (r > q0 ? 0u : 0xffffu) | (r > q0 + 1 ? 0u : 0xffff0000u);
+              pk[e] &= keep;
+              dk[c * 16 + e] &= keep;
+            }
+          }
+          if (c == 0) {
+            ptx::mbar_wait(dv_done, (it & 1) ^ 1);  // dV of the previous tile has read P^T
+            ptx::tc_fence_after();
+          }
+          ptx::tmem_st_32x32b_x16(tmem + kBwdTP + lane_off + kh * 32 + c * 16, pk);
         }
-        fence_proxy_async();
-        ptx::mbar_arrive(&ps_full[pb]);
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 4);
+        // both column halves of these rows have read dP^T before either overwrites it
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+        ptx::tmem_st_32x32b_x32(tmem + kBwdTDP + lane_off + kh * 32, dk);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(pt_full);  // dK / dV may start
+        // dS'^T into shared memory for dQ = dS' K, once dQ of the previous tile has read it
+        ptx::mbar_wait(mm_done, (it & 1) ^ 1);
         if (warp == 0 && lane == 0) ZP_TRACE(1, 5);
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          st_shared_v4(sds + p_off(r, kh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+        fence_proxy_async();
+        ptx::mbar_arrive(ds_full);
+        if (warp == 0 && lane == 0) ZP_TRACE(1, 6);
+        if (++ss == kBwdQD) {
+          ss = 0;
+          ss_ph ^= 1;
+        }
       }
     }
   } else {  // --------------------------------------------------------- warps 8-11: dQ + dK/dV out
-    ZP_TRACE_INIT;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    uint8_t* stg = sm + BwdSmem::kDQ + q4 * (32 * 32 * 4);
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
       const AttnTask tk = bwd_task_static(t, nz);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        if (warp == 8 && lane == 0) ZP_TRACE(2, 1);
-        ptx::mbar_wait_sleep(&mm_done[it % kBwdPS], (it / kBwdPS) & 1, 1000);
-        if (warp == 8 && lane == 0) ZP_TRACE(2, 2);
+        ptx::mbar_wait_sleep(mm_done, it & 1, 1000);
         ptx::tc_fence_after();
         uint32_t v[2][32];
-        ptx::tmem_ld_32x32b_x32(t_dq + lane_off, v[0]);
-        ptx::tmem_ld_32x32b_x32(t_dq + lane_off + 32, v[1]);
+        ptx::tmem_ld_32x32b_x32(tmem + kBwdTDQ + lane_off, v[0]);
+        ptx::tmem_ld_32x32b_x32(tmem + kBwdTDQ + lane_off + 32, v[1]);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(dq_free);
-        // dQ tile rows of this warp -> swizzled fp32 staging -> TMA reduce-add into dq32 (the
-        // reduction happens in L2 in whole lines; no per-thread atomics)
-        uint8_t* stg = sm + BwdSmem::kDQ + q4 * (32 * 64 * 4);
-        if (lane == 0) ptx::bulk_wait_read<0>();  // the previous tile's reduce has read the staging
-        __syncwarp();
+        // this warp's 32 dQ rows, 32 columns at a time -> swizzled fp32 box -> TMA reduce-add
+        const int row = smp * seq + i * kT + q4 * 32;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const uint32_t rowa = ptx::smem_u32(stg + c * 4096) + lane * 128;
+          if (lane == 0) ptx::bulk_wait_read<0>();  // the previous reduce has read the box
+          __syncwarp();
+          const uint32_t rowa = ptx::smem_u32(stg) + lane * 128;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + ((j ^ (lane & 7)) << 4)),
                          "r"(v[c][4 * j]), "r"(v[c][4 * j + 1]), "r"(v[c][4 * j + 2]), "r"(v[c][4 * j + 3])
                          : "memory");
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          const int row = smp * seq + i * kT + q4 * 32;
-          ptx::tma_reduce_add_2d(&map_dq, stg, head * kD, row);
-          ptx::tma_reduce_add_2d(&map_dq, stg + 4096, head * kD + 32, row);
-          ptx::bulk_commit();
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_reduce_add_2d(&map_dq, stg, head * kD + 32 * c, row);
+            ptx::bulk_commit();
+          }
         }
       }
-      // epilogue: dK, dV rows of this key tile -> bf16 into dqkv (all MMAs of the task are done)
+      // epilogue: dK (scaled), dV rows of this key tile -> bf16 into dqkv
       const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
         bf16* dst = dqkv + krow * 3 * h + (which == 0 ? h : 2 * h) + head * kD;
-        const uint32_t src = (which == 0 ? t_dk : t_dv) + lane_off;
+        const uint32_t src = tmem + (which == 0 ? kBwdTDK : kBwdTDV) + lane_off;
+        const float f = which == 0 ? scale : 1.f;  // dK = scale * dS'^T Q
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t v[32];
           ptx::tmem_ld_32x32b_x32(src + c * 32, v);
           ptx::tmem_ld_wait();
-          const float f = which == 0 ? scale : 1.f;  // dK = scale * dS'^T Q
 #pragma unroll
           for (int e = 0; e < 32; e += 8) {
             uint4 u;
@@ -931,7 +983,7 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   if (e != cudaSuccess) return e;
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
-  attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, mdq, lse, dvec, dq32, dqkv, seq,
+  attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, mdq, lse, dvec, dqkv, seq,
                                                                           heads, nz, 1.0f / std::sqrt(float(kD)));
   note_launch();
   attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h,

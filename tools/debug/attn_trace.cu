@@ -31,12 +31,16 @@ int main() {
     unsigned int zero[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(g_trace_n, zero, sizeof(zero));
 #endif
-    attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
+    cudaError_t eb = attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
+    if (eb != cudaSuccess) printf("attention_bwd: %s\n", cudaGetErrorString(eb));
   }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int rep = 0; rep < 10; ++rep) attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
+  for (int rep = 0; rep < 10; ++rep) {
+    cudaError_t eb = attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
+    if (eb != cudaSuccess && rep == 0) printf("attention_bwd (timed): %s\n", cudaGetErrorString(eb));
+  }
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
