@@ -53,24 +53,29 @@ def _worker(rank, world, q_in, q_out, stage, plan, tokens, peer=True):
         q_out.put((rank, traceback.format_exc(), None, None, None, None, None, None, None, None, None))
 
 
-@pytest.mark.parametrize("stage,peer", [(0, True), (1, True), (1, False), (2, True), (2, False), (3, True), (3, False)])
-def test_two_rank_hetero_step_matches_oracle(stage, peer):
+def _run(stage, peer, world):
     import torch
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
     from oracle import step as so
-    if stage >= 2:
-        plan = _plan(stage, [dict(device_id=0, b=3, gmbs=5, lbs=2, predicted_time=0.0),
-                         dict(device_id=1, b=1, gmbs=2, lbs=1, predicted_time=0.0)], gas=2)
+    # unequal per-rank micro-batches; at stage 2/3 every rank runs `gas` micro-steps (a rank may
+    # sit out the last one with lbs = 0), at stage 0/1 ranks run their own step counts
+    if world == 2:
+        devs = ([dict(b=3, gmbs=5, lbs=2), dict(b=1, gmbs=2, lbs=1)] if stage >= 2 else
+                [dict(b=3, gmbs=5, lbs=2), dict(b=2, gmbs=2, lbs=2)])
     else:
-        plan = _plan(stage, [dict(device_id=0, b=3, gmbs=5, lbs=2, predicted_time=0.0),
-                             dict(device_id=1, b=2, gmbs=2, lbs=2, predicted_time=0.0)], gas=2)
+        devs = ([dict(b=3, gmbs=5, lbs=2), dict(b=1, gmbs=2, lbs=1), dict(b=2, gmbs=4, lbs=2),
+                 dict(b=1, gmbs=1, lbs=0)] if stage >= 2 else
+                [dict(b=3, gmbs=5, lbs=2), dict(b=2, gmbs=2, lbs=2), dict(b=1, gmbs=3, lbs=1),
+                 dict(b=4, gmbs=4, lbs=4)])
+    plan = _plan(stage, [dict(device_id=i, predicted_time=0.0, **d) for i, d in enumerate(devs)], gas=2)
     B = plan["gbs"]
     tokens = np.random.default_rng(3).integers(0, TINY["vocab"], (B, TINY["seq_len"] + 1)).astype(np.int32)
     ctx = mp.get_context("spawn")
     q_in, q_out = ctx.Queue(), ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, q_in, q_out, stage, plan, tokens, peer)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, q_in, q_out, stage, plan, tokens, peer))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q_out.get(timeout=300) for _ in procs], key=lambda r: r[0])
@@ -78,14 +83,22 @@ def test_two_rank_hetero_step_matches_oracle(stage, peer):
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), [r[1] for r in res]
     # summed gradient: full on every rank (Z0) or the ranks' owned slices (Z1-3)
+    masks = [r[2] for r in res]
     if stage == 0:
         g = res[0][4]
-        assert np.array_equal(res[0][4], res[1][4])
+        for r in res[1:]:
+            assert np.array_equal(r[4], g)
     else:
-        assert not np.any(res[0][2] & res[1][2])
-        g = np.where(res[0][2], res[0][4], res[1][4])
-    (m0a, k0a), (m0b, k0b) = res[0][5], res[1][5]
-    p16 = np.where(k0a, m0a, m0b)
+        cover = np.zeros_like(masks[0], dtype=np.int32)
+        for m in masks:
+            cover += m.astype(np.int32)
+        assert cover.max() <= 1  # owned slices are disjoint
+        g = np.zeros_like(res[0][4])
+        for r in res:
+            g = np.where(r[2], r[4], g)
+    p16 = np.zeros_like(res[0][5][0])
+    for r in res:
+        p16 = np.where(r[5][1], r[5][0], p16) if stage else r[5][0]
     # oracle on the union of the samples
     names = res[0][3]
     P = _unflat(p16, names)
@@ -94,18 +107,32 @@ def test_two_rank_hetero_step_matches_oracle(stage, peer):
     Gg = _unflat(g, names)
     worst = max((so.rel_err(Gg[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
     assert worst[0] < 2e-2, worst
-    assert abs(res[0][7] + res[1][7] - loss) <= 1e-2 * abs(loss)
+    assert abs(sum(r[7] for r in res) - loss) <= 1e-2 * abs(loss)
     # all ranks end the iteration with identical bf16 parameters (Z0-2, gathered)
     if stage < 3:
-        assert np.array_equal(res[0][6], res[1][6])
+        for r in res[1:]:
+            assert np.array_equal(r[6], res[0][6])
     # the fused optimizer: new master == one float64 AdamW step (t=1) on the summed gradient
-    m0 = np.where(k0a, m0a, m0b).astype(np.float64) if stage else m0a.astype(np.float64)
-    exp, _, _ = so.adamw(m0, 0.0, 0.0, g.astype(np.float64), 1, 1e-3, 0.9, 0.95, 1e-8, 0.0)
-    master = res[0][9] if stage == 0 else np.where(res[0][2], res[0][9], res[1][9])
+    exp, _, _ = so.adamw(p16.astype(np.float64), 0.0, 0.0, g.astype(np.float64), 1, 1e-3, 0.9, 0.95, 1e-8, 0.0)
+    master = res[0][9]
+    if stage:
+        master = np.zeros_like(res[0][9])
+        for r in res:
+            master = np.where(r[2], r[9], master)
     assert so.rel_err(master, exp) < 1e-6
     # the collective path that actually ran
     if stage >= 1:
-        assert res[0][10] == res[1][10] == peer
+        assert all(r[10] == peer for r in res)
+
+
+@pytest.mark.parametrize("stage,peer", [(0, True), (1, True), (1, False), (2, True), (2, False), (3, True), (3, False)])
+def test_two_rank_hetero_step_matches_oracle(stage, peer):
+    _run(stage, peer, 2)
+
+
+@pytest.mark.parametrize("stage,peer", [(0, True), (1, True), (2, True), (2, False), (3, True)])
+def test_four_rank_hetero_step_matches_oracle(stage, peer):
+    _run(stage, peer, 4)
 
 
 def _unflat(flat, layout):
