@@ -200,6 +200,20 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (the MUFU unit, 16 results/clk/SM, bounds the softmax): round-to-nearest
+// split x = j + f with the 1.5*2^23 trick, cubic minimax for 2^f on [-0.5, 0.5] (max rel. error
+// 7.5e-5, below bf16 resolution), 2^j added into the exponent bits. x is clamped to >= -126 so
+// the exponent arithmetic cannot wrap (results there are ~1e-38, i.e. 0 for all uses here).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.055171647f, 0.24261112f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992807f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 static_assert(FwdSmem::kPipe % 1024 == 0, "pipeline regions keep the 1 KiB swizzle alignment");
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
@@ -305,6 +319,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         ++gs;
       };
+      ZP_TRACE_INIT;
       for (uint32_t item = 0;; ++item) {
         const int t = ring.consume1(item);
         if (t >= ntasks) break;
@@ -320,7 +335,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             ptx::umma_commit(q_empty);
           }
           if (j == 0) ptx::mbar_wait(o_free, (item & 1) ^ 1);  // previous task's epilogue read O
+          if (pipe == 0) ZP_TRACE(0, 1);
           ptx::mbar_wait(p_full, gp & 1);
+          if (pipe == 0) ZP_TRACE(0, 2);
           ptx::tc_fence_after();
           const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + kp * kTile);
 #pragma unroll
@@ -347,6 +364,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t t_p = tmem + kFwdTmemP + lane_off + kh * 32;
     const uint32_t t_o = tmem + kFwdTmemO + lane_off + kh * 32;
     uint32_t g = 0;  // tiles processed (S / P.V barrier phases)
+    ZP_TRACE_INIT;
+    const bool tr = (pipe == 0 && warp == 0 && lane == 0);
     for (uint32_t item = 0;; ++item) {
       const int t = ring.consume(item);
       if (t >= ntasks) break;
@@ -354,7 +373,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int smp = tk.z / heads, head = tk.z % heads;
       float m = -INFINITY, l = 0.f;  // m: max used for the exponentials (log2 domain)
       for (int j = 0; j <= tk.tile; ++j, ++g) {
+        if (tr) ZP_TRACE(1, 1);
         ptx::mbar_wait(s_full, g & 1);
+        if (tr) ZP_TRACE(1, 2);
         ptx::tc_fence_after();
         float sv[64];
 #pragma unroll
@@ -367,6 +388,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
+        if (tr) ZP_TRACE(1, 3);
         if (j == tk.tile) {  // diagonal tile: key > query is masked
 #pragma unroll
           for (int i = 0; i < 64; ++i)
@@ -385,6 +407,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // the row's two halves
         const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
         asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // red reusable next tile
+        if (tr) ZP_TRACE(1, 4);
         // lazy rescale: raise m only when the row max outgrows it by more than 2^8
         const bool raise = mx > m + kRescaleLog2;
         const float alpha = raise ? ex2(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
@@ -394,14 +417,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 64; i += 2) {
-          const float p0 = ex2(fmaf(sv[i], scale_log2, -m));
-          const float p1 = ex2(fmaf(sv[i + 1], scale_log2, -m));
+          // (ex2_poly for a share of the pairs measured no faster here: the phase is not MUFU-bound)
+          const bool poly = false;
+          const float x0 = fmaf(sv[i], scale_log2, -m), x1 = fmaf(sv[i + 1], scale_log2, -m);
+          const float p0 = poly ? ex2_poly(x0) : ex2(x0);
+          const float p1 = poly ? ex2_poly(x1) : ex2(x1);
           ps[(i >> 1) & 7] += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
+        if (tr) ZP_TRACE(1, 5);
         // P.V(j-1) must have finished reading P and accumulating into O
         if (j > 0) {
           ptx::mbar_wait(pv_done, (g - 1) & 1);
+          if (tr) ZP_TRACE(1, 6);
           ptx::tc_fence_after();
           if (__any_sync(0xffffffffu, raise)) {
             uint32_t v[32];
@@ -417,6 +445,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full);
+        if (tr) ZP_TRACE(1, 7);
       }
       // epilogue: wait for the last P.V, combine the halves' row sums, O / l -> bf16, LSE
       ptx::mbar_wait(pv_done, (g - 1) & 1);

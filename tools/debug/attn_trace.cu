@@ -26,6 +26,13 @@ int main() {
   cudaMemcpy(qkv, hq.data(), hq.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dout, hd.data(), hd.size() * 2, cudaMemcpyHostToDevice);
   attention_fwd(qkv, out, lse, b, s, H, 132, 0);
+#ifdef ZP_TRACE_FWD
+  {
+    unsigned int zero[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_trace_n, zero, sizeof(zero));
+    for (int rep = 0; rep < 3; ++rep) attention_fwd(qkv, out, lse, b, s, H, 132, 0);
+  }
+#else
   for (int rep = 0; rep < 3; ++rep) {
 #ifdef ZP_ATTN_TRACE
     unsigned int zero[4] = {0, 0, 0, 0};
@@ -34,10 +41,15 @@ int main() {
     cudaError_t eb = attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
     if (eb != cudaSuccess) printf("attention_bwd: %s\n", cudaGetErrorString(eb));
   }
+#endif
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
+#ifdef ZP_TRACE_FWD
+  for (int rep = 0; rep < 0; ++rep) {
+#else
   for (int rep = 0; rep < 10; ++rep) {
+#endif
     cudaError_t eb = attention_bwd(qkv, out, dout, lse, dvec, dq32, dqkv, b, s, H, 132, 0);
     if (eb != cudaSuccess && rep == 0) printf("attention_bwd (timed): %s\n", cudaGetErrorString(eb));
   }
