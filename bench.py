@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--gbs", type=int, default=0, help="override global batch (samples)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-recalibrate", action="store_true",
+                    help="plan from the Alg. 1 profile only (no measured-iteration correction)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -248,6 +250,16 @@ def main():
     uniform = poplar.poplar_plan(rt, profile, gbs, stage, world, uniform=True)
     first, count = poplar.rank_slice(plan, rank)
     rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
+    plan_initial = plan
+    if world > 1 and not args.no_recalibrate:
+        # one measured iteration corrects every rank's curve for the power-capped steady state,
+        # then the same planner re-plans (poplar.recalibrate)
+        rt.execute_iteration(plan, stage)
+        t_cal = rt.execute_iteration(plan, stage)
+        profile = poplar.recalibrate(profile, plan, allgather({"compute": t_cal["compute"]}))
+        plan = poplar.poplar_plan(rt, profile, gbs, stage, world)
+        first, count = poplar.rank_slice(plan, rank)
+        rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
 
     def timed(k, plan_d, host_tokens=None):
         from paper_2408_12596_b200.host import plan_from_py
@@ -352,6 +364,10 @@ def main():
                        "sm_budgets": [cfg["tiers"][r % len(cfg["tiers"])] for r in range(world)],
                        "plan": {"b": [d["b"] for d in plan["devices"]], "lbs": [d["lbs"] for d in plan["devices"]],
                                 "gmbs": [d["gmbs"] for d in plan["devices"]], "gas": plan["gas"]},
+                       "plan_alg1_only": {"b": [d["b"] for d in plan_initial["devices"]],
+                                          "gmbs": [d["gmbs"] for d in plan_initial["devices"]],
+                                          "gas": plan_initial["gas"]},
+                       "recalibrated": plan is not plan_initial,
                        "mbs": [d["mbs"] for d in profile["devices"]],
                        "profile_seconds": t_profile, "parallelism": f"zero{stage}-dp{world}",
                        "collectives": (("nvlink-peer (pull RS/AG; fused RS+AdamW+AG at sync)" if stage in (1, 2) else "nvlink-peer (pull RS/AG)" if stage == 3 else "nccl (all-reduce)") if rt.peer_collectives() else "nccl") if world > 1 else "none",

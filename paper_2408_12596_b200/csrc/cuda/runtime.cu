@@ -1082,7 +1082,7 @@ struct Runtime {
   }
 
   // ---------------------------------------------------------------- lockstep profiler (Alg. 1)
-  static constexpr double kSettleSeconds = 0.25;  // per-probe device time before the kept sample
+  static constexpr double kSettleSeconds = 0.6;  // per-probe device time before the kept sample
   static constexpr int64_t kSettleMaxReps = 24;
   int* dscratch = nullptr;  // small device buffer for rank-agreement collectives
   int64_t agree(int64_t v, ncclRedOp_t op) {

@@ -1,0 +1,33 @@
+"""poplar.recalibrate: every rank's profile samples are rescaled by measured / predicted compute of
+one planned iteration; the planner itself is unchanged (CPU, no GPU needed)."""
+import pytest
+
+from paper_2408_12596_b200 import poplar
+
+
+def _profile():
+    return {"effective_stage": 2, "n": 2, "devices": [
+        {"device_id": 0, "mbs": 64, "probes_used": 5, "optimizer_time": 0.01,
+         "samples": [(1, 0.010), (2, 0.018), (4, 0.034), (8, 0.066)]},
+        {"device_id": 1, "mbs": 64, "probes_used": 5, "optimizer_time": 0.02,
+         "samples": [(1, 0.020), (2, 0.036), (4, 0.068), (8, 0.132)]}]}
+
+
+def test_recalibrate_scales_each_rank():
+    prof = _profile()
+    plan = {"stage": 2, "gas": 2, "devices": [{"predicted_time": 0.100}, {"predicted_time": 0.200}]}
+    out = poplar.recalibrate(prof, plan, [{"compute": 0.110}, {"compute": 0.200}])
+    r = 0.110 / 0.100
+    assert out["devices"][0]["samples"] == [(b, t * r) for b, t in prof["devices"][0]["samples"]]
+    assert out["devices"][1]["samples"] == prof["devices"][1]["samples"]
+    assert out["devices"][0]["mbs"] == 64 and out["devices"][0]["optimizer_time"] == 0.01
+    # the input profile is not modified
+    assert prof["devices"][0]["samples"][0] == (1, 0.010)
+
+
+def test_recalibrate_keeps_idle_rank():
+    prof = _profile()
+    plan = {"stage": 2, "gas": 1, "devices": [{"predicted_time": 0.0}, {"predicted_time": 0.2}]}
+    out = poplar.recalibrate(prof, plan, [{"compute": 0.0}, {"compute": 0.1}])
+    assert out["devices"][0]["samples"] == prof["devices"][0]["samples"]
+    assert out["devices"][1]["samples"][3][1] == pytest.approx(0.066)
