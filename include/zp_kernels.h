@@ -22,7 +22,7 @@ extern "C" {
 /* GEMM: C[z][m,n] = epilogue(alpha * sum_k A[z][m,k] * B[z][n,k]), bf16 in, fp32 accumulate.
  * major: 0 = K-major (elem (r,k) at ptr[r*ld+k]), 1 = MN-major (elem (r,k) at ptr[k*ld+r]).
  * epilogue: 0 store bf16, 1 store f32, 2 accumulate f32, 3 +bias bf16, 4 +bias+residual bf16,
- *           5 +bias then GELU (pre-activation to aux_out) bf16, 6 times GELU'(aux) bf16,
+ *           5 +bias then GELU bf16 (GELU'(pre-activation) to aux_out), 6 times aux (= GELU') bf16,
  *           7 fp32 atomic add (split-K partial sums).
  * causal:   0 none, 1 skip tiles above the diagonal, 2 k <= tile last row, 3 k >= tile first row.
  */

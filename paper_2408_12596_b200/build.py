@@ -26,10 +26,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # (g++ -O2, no FMA contraction, no fast-math).
 HOST_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
               "-Wno-unused-parameter"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ARCH + os.environ.get("ZP_EXTRA_NVCC", "").split() + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
                      "-Xptxas", "-v"] if os.environ.get("ZP_PTXAS_V") else \
-    ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
+    ARCH + os.environ.get("ZP_EXTRA_NVCC", "").split() + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
             "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr"]
 INCLUDES = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(CSRC, "host")]
 

@@ -106,11 +106,26 @@ struct EpiParams {
 // GELU (tanh form) with the MUFU tanh approximation (rel. error ~2^-11, below bf16 output
 // rounding).
 __device__ __forceinline__ float gelu_tanh(float x) {
+#ifdef ZP_GEMM_CHEAP_GELU  // timing experiment only (wrong values)
+  return 0.5f * x;
+#endif
   // 0.5 x (1 + tanh(k0 (x + k1 x^3))): 3 FMUL + 2 FFMA + 1 MUFU
   constexpr float k0 = 0.7978845608028654f, k0k1 = 0.7978845608028654f * 0.044715f;
   const float t = ptx::tanh_approx(x * fmaf(k0k1, x * x, k0));
   const float hx = 0.5f * x;
   return fmaf(hx, t, hx);
+}
+
+// GELU and its derivative from one tanh: the forward epilogue stores gelu'(u) for the backward,
+// whose epilogue then only multiplies (no tanh, no pre-activation reload).
+__device__ __forceinline__ void gelu_tanh_and_grad(float x, float& y, float& dy) {
+  constexpr float k0 = 0.7978845608028654f, k0k1 = 0.7978845608028654f * 0.044715f;
+  const float x2 = x * x;
+  const float t = ptx::tanh_approx(x * fmaf(k0k1, x2, k0));
+  const float hx = 0.5f * x;
+  y = fmaf(hx, t, hx);
+  const float hd = x * fmaf(1.5f * k0k1, x2, 0.5f * k0);
+  dy = fmaf(hd, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
@@ -168,6 +183,10 @@ __device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32
         _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] += __bfloat162float(ep.aux[off + i]);
       }
     } else if (e == kEpiBiasGeluBf16) {
+      // C = gelu(u), aux_out = gelu'(u)
+      float d[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) gelu_tanh_and_grad(v[i], v[i], d[i]);
       __nv_bfloat16* u = ep.aux_out + off;
       if (full) {
 #pragma unroll
@@ -175,14 +194,12 @@ __device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32
           uint4 o;
           __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(v[i + 2 * j], v[i + 2 * j + 1]);
+          for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(d[i + 2 * j], d[i + 2 * j + 1]);
           *reinterpret_cast<uint4*>(u + i) = o;
         }
       } else if (valid) {
-        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) u[i] = __float2bfloat16_rn(v[i]);
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) u[i] = __float2bfloat16_rn(d[i]);
       }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
     }
   } else if (e == kEpiGeluBwdBf16) {
     if (full) {
@@ -193,12 +210,12 @@ __device__ __forceinline__ void epi_bf16_math(const EpiParams& ep, float (&v)[32
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 uf = __bfloat1622float2(u2[j]);
-          v[i + 2 * j] *= gelu_tanh_grad(uf.x);
-          v[i + 2 * j + 1] *= gelu_tanh_grad(uf.y);
+          v[i + 2 * j] *= uf.x;  // aux = gelu'(u) stored by the forward epilogue
+          v[i + 2 * j + 1] *= uf.y;
         }
       }
     } else if (valid) {
-      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] *= gelu_tanh_grad(__bfloat162float(ep.aux[off + i]));
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (n + i < N) v[i] *= __bfloat162float(ep.aux[off + i]);
     }
   }
 }
@@ -512,9 +529,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 const float a0 = __uint_as_float(p[k] << 16), a1 = __uint_as_float(p[k] & 0xffff0000u);
-                if (ep.epilogue == kEpiGeluBwdBf16) {
-                  w[2 * k] *= gelu_tanh_grad(a0);
-                  w[2 * k + 1] *= gelu_tanh_grad(a1);
+                if (ep.epilogue == kEpiGeluBwdBf16) {  // aux = gelu'(u)
+                  w[2 * k] *= a0;
+                  w[2 * k + 1] *= a1;
                 } else {  // residual
                   w[2 * k] += a0;
                   w[2 * k + 1] += a1;
@@ -527,13 +544,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int g = 0; g < 2; ++g) epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
             }
           } else if (ep.epilogue == kEpiBiasGeluBf16 && ep.aux_out_tma) {
-            // U = pre-activation (bias added) -> staging box -> TMA store; then GELU
+            // C = gelu(u); gelu'(u) -> staging box -> TMA store into aux_out
+            float d[2][32];
 #pragma unroll
-            for (int g = 0; g < 2; ++g) epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
+            for (int g = 0; g < 2; ++g) {
+              epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) gelu_tanh_and_grad(v[g][i], v[g][i], d[g][i]);
+            }
             if (lane == 0) ptx::bulk_wait_read<1>();
             __syncwarp();
             uint8_t* sb = stage_buf + buf * kStageBufBytes;
-            stage_row_bf16(sb, lane, v);
+            stage_row_bf16(sb, lane, d);
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -541,10 +563,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::bulk_commit();
             }
             buf ^= 1;
-#pragma unroll
-            for (int g = 0; g < 2; ++g)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[g][i] = gelu_tanh(v[g][i]);
           } else {
 #pragma unroll
             for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + n0 + 32 * g, n0 + 32 * g, sched.N, valid);

@@ -23,8 +23,8 @@ enum GemmEpilogue : int {
   kEpiAccumF32 = 2,       // C(f32) += alpha*acc
   kEpiBiasBf16 = 3,       // C(bf16) = acc + bias[n]
   kEpiBiasResidBf16 = 4,  // C(bf16) = acc + bias[n] + R[m, n]   (R may alias C)
-  kEpiBiasGeluBf16 = 5,   // U(bf16) = acc + bias[n];  C(bf16) = gelu(U)
-  kEpiGeluBwdBf16 = 6,    // C(bf16) = acc * gelu'(U[m, n])
+  kEpiBiasGeluBf16 = 5,   // u = acc + bias[n]; C(bf16) = gelu(u), aux_out(bf16) = gelu'(u)
+  kEpiGeluBwdBf16 = 6,    // C(bf16) = acc * aux[m, n]   (aux = gelu'(u) from the forward)
   kEpiAtomicF32 = 7,      // C(f32) += alpha*acc with fp32 vector atomics (split-K partials)
 };
 
@@ -53,7 +53,7 @@ struct GemmArgs {
   int causal = kCausalNone;
   const void* bias = nullptr;  // bf16 [N]; may be null (no bias)
   const void* aux = nullptr;   // bf16, same layout as C (residual R or pre-activation U)
-  void* aux_out = nullptr;     // bf16, same layout as C (U written by kEpiBiasGeluBf16)
+  void* aux_out = nullptr;     // bf16, same layout as C (gelu'(u) written by kEpiBiasGeluBf16)
   int max_ctas = 0;            // SM budget cap (0 = all SMs)
   int split_k = 1;             // >1: K range split across CTAs; -1: auto; requires kEpiAtomicF32
 };

@@ -189,6 +189,8 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
 
 // ------------------------------------------------------------------ activations of one micro-step
 struct LayerActs {
+  // u: GPT-2 GELU'(fc pre-activation) saved by the fc GEMM epilogue for the backward;
+  //    Llama gate/up projection (interleaved) for SwiGLU. g: MLP activation.
   bf16 *x_in, *ln1, *qkv, *attn, *x_mid, *ln2, *u, *g;
   float *mu1, *rs1, *mu2, *rs2, *lse;
 };

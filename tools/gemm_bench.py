@@ -35,6 +35,7 @@ def main():
     torch.manual_seed(0)
     # name, M, N, K, a_major, b_major, epilogue
     shapes = [("fwd qkv", T, 3 * h, h, 0, 0, 0), ("fwd fc", T, f, h, 0, 0, 0), ("fwd proj", T, h, f, 0, 0, 0),
+              ("fwd fc +bias", T, f, h, 0, 0, 3),
               ("fwd fc +bias+GELU(+U)", T, f, h, 0, 0, 5), ("fwd proj +bias+resid", T, h, f, 0, 0, 4),
               ("dgrad fc +GELU'", T, f, h, 0, 1, 6),
               ("lm head", T, V, h, 0, 0, 0), ("dgrad proj", T, f, h, 0, 1, 0), ("dgrad fc", T, h, f, 0, 1, 0),
@@ -51,6 +52,8 @@ def main():
         fl = 2.0 * M * N * K
         res = []
         extra = {}
+        if epi == 3:
+            extra["bias"] = (torch.randn(N, device=dev) * 0.1).to(torch.bfloat16)
         if epi in (4, 5, 6):
             extra["bias"] = (torch.randn(N, device=dev) * 0.1).to(torch.bfloat16) if epi in (4, 5) else None
             aux = (torch.randn(M * N, device=dev) * 0.1).to(torch.bfloat16)
