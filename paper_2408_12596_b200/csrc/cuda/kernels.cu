@@ -658,26 +658,47 @@ __global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, floa
 
 // ------------------------------------------------------------------ RoPE (rotate-half, head_dim 64)
 
+// cos / sin of pos * theta^(-2j/64) for pos < seq, j < 32 (computed once per (seq, theta) in
+// double precision, kept in a small per-process table).
+__global__ void rope_table_k(float2* tab, int seq, double log_theta) {
+  const int n = seq * 32;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int pos = i / 32, j = i % 32;
+    const double ang = double(pos) * exp(-double(2 * j) / 64.0 * log_theta);
+    tab[i] = make_float2(float(cos(ang)), float(sin(ang)));
+  }
+}
+
 // In place on the Q and K column blocks of qkv [T, 3h]; inverse = rotation by -theta (backward).
-__global__ void rope_k(bf16* qkv, int64_t tokens, int seq, int h, float theta, float sign) {
-  const int pairs = h / 2;  // per Q or K block: heads * 32 pairs
-  const int64_t total = tokens * 2 * pairs;
+// One thread per (token, Q|K, head, group of 8 rotation pairs): two 16-byte loads / stores.
+__global__ void rope_k(bf16* qkv, const float2* __restrict__ tab, int64_t tokens, int seq, int h, float sign) {
+  const int heads = h / 64;
+  const int per_tok = 2 * heads * 4;
+  const int64_t total = tokens * per_tok;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = i / (2 * pairs);
-    const int r = int(i % (2 * pairs));
-    const int blk = r / pairs;          // 0 = Q, 1 = K
-    const int p = r % pairs;
-    const int head = p / 32, j = p % 32;
+    const int64_t t = i / per_tok;
+    const int r = int(i - t * per_tok);
+    const int blk = r / (heads * 4), rem = r - blk * (heads * 4);
+    const int head = rem >> 2, j0 = (rem & 3) * 8;
     const int pos = int(t % seq);
-    const float inv_freq = exp2f(-float(2 * j) / 64.0f * log2f(theta));
-    float sn, cs;
-    sincosf(float(pos) * inv_freq, &sn, &cs);
-    sn *= sign;
-    bf16* v = qkv + t * 3 * h + blk * h + head * 64;
-    const float a = __bfloat162float(v[j]), b = __bfloat162float(v[j + 32]);
-    v[j] = __float2bfloat16_rn(a * cs - b * sn);
-    v[j + 32] = __float2bfloat16_rn(b * cs + a * sn);
+    bf16* v = qkv + t * 3 * h + blk * h + head * 64 + j0;
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(v), a);
+    unpack8(*reinterpret_cast<const uint4*>(v + 32), b);
+    const float4* cs4 = reinterpret_cast<const float4*>(tab + pos * 32 + j0);
+    float o0[8], o1[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 w = cs4[k];  // (cos, sin) of pairs 2k and 2k+1
+      const float c0 = w.x, s0 = sign * w.y, c1 = w.z, s1 = sign * w.w;
+      o0[2 * k] = a[2 * k] * c0 - b[2 * k] * s0;
+      o1[2 * k] = b[2 * k] * c0 + a[2 * k] * s0;
+      o0[2 * k + 1] = a[2 * k + 1] * c1 - b[2 * k + 1] * s1;
+      o1[2 * k + 1] = b[2 * k + 1] * c1 + a[2 * k + 1] * s1;
+    }
+    *reinterpret_cast<uint4*>(v) = pack8(o0);
+    *reinterpret_cast<uint4*>(v + 32) = pack8(o1);
   }
 }
 
@@ -752,8 +773,22 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
                                                                           rows, h); note_launch();
 }
 void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s) {
-  rope_k<<<grid_for(tokens * h, kThreads, ctas), kThreads, 0, s>>>(qkv, tokens, seq, h, theta,
-                                                                  inverse ? -1.f : 1.f); note_launch();
+  // per-process cos/sin table for the largest sequence seen (one process drives one GPU)
+  static float2* tab = nullptr;
+  static int tab_seq = 0;
+  static float tab_theta = 0.f;
+  if (seq > tab_seq || theta != tab_theta) {
+    if (tab) cudaFree(tab);
+    tab = nullptr;
+    if (cudaMalloc(&tab, size_t(seq) * 32 * sizeof(float2)) != cudaSuccess) return;
+    rope_table_k<<<(seq * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(tab, seq, std::log(double(theta)));
+    note_launch();
+    tab_seq = seq;
+    tab_theta = theta;
+  }
+  rope_k<<<grid_for(tokens * 2 * (h / 64) * 4, kThreads, ctas), kThreads, 0, s>>>(qkv, tab, tokens, seq, h,
+                                                                                  inverse ? -1.f : 1.f);
+  note_launch();
 }
 void swiglu_fwd(const bf16* gu, bf16* out, int64_t tokens, int f, int ctas, cudaStream_t s) {
   swiglu_fwd_k<<<grid_for(tokens * f / 8, kThreads, ctas), kThreads, 0, s>>>(gu, out, tokens, f); note_launch();
