@@ -900,16 +900,19 @@ __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __rest
 // dqkv[:, 0:h] (bf16, row stride 3h) = dq32 [T, h]
 __global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __restrict__ dqkv, int64_t tokens, int h,
                                     float scale) {
-  const int64_t n4 = tokens * h / 4;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e = i * 4;
-    const int64_t tok = e / h;
-    const int col = int(e % h);
-    const float4 v = reinterpret_cast<const float4*>(dq32)[i];
-    uint2 o;
-    o.x = pack_bf16(v.x * scale, v.y * scale);  // dQ = scale * dS' K
-    o.y = pack_bf16(v.z * scale, v.w * scale);
-    *reinterpret_cast<uint2*>(dqkv + tok * 3 * h + col) = o;
+  // 8 elements per item: two 16-byte loads, one 16-byte store
+  const int per_row = h / 8;
+  const int64_t n8 = tokens * per_row;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t tok = i / per_row;
+    const int col = int(i - tok * per_row) * 8;
+    const float4 a = reinterpret_cast<const float4*>(dq32)[2 * i], b = reinterpret_cast<const float4*>(dq32)[2 * i + 1];
+    uint4 o;
+    o.x = pack_bf16(a.x * scale, a.y * scale);  // dQ = scale * dS' K
+    o.y = pack_bf16(a.z * scale, a.w * scale);
+    o.z = pack_bf16(b.x * scale, b.y * scale);
+    o.w = pack_bf16(b.z * scale, b.w * scale);
+    *reinterpret_cast<uint4*>(dqkv + tok * 3 * h + col) = o;
   }
 }
 
@@ -1015,7 +1018,7 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   attn_bwd_kernel<<<std::min(ntasks, cap), kBwdThreads, BwdSmem::kBytes, s>>>(mq, md, mdq, lse, dvec, dqkv, seq,
                                                                           heads, nz, 1.0f / std::sqrt(float(kD)));
   note_launch();
-  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 4 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h,
+  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h,
                                                                                        1.0f / std::sqrt(float(kD)));
   note_launch();
   return cudaGetLastError();

@@ -17,6 +17,14 @@ __global__ void k(float* out, int iters) {
     } else if (MODE == 2) {
       asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h0)); asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h1));
       asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h2)); asm volatile("tanh.approx.bf16x2 %0, %0;" : "+r"(h3));
+    } else if (MODE == 4) {
+      // cvt.rn.bf16x2.f32 (F2FP pack), dependent through the float inputs
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h0) : "f"(x0), "f"(x1));
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h1) : "f"(x1), "f"(x2));
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h2) : "f"(x2), "f"(x3));
+      asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h3) : "f"(x3), "f"(x0));
+      x0 = __uint_as_float(h0 ^ 0x3f800000u); x1 = __uint_as_float(h1 ^ 0x3f800000u);
+      x2 = __uint_as_float(h2 ^ 0x3f800000u); x3 = __uint_as_float(h3 ^ 0x3f800000u);
     } else {
       asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x0)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x1));
       asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x2)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x3));
@@ -29,13 +37,14 @@ __global__ void k(float* out, int iters) {
 int main() {
   float* d; cudaMalloc(&d, 64);
   const int iters = 4096, threads = 1024;
-  const char* n[4] = {"tanh.f32", "ex2.f32", "tanh.bf16x2", "rcp.f32"};
-  for (int m = 0; m < 4; ++m) {
+  const char* n[5] = {"tanh.f32", "ex2.f32", "tanh.bf16x2", "rcp.f32", "cvt.bf16x2 (+4 LOP)"};
+  for (int m = 0; m < 5; ++m) {
     for (int r = 0; r < 2; ++r) {
       if (m == 0) k<0><<<148, threads>>>(d, iters);
       if (m == 1) k<1><<<148, threads>>>(d, iters);
       if (m == 2) k<2><<<148, threads>>>(d, iters);
       if (m == 3) k<3><<<148, threads>>>(d, iters);
+      if (m == 4) k<4><<<148, threads>>>(d, iters);
     }
     cudaDeviceSynchronize();
     float c; cudaMemcpy(&c, d + m, 4, cudaMemcpyDeviceToHost);
