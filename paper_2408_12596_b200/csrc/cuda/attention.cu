@@ -494,13 +494,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // as an MN-major operand. Four warps read dQ out of TMEM and add it into the fp32 dQ with TMA
 // bulk reduce-add; after a task's last tile they write dK (scaled) and dV.
 // Warp roles: 0-7 builders (TMEM lane quarter w % 4, query half w / 4), 8-11 dQ / dK dV out,
-// 12 TMA producer, 13 MMA issuer. K/V are double-buffered so the next task's key tile loads
+// 12 TMA producer, 13 score MMA issuer (S^T, dP^T), 14 gradient MMA issuer (dK, dV, dQ): the two
+// issuers never block each other, so the next tile's scores are issued while this tile's
+// gradient products wait for the builders. K/V are double-buffered so the next task's key tile loads
 // while this one runs.
-constexpr int kBwdThreads = 448;
+constexpr int kBwdThreads = 480;
 constexpr int kBwdQD = 3;  // Q/dO (+LSE, D) stages
 constexpr int kBwdKV = 2;  // K/V stages
-// TMEM columns: S^T, dP^T (-> dS'^T packed), dV, dK, dQ, P^T packed
-constexpr int kBwdTS = 0, kBwdTDP = 128, kBwdTDV = 256, kBwdTDK = 320, kBwdTDQ = 384, kBwdTP = 448;
+// TMEM columns: S^T, dP^T, dS'^T packed (then dQ of the same tile, after dK has read dS'^T),
+// P^T packed, dV, dK. S^T and dP^T of the next tile are issued as soon as the builders have read
+// this one; the builders store P^T once dV of the previous tile is done and dS'^T (the last thing
+// they write) once the previous dQ has been read out.
+constexpr int kBwdTS = 0, kBwdTDP = 128, kBwdTDS = 256, kBwdTDQ = 256, kBwdTP = 320, kBwdTDV = 384,
+              kBwdTDK = 448;
 
 struct BwdSmem {
   static constexpr int kK = 0;                        // kBwdKV stages
@@ -531,13 +537,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* s_free = s_full + 1;                   // S^T read by the builders
   uint64_t* dp_full = s_full + 2;                  // dP^T in TMEM
   uint64_t* pt_full = s_full + 3;                  // P^T, dS'^T in TMEM
-  uint64_t* dk_done = s_full + 4;                  // dK product done: dS'^T TMEM (dP^T columns) reusable
-  uint64_t* mm_done = s_full + 5;                  // dQ product done: dQ in TMEM, dS' smem free
+  uint64_t* dp_free = s_full + 4;                  // dP^T read by the builders
+  uint64_t* mm_done = s_full + 5;                  // dQ product done: dQ in TMEM (dS'^T columns), dS' smem free
   uint64_t* acc_free = s_full + 6;                 // dK/dV read out by the epilogue
   uint64_t* dq_free = s_full + 7;                  // dQ read out of TMEM
-  uint64_t* dv_done = s_full + 8;                  // dV product done: P^T TMEM reusable
+  uint64_t* dv_done = s_full + 8;                  // dV product done: P^T TMEM read
+  uint64_t* dk_done = s_full + 10;                 // dK product done: dS'^T TMEM read
   uint64_t* ds_full = s_full + 9;                  // dS'^T in shared memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 10);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 11);
 
   const int warp = int(ptx::warp_id());
   const int lane = threadIdx.x & 31;
@@ -562,6 +569,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::mbar_init(dp_full, 1);
     ptx::mbar_init(pt_full, 256);
     ptx::mbar_init(ds_full, 256);
+    ptx::mbar_init(dp_free, 256);
     ptx::mbar_init(dk_done, 1);
     ptx::mbar_init(dv_done, 1);
     ptx::mbar_init(mm_done, 1);
@@ -608,94 +616,74 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 13) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T
-      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 0, 1);    // dV, dK: A in TMEM, B MN-major
-      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 1, 1);    // dQ: A = dS' (MN-major), B = K
-      ZP_TRACE_INIT;
-      const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
-      int ss = 0;  // Q/dO stage of the tile whose products are issued next
+    if (lane == 0) {  // ------------------------------------------ score MMA issuer: S^T, dP^T
+      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      int ss = 0;
       uint32_t ss_ph = 0, item = 0, it = 0;
-      // S^T / dP^T of the tile in Q/dO stage st
-      auto issue_s = [&](uint32_t sk, int st) {
-        const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + st * kTile);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTS, kdesc(sk, k), kdesc(sq, k), id_ss, k > 0);
-        ptx::umma_commit(s_full);
-      };
-      auto issue_dp = [&](uint32_t sv, int st) {
-        const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + st * kTile);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTDP, kdesc(sv, k), kdesc(sdo, k), id_ss, k > 0);
-        ptx::umma_commit(dp_full);
-      };
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
         const AttnTask tk = bwd_task_static(t, nz);
         const int kvs = item % kBwdKV;
         ptx::mbar_wait(&kv_full[kvs], (item / kBwdKV) & 1);
         const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK + kvs * kTile);
         const uint32_t sv = ptx::smem_u32(sm + BwdSmem::kV + kvs * kTile);
-        // prologue: S^T / dP^T of the task's first tile
-        ptx::mbar_wait(&qd_full[ss], ss_ph);
-        ptx::mbar_wait(s_free, (it & 1) ^ 1);   // builders read the previous S^T
-        ptx::tc_fence_after();
-        issue_s(sk, ss);
-        ptx::mbar_wait(dk_done, (it & 1) ^ 1);  // previous dK read dS'^T out of the dP^T columns
-        ptx::tc_fence_after();
-        issue_dp(sv, ss);
-        int nx = ss + 1 == kBwdQD ? 0 : ss + 1;  // stage of the next tile
-        uint32_t nx_ph = ss + 1 == kBwdQD ? (ss_ph ^ 1) : ss_ph;
         for (int i = tk.tile; i < nt; ++i, ++it) {
-          const bool more = i + 1 < nt;
+          ptx::mbar_wait(&qd_full[ss], ss_ph);
           const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
           const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
-          ZP_TRACE(0, 1);
-          if (more) {  // S^T(i+1) as soon as the builders have read S^T(i)
-            ptx::mbar_wait(&qd_full[nx], nx_ph);
-            ZP_TRACE(0, 2);
-            ptx::mbar_wait(s_free, it & 1);
-            ZP_TRACE(0, 3);
-            ptx::tc_fence_after();
-            issue_s(sk, nx);
+          ptx::mbar_wait(s_free, (it & 1) ^ 1);  // builders read the previous S^T
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTS, kdesc(sk, k), kdesc(sq, k), id_ss, k > 0);
+          ptx::umma_commit(s_full);
+          ptx::mbar_wait(dp_free, (it & 1) ^ 1);  // builders read the previous dP^T
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ptx::umma_bf16(tmem + kBwdTDP, kdesc(sv, k), kdesc(sdo, k), id_ss, k > 0);
+          ptx::umma_commit(dp_full);
+          if (++ss == kBwdQD) {
+            ss = 0;
+            ss_ph ^= 1;
           }
+        }
+      }
+    }
+  } else if (warp == 14) {
+    if (lane == 0) {  // --------------------------------------- gradient MMA issuer: dK, dV, dQ
+      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 64, 0, 1);  // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 64, 1, 1);  // dQ: A = dS' (MN-major), B = K
+      const uint32_t sds = ptx::smem_u32(sm + BwdSmem::kDS);
+      int ss = 0;
+      uint32_t item = 0, it = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = bwd_task_static(t, nz);
+        const int kvs = item % kBwdKV;
+        ptx::mbar_wait(&kv_full[kvs], (item / kBwdKV) & 1);
+        const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK + kvs * kTile);
+        for (int i = tk.tile; i < nt; ++i, ++it) {
+          const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + ss * kTile);
+          const uint32_t sdo = ptx::smem_u32(sm + BwdSmem::kDO + ss * kTile);
           const bool first = (i == tk.tile);
           if (first) ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // previous task's dK/dV read out
-          ZP_TRACE(0, 4);
           ptx::mbar_wait(pt_full, it & 1);
-          ZP_TRACE(0, 5);
           ptx::tc_fence_after();
-          // dK first: its dS'^T operand sits in the dP^T columns, which dP^T(i+1) reuses
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            ptx::umma_bf16_ts(tmem + kBwdTDK, tmem + kBwdTDP + 8 * k, mndesc(sq, k), id_t, (!first || k > 0));
+            ptx::umma_bf16_ts(tmem + kBwdTDK, tmem + kBwdTDS + 8 * k, mndesc(sq, k), id_t, (!first || k > 0));
           ptx::umma_commit(dk_done);
-          if (more) {  // dP^T(i+1) overwrites dS'^T(i): after dK(i) has read it
-            ZP_TRACE(0, 6);
-            ptx::mbar_wait(dk_done, it & 1);
-            ZP_TRACE(0, 7);
-            ptx::tc_fence_after();
-            issue_dp(sv, nx);
-          }
-          // dV while the builders already work on tile i+1 (they wait for it before writing P^T)
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             ptx::umma_bf16_ts(tmem + kBwdTDV, tmem + kBwdTP + 8 * k, mndesc(sdo, k), id_t, (!first || k > 0));
           ptx::umma_commit(dv_done);
-          ZP_TRACE(0, 8);
-          ptx::mbar_wait(ds_full, it & 1);         // dS'^T in shared memory
-          ptx::mbar_wait(dq_free, (it & 1) ^ 1);  // dQ of the previous tile has been read out
+          // dQ lands in the dS'^T columns: after dK has read dS'^T
+          ptx::mbar_wait(dk_done, it & 1);
+          ptx::mbar_wait(ds_full, it & 1);  // dS'^T in shared memory
           ptx::tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kBwdTDQ, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
           ptx::umma_commit(mm_done);
-          ptx::umma_commit(&qd_empty[ss]);
+          ptx::umma_commit(&qd_empty[ss]);  // the stage's S^T / dP^T products finished before pt_full
           if (i == nt - 1) ptx::umma_commit(&kv_empty[kvs]);
-          ss = nx;
-          ss_ph = nx_ph;
-          if (++nx == kBwdQD) {
-            nx = 0;
-            nx_ph ^= 1;
-          }
+          if (++ss == kBwdQD) ss = 0;
         }
       }
     }
@@ -732,7 +720,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           ptx::tmem_ld_wait();
           if (c == 1) {
             ptx::tc_fence_before();
-            ptx::mbar_arrive(s_free);  // S^T fully read: the MMA warp may issue the next one
+            ptx::mbar_arrive(s_free);   // S^T and dP^T fully read: the MMA warp may issue the
+            ptx::mbar_arrive(dp_free);  // next tile's products into these columns
           }
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
@@ -766,9 +755,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           ptx::tmem_st_32x32b_x16(tmem + kBwdTP + lane_off + kh * 32 + c * 16, pk);
         }
         if (warp == 0 && lane == 0) ZP_TRACE(1, 4);
-        // both column halves of these rows have read dP^T before either overwrites it
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
-        ptx::tmem_st_32x32b_x32(tmem + kBwdTDP + lane_off + kh * 32, dk);
+        // the dS'^T columns held dQ of the previous tile: read out by the dQ warps
+        ptx::mbar_wait(dq_free, (it & 1) ^ 1);
+        ptx::tc_fence_after();
+        ptx::tmem_st_32x32b_x32(tmem + kBwdTDS + lane_off + kh * 32, dk);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(pt_full);  // dK / dV may start
@@ -787,7 +777,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     }
-  } else {  // --------------------------------------------------------- warps 8-11: dQ + dK/dV out
+  } else if (warp < 12) {  // ------------------------------------------ warps 8-11: dQ + dK/dV out
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
@@ -797,7 +787,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const AttnTask tk = bwd_task_static(t, nz);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        ptx::mbar_wait_sleep(mm_done, it & 1, 1000);
+        ptx::mbar_wait(mm_done, it & 1);  // on the critical path: dQ shares the P^T columns
         ptx::tc_fence_after();
         uint32_t v[2][32];
         ptx::tmem_ld_32x32b_x32(tmem + kBwdTDQ + lane_off, v[0]);
