@@ -23,7 +23,9 @@ extern "C" {
  * major: 0 = K-major (elem (r,k) at ptr[r*ld+k]), 1 = MN-major (elem (r,k) at ptr[k*ld+r]).
  * epilogue: 0 store bf16, 1 store f32, 2 accumulate f32, 3 +bias bf16, 4 +bias+residual bf16,
  *           5 +bias then GELU bf16 (GELU'(pre-activation) to aux_out), 6 times aux (= GELU') bf16,
- *           7 fp32 atomic add (split-K partial sums).
+ *           7 fp32 atomic add (split-K partial sums),
+ *           8 bf16 store + SwiGLU: aux_out[m, j] = silu(gate_j) * up_j, gate/up interleaved in
+ *             32-column blocks of C, aux_out row stride ldc / 2 (N % 64 == 0).
  * causal:   0 none, 1 skip tiles above the diagonal, 2 k <= tile last row, 3 k >= tile first row.
  */
 typedef struct zp_gemm_desc {

@@ -563,6 +563,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::bulk_commit();
             }
             buf ^= 1;
+          } else if (ep.epilogue == kEpiSwiGluBf16) {
+            // 64-column chunk = 32 gate + 32 up columns of 32 features: h = silu(gate) * up,
+            // written straight from registers (64 contiguous bytes per row)
+            if (valid && n0 < sched.N) {
+              __nv_bfloat16* hrow = ep.aux_out + int64_t(row) * (ep.ldc / 2) + n0 / 2;
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                uint32_t p[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const float g0 = v[0][i + 2 * k], g1 = v[0][i + 2 * k + 1];
+                  const float h0 = g0 / (1.f + __expf(-g0)) * v[1][i + 2 * k];
+                  const float h1 = g1 / (1.f + __expf(-g1)) * v[1][i + 2 * k + 1];
+                  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p[k]) : "f"(h1), "f"(h0));
+                }
+                *reinterpret_cast<uint4*>(hrow + i) = make_uint4(p[0], p[1], p[2], p[3]);
+              }
+            }
           } else {
 #pragma unroll
             for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + n0 + 32 * g, n0 + 32 * g, sched.N, valid);
@@ -700,9 +718,12 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   // bf16 outputs of plain (unbatched) GEMMs go through TMA stores.
   const bool bf16_out = a.epilogue == kEpiStoreBf16 || a.epilogue == kEpiBiasBf16 ||
                         a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiBiasGeluBf16 ||
-                        a.epilogue == kEpiGeluBwdBf16;
+                        a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiSwiGluBf16;
+  if (a.epilogue == kEpiSwiGluBf16 && (a.N % 64 || !a.aux_out || a.nb1 != 1 || a.nb2 != 1))
+    return cudaErrorInvalidValue;
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
+  if (a.epilogue == kEpiSwiGluBf16 && !tma_store) return cudaErrorInvalidValue;
   if (!tma_store) mc = ma;  // unused placeholder
   // aux tiles share C's layout (ldc): residual / GELU input loaded, pre-activation stored by TMA
   CUtensorMap mx = mc;

@@ -26,6 +26,8 @@ enum GemmEpilogue : int {
   kEpiBiasGeluBf16 = 5,   // u = acc + bias[n]; C(bf16) = gelu(u), aux_out(bf16) = gelu'(u)
   kEpiGeluBwdBf16 = 6,    // C(bf16) = acc * aux[m, n]   (aux = gelu'(u) from the forward)
   kEpiAtomicF32 = 7,      // C(f32) += alpha*acc with fp32 vector atomics (split-K partials)
+  kEpiSwiGluBf16 = 8,     // C(bf16) = acc (gate/up interleaved in 32-column blocks);
+                          // aux_out[m, j] (bf16, ld = ldc / 2) = silu(gate_j) * up_j
 };
 
 enum GemmCausal : int {

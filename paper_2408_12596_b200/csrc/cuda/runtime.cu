@@ -667,8 +667,9 @@ struct Runtime {
       CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st));
       mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_in);
       CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), nullptr, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
-      mm(T, 2 * f, h, L.ln2, kKMajor, h, Wp(P.w_gu), kKMajor, h, L.u, 2 * f, kEpiStoreBf16);
-      swiglu_fwd(L.u, L.g, T, int(f), ctas, st);
+      // gate/up projection; its epilogue also writes h = silu(gate) * up (SwiGLU fused)
+      mm(T, 2 * f, h, L.ln2, kKMajor, h, Wp(P.w_gu), kKMajor, h, L.u, 2 * f, kEpiSwiGluBf16, 1.f, nullptr,
+         nullptr, L.g);
       mm(T, h, f, L.g, kKMajor, f, Wp(P.w_down), kKMajor, f, x_out, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_mid);
     }
     z3_gather(NG - 1, kAgF);

@@ -121,6 +121,20 @@ def test_gemm_bias_resid_gelu(cuda, M, N, K):
     assert relerr(D, acc * Dg.float()) < 1e-2
 
 
+@pytest.mark.parametrize("M,f,K", [(256, 256, 128), (640, 5504, 512)])
+def test_gemm_swiglu_epilogue(cuda, M, f, K):
+    # gate/up interleaved in 32-column blocks of C [M, 2f]; aux_out [M, f] = silu(gate) * up
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = (0.1 * torch.randn(2 * f, K, device=cuda)).to(torch.bfloat16)
+    H = torch.empty(M, f, device=cuda, dtype=torch.bfloat16)
+    C = run_gemm(A, 0, B, 0, M, 2 * f, K, out_dtype=torch.bfloat16, epilogue=8, aux_out=H).view(M, 2 * f)
+    acc = A.float() @ B.float().t()
+    assert relerr(C, acc) < 8e-3
+    cols = torch.arange(2 * f, device=cuda)
+    gate, up = acc[:, (cols % 64) < 32], acc[:, (cols % 64) >= 32]
+    assert relerr(H, torch.nn.functional.silu(gate) * up) < 1e-2
+
+
 def test_gemm_attention_batched_heads(cuda):
     # S[z=(head, sample)] = Q_h K_h^T read in place from a fused [b*s, 3h] QKV activation.
     b, s, H, d = 2, 256, 4, 64
