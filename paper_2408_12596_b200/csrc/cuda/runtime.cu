@@ -567,15 +567,72 @@ struct Runtime {
     if (g == int(lay.groups.size()) - 1) return gb_fin;
     return gb_layer[(g - 1) & 1];
   }
+  // Over NVLink the first gather of an iteration is the barrier kernel (every rank's shard is
+  // final once all ranks reach it: the optimizer precedes it in each rank's stream). Later
+  // gathers are one-sided copy-engine pulls from the mapped peer shards; the next layer in issue
+  // order is pulled on a side stream while the current layer computes. Gathered groups stay
+  // valid until the next optimizer step, so the embedding, the final group and the two layers
+  // still in the double buffer at a forward/backward turn are not gathered again.
+  cudaStream_t cst = nullptr;             // gather prefetch stream (peer path)
+  cudaEvent_t ev_free = nullptr;          // main stream finished with the buffer being refilled
+  cudaEvent_t ev_done[2] = {};            // prefetch into gb_layer[i] landed
+  int buf_holds[2] = {-1, -1};            // group held (or being pulled) in gb_layer[i]
+  bool buf_pending[2] = {false, false};
+  bool emb_res = false, fin_res = false, z3_fresh = true;
+  void z3_invalidate() {
+    z3_fresh = true;
+    buf_holds[0] = buf_holds[1] = -1;
+    emb_res = fin_res = false;
+  }
+  void z3_pull(int g, cudaStream_t s) {
+    const int64_t part = lay.groups[g].len / n;
+    bf16* dst = gather_dst(g);
+    for (int j = 0; j < n; ++j)
+      CK(cudaMemcpyAsync(dst + part * j, pv.base[j] + off(p16s + shoff[g]), size_t(part) * 2,
+                         cudaMemcpyDeviceToDevice, s));
+  }
+  void z3_note(int g) {
+    if (g == 0)
+      emb_res = true;
+    else if (g == int(lay.groups.size()) - 1)
+      fin_res = true;
+    else
+      buf_holds[(g - 1) & 1] = g;
+  }
   void z3_gather(int g, int kind) {
     if (stage != 3 || n == 1) return;
     const Group& G = lay.groups[g];
     const int s0 = tm.mark(st);
-    if (peer)
-      CK(peer_all_gather(pv, off(p16s + shoff[g]), gather_dst(g), G.len / n, ++epoch, ctas, st));
-    else
+    if (!peer) {
       NK(ncclAllGather(p16s + shoff[g], gather_dst(g), size_t(G.len / n), ncclBfloat16, comm, st));
+      tm.close(kind, s0, st);
+      return;
+    }
+    const bool layer = g >= 1 && g <= c.n_layer;
+    const int b = (g - 1) & 1;
+    if (layer && buf_pending[b]) {  // a pull into this buffer is in flight (normally: this group's)
+      CK(cudaStreamWaitEvent(st, ev_done[b], 0));
+      buf_pending[b] = false;
+    }
+    if (z3_fresh) {
+      CK(peer_all_gather(pv, off(p16s + shoff[g]), gather_dst(g), G.len / n, ++epoch, ctas, st));
+      z3_fresh = false;
+      z3_note(g);
+    } else if (layer ? buf_holds[b] != g : !(g == 0 ? emb_res : fin_res)) {
+      z3_pull(g, st);
+      z3_note(g);
+    }
     tm.close(kind, s0, st);
+    const int nx = kind == kAgB ? g - 1 : g + 1;  // next layer group in issue order
+    if (nx >= 1 && nx <= c.n_layer && buf_holds[(nx - 1) & 1] != nx) {
+      const int nb = (nx - 1) & 1;
+      CK(cudaEventRecord(ev_free, st));
+      CK(cudaStreamWaitEvent(cst, ev_free, 0));
+      z3_pull(nx, cst);
+      CK(cudaEventRecord(ev_done[nb], cst));
+      buf_holds[nb] = nx;
+      buf_pending[nb] = true;
+    }
   }
   void z3_reduce(int g) {
     if (stage != 3 || n == 1) return;
@@ -849,7 +906,13 @@ struct Runtime {
       pv.flags[j] = static_cast<PeerFlags*>(f);
     }
     peer = agree(ok, ncclMin) == 1;
-    if (!peer) close_peers();
+    if (!peer) {
+      close_peers();
+      return;
+    }
+    CK(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_free, cudaEventDisableTiming));
+    for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   void close_peers() {
     for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
@@ -892,6 +955,7 @@ struct Runtime {
     const float gscale = 1.0f / float(double(global_batch) * c.seq_len);
     tm.reset();
     const int t0 = tm.mark(st);
+    z3_invalidate();
     int64_t sample = 0, active = 0;
     bool any_local = false;
     CK(cudaMemsetAsync(loss_steps, 0, sizeof(float) * steps.size(), st));
@@ -1316,8 +1380,13 @@ int zp_runtime_destroy(zp_runtime* h) {
   if (R.dscratch) cudaFree(R.dscratch);
   for (auto& e : R.marks)
     if (e) cudaEventDestroy(e);
+  if (R.cst) cudaStreamSynchronize(R.cst);
   if (R.arena.base) cudaFree(R.arena.base);
   if (R.st) cudaStreamDestroy(R.st);
+  if (R.cst) cudaStreamDestroy(R.cst);
+  if (R.ev_free) cudaEventDestroy(R.ev_free);
+  for (auto e : R.ev_done)
+    if (e) cudaEventDestroy(e);
   delete h;
   return ZP_OK;
 }
