@@ -2,6 +2,7 @@
 // and the ZeRO accumulate / AdamW update. 16-byte vector accesses, warp-shuffle
 // reductions, grid-stride loops capped at the rank's CTA budget.
 #include <atomic>
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.h"
@@ -242,6 +243,106 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_rows_k(const bf16* __restrict
       for (int k = 0; k < 8; ++k) o[k] = rr[k] + rs * (gg[k] * dv[k] - m1 - (xv[k] - mu) * rs * m2);
       *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
     }
+  }
+}
+
+// LayerNorm / RMSNorm backward in one pass over the rows: dx (+ residual) as above, plus per-CTA
+// column partials of dgamma, dbeta and, when cs != nullptr, of dx itself (the bias gradient of
+// the linear layer whose output this norm read). Each warp owns a strided subset of the CTA's
+// rows and accumulates into its own shared-memory slice (plain ld/st, no atomics); the CTA folds
+// the 8 slices once at the end. Replaces the rows kernel + the column kernel (which re-read dy
+// and x from HBM) + the separate bias colsum (which re-read dx).
+template <bool RMS, bool CS>
+__global__ void __launch_bounds__(kThreads) ln_bwd_fused_k(const bf16* __restrict__ dy,
+                                                           const bf16* __restrict__ x,
+                                                           const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd,
+                                                           const bf16* __restrict__ g, const bf16* dres,
+                                                           bf16* dx, int64_t rows, int h, int64_t chunk,
+                                                           float* __restrict__ part, float* __restrict__ cs) {
+  constexpr int Q = (RMS ? 1 : 2) + (CS ? 1 : 0);
+  extern __shared__ float4 ln_acc4[];
+  float* acc = reinterpret_cast<float*>(ln_acc4);  // [8 warps][Q][h]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* my = acc + size_t(w) * Q * h;
+  for (int i = lane * 4; i < Q * h; i += 128) *reinterpret_cast<float4*>(my + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  const float inv_h = 1.0f / h;
+  const int64_t r0 = blockIdx.x * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  for (int64_t r = r0 + w; r < r1; r += kThreads / 32) {
+    const float mu = mean[r], rs = rstd[r];
+    const bf16* xr = x + r * h;
+    const bf16* dyr = dy + r * h;
+    float s1 = 0.f, s2 = 0.f;
+    for (int col = lane * 8; col < h; col += 256) {
+      float xv[8], dv[8], gg[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float gd = gg[k] * dv[k];
+        s1 += gd;
+        s2 += gd * (xv[k] - mu) * rs;
+      }
+    }
+    const float m1 = RMS ? 0.f : warp_sum(s1) * inv_h;
+    const float m2 = warp_sum(s2) * inv_h;
+    for (int col = lane * 8; col < h; col += 256) {
+      float xv[8], dv[8], gg[8], rr[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
+      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+      if (dres) {
+        unpack8(*reinterpret_cast<const uint4*>(dres + r * h + col), rr);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rr[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xh = (xv[k] - mu) * rs;
+        o[k] = rr[k] + rs * (gg[k] * dv[k] - m1 - xh * m2);
+        xv[k] = xh;
+      }
+      *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
+      float4* pg = reinterpret_cast<float4*>(my + col);
+      float4 v0 = pg[0], v1 = pg[1];
+      v0.x += dv[0] * xv[0]; v0.y += dv[1] * xv[1]; v0.z += dv[2] * xv[2]; v0.w += dv[3] * xv[3];
+      v1.x += dv[4] * xv[4]; v1.y += dv[5] * xv[5]; v1.z += dv[6] * xv[6]; v1.w += dv[7] * xv[7];
+      pg[0] = v0;
+      pg[1] = v1;
+      if (!RMS) {
+        float4* pb = reinterpret_cast<float4*>(my + h + col);
+        v0 = pb[0]; v1 = pb[1];
+        v0.x += dv[0]; v0.y += dv[1]; v0.z += dv[2]; v0.w += dv[3];
+        v1.x += dv[4]; v1.y += dv[5]; v1.z += dv[6]; v1.w += dv[7];
+        pb[0] = v0;
+        pb[1] = v1;
+      }
+      if (CS) {
+        float4* pc = reinterpret_cast<float4*>(my + (Q - 1) * h + col);
+        v0 = pc[0]; v1 = pc[1];
+        v0.x += o[0]; v0.y += o[1]; v0.z += o[2]; v0.w += o[3];
+        v1.x += o[4]; v1.y += o[5]; v1.z += o[6]; v1.w += o[7];
+        pc[0] = v0;
+        pc[1] = v1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < Q * h; i += kThreads) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < kThreads / 32; ++k) t += acc[size_t(k) * Q * h + i];
+    const int q = i / h, c = i - q * h;
+    if (q == 0)
+      part[int64_t(blockIdx.x) * h + c] = t;
+    else if (!RMS && q == 1)
+      part[int64_t(gridDim.x + blockIdx.x) * h + c] = t;
+    else
+      cs[int64_t(blockIdx.x) * h + c] = t;
   }
 }
 
@@ -825,8 +926,37 @@ cudaError_t layernorm_fwd(const bf16* x, const bf16* g, const bf16* b, bf16* y, 
 
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
-                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms) {
+                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms, float* cs) {
   if (h % 256) return cudaErrorInvalidValue;
+  const int Q = (rms ? 1 : 2) + (cs ? 1 : 0);
+  const size_t smem = size_t(kThreads / 32) * Q * h * sizeof(float);
+  if (smem <= 200 * 1024) {
+    // one pass; up to 4 CTAs per SM slot of the budget, at least 8 rows per warp
+    const int per_sm = int(std::max<size_t>(1, std::min<size_t>(4, 220 * 1024 / smem)));
+    int grid = int(std::min<int64_t>(int64_t(ctas) * per_sm, (rows + 63) / 64));
+    if (grid < 1) grid = 1;
+    const int64_t chunk = (rows + grid - 1) / grid;
+    grid = int((rows + chunk - 1) / chunk);
+    *nblk = grid;
+#define ZP_LNB(R, C)                                                                                   \
+  {                                                                                                    \
+    static bool attr = false;                                                                          \
+    if (!attr) {                                                                                       \
+      cudaFuncSetAttribute(ln_bwd_fused_k<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      attr = true;                                                                                     \
+    }                                                                                                  \
+    ln_bwd_fused_k<R, C><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, chunk, part, cs); \
+  }
+    if (rms) {
+      if (cs) ZP_LNB(true, true) else ZP_LNB(true, false)
+    } else {
+      if (cs) ZP_LNB(false, true) else ZP_LNB(false, false)
+    }
+#undef ZP_LNB
+    note_launch();
+    return cudaGetLastError();
+  }
+  if (cs) return cudaErrorInvalidValue;
   const int grid = grid_for(rows, kThreads / 32, ctas, 8);
   if (rms)
     ln_bwd_rows_k<true><<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h);

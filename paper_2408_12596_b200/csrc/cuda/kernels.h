@@ -33,10 +33,12 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
                            int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s);
 
 // ---- backward
-// dx = dres + LN_bwd(dy); dgamma/dbeta partials per block into part[2][nblk][h]; returns nblk.
+// dx = dres + LN_bwd(dy); dgamma/dbeta partials per block into part[2][nblk][h] (RMS: dgamma
+// only); with cs, column partials of dx itself into cs[nblk][h]; returns nblk (<= 4 * 148).
 cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, const float* rstd,
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
-                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms = false);
+                          int64_t rows, int h, int ctas, cudaStream_t s, bool rms = false,
+                          float* cs = nullptr);
 // Rotary embedding (rotate-half, head_dim 64) on the Q and K blocks of qkv [T, 3h], in place.
 void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s);
 // SwiGLU with gate/up interleaved in 32-column blocks of gu [T, 2f]: out [T, f].

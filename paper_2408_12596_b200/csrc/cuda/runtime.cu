@@ -289,6 +289,7 @@ struct Runtime {
   float* dwpe32 = nullptr;
   float* wgrad32 = nullptr;
   float* ln_part = nullptr;
+  float* cs_part = nullptr;  // column partials of a LayerNorm backward's output (bias gradients)
   float* col_work = nullptr;
   float* loss_steps = nullptr;  // [kMaxSteps]
   int32_t* tokens = nullptr;
@@ -484,6 +485,7 @@ struct Runtime {
     dwpe32 = F32(int64_t(c.seq_len) * h, "dwpe");
     wgrad32 = F32(std::max<int64_t>(3 * h, 2 * int64_t(c.d_ff)) * h, "wgrad");
     ln_part = F32(int64_t(2) * 4 * 148 * h, "ln partials");
+    cs_part = F32(int64_t(4) * 148 * h, "bias colsum partials");
     const int64_t maxN = std::max<int64_t>(3 * h, c.d_ff);
     col_work = F32(256 * maxN, "colsum work");
     loss_steps = F32(kMaxSteps, "loss");
@@ -790,8 +792,12 @@ struct Runtime {
     // LM head (tied with wte): dlnf = dlogits * wte ; dwte = dlogits^T * lnf
     mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, Wp(lay.wte), kMNMajor, h, A.dln, h, kEpiStoreBf16);
     mm(vocab_pad, h, T, A.logits, kMNMajor, vocab_pad, A.lnf, kMNMajor, h, dwte32, h, kEpiStoreF32);
+    // every LayerNorm backward also emits the column partials of its output gradient: the bias
+    // gradient of the projection below it (b_proj from ln1 / final LN, b_o from ln2)
+    int ncs = 0;
     CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, Wp(lay.lnf_g), nullptr, A.dx, ln_part, &nblk, T,
-                     int(h), ctas, st));
+                     int(h), ctas, st, false, cs_part));
+    ncs = nblk;
     ln_grads(lay.lnf_g, lay.lnf_b, nblk);
     z3_reduce(NG - 1);
     for (int i = c.n_layer - 1; i >= 0; --i) {
@@ -800,17 +806,17 @@ struct Runtime {
       z3_gather(i + 1, kAgB);
       z3_clear_group(i + 1);
       // MLP
-      colsum_bf16(A.dx, T, int(h), int(h), col_work, Gp(P.b_proj), ctas, st);
+      sum_partials(cs_part, ncs, int(h), Gp(P.b_proj), st);
       wgrad(h, f, T, A.dx, h, L.g, f, Gp(P.w_proj));
       mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_proj), kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
       colsum_bf16(A.du, T, int(f), int(f), col_work, Gp(P.b_fc), ctas, st);
       wgrad(f, h, T, A.du, f, L.ln2, h, Gp(P.w_fc));
       mm(T, h, f, A.du, kKMajor, f, Wp(P.w_fc), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h),
-                       ctas, st));
+                       ctas, st, false, cs_part));
       ln_grads(P.ln2_g, P.ln2_b, nblk);
       // attention output projection
-      colsum_bf16(A.dx2, T, int(h), int(h), col_work, Gp(P.b_o), ctas, st);
+      sum_partials(cs_part, nblk, int(h), Gp(P.b_o), st);
       wgrad(h, h, T, A.dx2, h, L.attn, h, Gp(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
       // fused attention backward (recomputes P from the saved LSE)
@@ -820,7 +826,8 @@ struct Runtime {
       wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h),
-                       ctas, st));
+                       ctas, st, false, i > 0 ? cs_part : nullptr));
+      ncs = nblk;
       ln_grads(P.ln1_g, P.ln1_b, nblk);
       z3_reduce(i + 1);
     }
