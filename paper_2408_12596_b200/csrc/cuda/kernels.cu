@@ -4,6 +4,7 @@
 #include <atomic>
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -247,96 +248,124 @@ __global__ void __launch_bounds__(kThreads) ln_bwd_rows_k(const bf16* __restrict
 }
 
 // LayerNorm / RMSNorm backward in one pass over the rows: dx (+ residual) as above, plus per-CTA
-// column partials of dgamma, dbeta and, when cs != nullptr, of dx itself (the bias gradient of
-// the linear layer whose output this norm read). Each warp owns a strided subset of the CTA's
-// rows and accumulates into its own shared-memory slice (plain ld/st, no atomics); the CTA folds
-// the 8 slices once at the end. Replaces the rows kernel + the column kernel (which re-read dy
-// and x from HBM) + the separate bias colsum (which re-read dx).
-template <bool RMS, bool CS>
-__global__ void __launch_bounds__(kThreads) ln_bwd_fused_k(const bf16* __restrict__ dy,
-                                                           const bf16* __restrict__ x,
+// column partials of dgamma, dbeta and, with CS, of dx itself (the bias gradient of the linear
+// layer whose output this norm read). Replaces the rows kernel + the column kernel (which re-read
+// dy and x from HBM) + the separate bias colsum (which re-read dx). Each warp takes two rows at
+// a time (their loads in flight together; a lane owns 8 consecutive columns per 256), adds the
+// two rows' column contributions in registers and folds them into its own shared-memory slice,
+// laid out [q][vector][k][lane] so each access is one conflict-free wavefront; the CTA folds its
+// 8 slices at the end.
+template <bool RMS, bool CS, int NV>  // NV = h / 256 when known at compile time, else 0
+__global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                                            const float* __restrict__ mean,
                                                            const float* __restrict__ rstd,
-                                                           const bf16* __restrict__ g, const bf16* dres,
-                                                           bf16* dx, int64_t rows, int h, int64_t chunk,
+                                                           const bf16* __restrict__ g, const bf16* dres, bf16* dx,
+                                                           int64_t rows, int h, int64_t chunk,
                                                            float* __restrict__ part, float* __restrict__ cs) {
   constexpr int Q = (RMS ? 1 : 2) + (CS ? 1 : 0);
   extern __shared__ float4 ln_acc4[];
   float* acc = reinterpret_cast<float*>(ln_acc4);  // [8 warps][Q][h]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nv = NV > 0 ? NV : h / 256;
   float* my = acc + size_t(w) * Q * h;
-  for (int i = lane * 4; i < Q * h; i += 128) *reinterpret_cast<float4*>(my + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = lane; i < Q * h; i += 32) my[i] = 0.f;
   __syncwarp();
   const float inv_h = 1.0f / h;
   const int64_t r0 = blockIdx.x * chunk;
   const int64_t r1 = min(rows, r0 + chunk);
-  for (int64_t r = r0 + w; r < r1; r += kThreads / 32) {
-    const float mu = mean[r], rs = rstd[r];
-    const bf16* xr = x + r * h;
-    const bf16* dyr = dy + r * h;
-    float s1 = 0.f, s2 = 0.f;
-    for (int col = lane * 8; col < h; col += 256) {
-      float xv[8], dv[8], gg[8];
-      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
-      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
-      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+  for (int64_t ra = r0 + 2 * w; ra < r1; ra += 2 * (kThreads / 32)) {
+    const bool two = ra + 1 < r1;
+    const int64_t rb = two ? ra + 1 : ra;
+    const float mua = mean[ra], rsa = rstd[ra], mub = mean[rb], rsb = rstd[rb];
+    const bf16* xa = x + ra * h + lane * 8;
+    const bf16* xb = x + rb * h + lane * 8;
+    const bf16* da = dy + ra * h + lane * 8;
+    const bf16* db = dy + rb * h + lane * 8;
+    float s1a = 0.f, s2a = 0.f, s1b = 0.f, s2b = 0.f;
+#pragma unroll
+    for (int j = 0; j < nv; ++j) {
+      const uint4 qxa = *reinterpret_cast<const uint4*>(xa + 256 * j);
+      const uint4 qda = *reinterpret_cast<const uint4*>(da + 256 * j);
+      const uint4 qxb = *reinterpret_cast<const uint4*>(xb + 256 * j);
+      const uint4 qdb = *reinterpret_cast<const uint4*>(db + 256 * j);
+      float gg[8], xv[8], dv[8];
+      unpack8(*reinterpret_cast<const uint4*>(g + lane * 8 + 256 * j), gg);
+      unpack8(qxa, xv);
+      unpack8(qda, dv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float gd = gg[k] * dv[k];
-        s1 += gd;
-        s2 += gd * (xv[k] - mu) * rs;
+        s1a += gd;
+        s2a += gd * (xv[k] - mua) * rsa;
       }
-    }
-    const float m1 = RMS ? 0.f : warp_sum(s1) * inv_h;
-    const float m2 = warp_sum(s2) * inv_h;
-    for (int col = lane * 8; col < h; col += 256) {
-      float xv[8], dv[8], gg[8], rr[8], o[8];
-      unpack8(*reinterpret_cast<const uint4*>(xr + col), xv);
-      unpack8(*reinterpret_cast<const uint4*>(dyr + col), dv);
-      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
-      if (dres) {
-        unpack8(*reinterpret_cast<const uint4*>(dres + r * h + col), rr);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) rr[k] = 0.f;
-      }
+      unpack8(qxb, xv);
+      unpack8(qdb, dv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float xh = (xv[k] - mu) * rs;
-        o[k] = rr[k] + rs * (gg[k] * dv[k] - m1 - xh * m2);
-        xv[k] = xh;
+        const float gd = gg[k] * dv[k];
+        s1b += gd;
+        s2b += gd * (xv[k] - mub) * rsb;
       }
-      *reinterpret_cast<uint4*>(dx + r * h + col) = pack8(o);
-      float4* pg = reinterpret_cast<float4*>(my + col);
-      float4 v0 = pg[0], v1 = pg[1];
-      v0.x += dv[0] * xv[0]; v0.y += dv[1] * xv[1]; v0.z += dv[2] * xv[2]; v0.w += dv[3] * xv[3];
-      v1.x += dv[4] * xv[4]; v1.y += dv[5] * xv[5]; v1.z += dv[6] * xv[6]; v1.w += dv[7] * xv[7];
-      pg[0] = v0;
-      pg[1] = v1;
-      if (!RMS) {
-        float4* pb = reinterpret_cast<float4*>(my + h + col);
-        v0 = pb[0]; v1 = pb[1];
-        v0.x += dv[0]; v0.y += dv[1]; v0.z += dv[2]; v0.w += dv[3];
-        v1.x += dv[4]; v1.y += dv[5]; v1.z += dv[6]; v1.w += dv[7];
-        pb[0] = v0;
-        pb[1] = v1;
+    }
+    const float m1a = RMS ? 0.f : warp_sum(s1a) * inv_h;
+    const float m2a = warp_sum(s2a) * inv_h;
+    const float m1b = RMS ? 0.f : warp_sum(s1b) * inv_h;
+    const float m2b = warp_sum(s2b) * inv_h;
+#pragma unroll 1
+    for (int j = 0; j < nv; ++j) {  // second pass re-reads the two rows (L1 hits)
+      const int col = lane * 8 + 256 * j;
+      const uint4 qxa = *reinterpret_cast<const uint4*>(xa + 256 * j);
+      const uint4 qda = *reinterpret_cast<const uint4*>(da + 256 * j);
+      const uint4 qxb = *reinterpret_cast<const uint4*>(xb + 256 * j);
+      const uint4 qdb = *reinterpret_cast<const uint4*>(db + 256 * j);
+      uint4 qra = make_uint4(0, 0, 0, 0), qrb = make_uint4(0, 0, 0, 0);
+      if (dres) {
+        qra = *reinterpret_cast<const uint4*>(dres + ra * h + col);
+        qrb = *reinterpret_cast<const uint4*>(dres + rb * h + col);
       }
-      if (CS) {
-        float4* pc = reinterpret_cast<float4*>(my + (Q - 1) * h + col);
-        v0 = pc[0]; v1 = pc[1];
-        v0.x += o[0]; v0.y += o[1]; v0.z += o[2]; v0.w += o[3];
-        v1.x += o[4]; v1.y += o[5]; v1.z += o[6]; v1.w += o[7];
-        pc[0] = v0;
-        pc[1] = v1;
+      float gg[8], xv[8], dv[8], o[8], sg[8], sb[8], sc[8];
+      unpack8(*reinterpret_cast<const uint4*>(g + col), gg);
+      unpack8(qxa, xv);
+      unpack8(qda, dv);
+      unpack8(qra, o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xh = (xv[k] - mua) * rsa;
+        o[k] += rsa * (gg[k] * dv[k] - m1a - xh * m2a);
+        sg[k] = xh * dv[k];
+        sb[k] = dv[k];
+        sc[k] = o[k];
+      }
+      *reinterpret_cast<uint4*>(dx + ra * h + col) = pack8(o);
+      unpack8(qxb, xv);
+      unpack8(qdb, dv);
+      unpack8(qrb, o);
+      const float keep = two ? 1.f : 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float xh = (xv[k] - mub) * rsb;
+        o[k] += rsb * (gg[k] * dv[k] - m1b - xh * m2b);
+        sg[k] += keep * (xh * dv[k]);
+        sb[k] += keep * dv[k];
+        sc[k] += keep * o[k];
+      }
+      if (two) *reinterpret_cast<uint4*>(dx + rb * h + col) = pack8(o);
+      float* p0 = my + (size_t(j) * 8) * 32 + lane;  // [q][j][k][lane]
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        p0[k * 32] += sg[k];
+        if (!RMS) p0[h + k * 32] += sb[k];
+        if (CS) p0[(Q - 1) * h + k * 32] += sc[k];
       }
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < Q * h; i += kThreads) {
+    const int q = i / h, c = i - q * h;
+    const int sl = q * h + ((c >> 8) * 8 + (c & 7)) * 32 + ((c & 255) >> 3);
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < kThreads / 32; ++k) t += acc[size_t(k) * Q * h + i];
-    const int q = i / h, c = i - q * h;
+    for (int k = 0; k < kThreads / 32; ++k) t += acc[size_t(k) * Q * h + sl];
     if (q == 0)
       part[int64_t(blockIdx.x) * h + c] = t;
     else if (!RMS && q == 1)
@@ -931,26 +960,30 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
   const int Q = (rms ? 1 : 2) + (cs ? 1 : 0);
   const size_t smem = size_t(kThreads / 32) * Q * h * sizeof(float);
   if (smem <= 200 * 1024) {
-    // one pass; up to 4 CTAs per SM slot of the budget, at least 8 rows per warp
-    const int per_sm = int(std::max<size_t>(1, std::min<size_t>(4, 220 * 1024 / smem)));
+    // one pass; as many CTAs per SM slot of the budget as shared memory allows
+    const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, 227 * 1024 / (smem + 1024))));  // 2: registers
     int grid = int(std::min<int64_t>(int64_t(ctas) * per_sm, (rows + 63) / 64));
     if (grid < 1) grid = 1;
     const int64_t chunk = (rows + grid - 1) / grid;
     grid = int((rows + chunk - 1) / chunk);
     *nblk = grid;
-#define ZP_LNB(R, C)                                                                                   \
+#define ZP_LNB(R, C, NV)                                                                               \
   {                                                                                                    \
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
-      cudaFuncSetAttribute(ln_bwd_fused_k<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+      cudaFuncSetAttribute(ln_bwd_fused_k<R, C, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
       attr = true;                                                                                     \
     }                                                                                                  \
-    ln_bwd_fused_k<R, C><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, chunk, part, cs); \
+    ln_bwd_fused_k<R, C, NV><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, chunk, part, cs); \
   }
     if (rms) {
-      if (cs) ZP_LNB(true, true) else ZP_LNB(true, false)
+      if (cs) ZP_LNB(true, true, 0) else ZP_LNB(true, false, 0)
+    } else if (h == 768) {
+      if (cs) ZP_LNB(false, true, 3) else ZP_LNB(false, false, 3)
+    } else if (h == 1024) {
+      if (cs) ZP_LNB(false, true, 4) else ZP_LNB(false, false, 4)
     } else {
-      if (cs) ZP_LNB(false, true) else ZP_LNB(false, false)
+      if (cs) ZP_LNB(false, true, 0) else ZP_LNB(false, false, 0)
     }
 #undef ZP_LNB
     note_launch();
