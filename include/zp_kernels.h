@@ -41,6 +41,8 @@ typedef struct zp_gemm_desc {
   void* aux_out;
   int32_t max_ctas;
   int32_t split_k;  /* > 1 splits the K range across CTAs, -1 picks the split for full waves; needs epilogue 7 (fp32 atomic add) */
+  float* colsum;    /* optional, bf16 epilogues of unbatched GEMMs: colsum[n] += sum over m of C[m, n]
+                       (fp32 [N], caller-zeroed; the bias gradient when C is an output gradient) */
 } zp_gemm_desc;
 
 int zp_gemm(const zp_gemm_desc* d, void* stream);

@@ -42,6 +42,7 @@ class GemmDesc(C.Structure):
         ("aux_out", C.c_void_p),
         ("max_ctas", C.c_int32),
         ("split_k", C.c_int32),
+        ("colsum", C.c_void_p),
     ]
 
 

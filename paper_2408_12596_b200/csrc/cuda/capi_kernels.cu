@@ -19,6 +19,7 @@ extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
   a.aux_out = d->aux_out;
   a.max_ctas = d->max_ctas;
   a.split_k = d->split_k;
+  a.colsum = d->colsum;
   const cudaError_t e = zp::gemm(a, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : 5;
 }

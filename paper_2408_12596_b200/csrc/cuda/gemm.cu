@@ -101,7 +101,34 @@ struct EpiParams {
   int tma_store;  // bf16 output written through swizzled smem boxes + TMA stores
   int aux_tma;      // residual / GELU-input rows loaded by TMA into the staging boxes
   int aux_out_tma;  // GELU pre-activation written by TMA stores
+  float* colsum;    // += column sums of the bf16-path output over the rows (fp32 [N]); may be null
 };
+
+// Column sums of one warp's 32 rows x 64 columns (v[g][i]: row = lane, column = 32g + i) added
+// into colsum with one fp32 atomic per column: a butterfly transpose-reduce leaves column L's sum
+// in lane L (31 shuffles per 32 columns). Destroys v.
+__device__ __forceinline__ void warp_colsum_add(float (&v)[2][32], bool valid, float* colsum, int n0, int N) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    if (!valid) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[g][i] = 0.f;
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool up = lane & s;
+#pragma unroll
+      for (int i = 0; i < s; ++i) {
+        const float send = up ? v[g][i] : v[g][i + s];
+        const float keep = up ? v[g][i + s] : v[g][i];
+        v[g][i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    const int n = n0 + 32 * g + lane;
+    if (n < N) atomicAdd(colsum + n, v[g][0]);
+  }
+}
 
 // GELU (tanh form) with the MUFU tanh approximation (rel. error ~2^-11, below bf16 output
 // rounding).
@@ -597,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::bulk_commit();
           }
           buf ^= 1;
+          if (ep.colsum) warp_colsum_add(v, valid, ep.colsum, n0, sched.N);
         } else {
 #pragma unroll 1
           for (int g = 0; g < 2; ++g) {
@@ -724,6 +752,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
   if (a.epilogue == kEpiSwiGluBf16 && !tma_store) return cudaErrorInvalidValue;
+  if (a.colsum && !tma_store) return cudaErrorInvalidValue;
   if (!tma_store) mc = ma;  // unused placeholder
   // aux tiles share C's layout (ldc): residual / GELU input loaded, pre-activation stored by TMA
   CUtensorMap mx = mc;
@@ -780,6 +809,7 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.tma_store = tma_store ? 1 : 0;
   ep.aux_tma = aux_tma ? 1 : 0;
   ep.aux_out_tma = aux_out_tma ? 1 : 0;
+  ep.colsum = a.colsum;
   int units = workers;
   if (s.total < units) units = s.total;
   if (units < 1) return cudaSuccess;

@@ -58,6 +58,7 @@ struct GemmArgs {
   void* aux_out = nullptr;     // bf16, same layout as C (gelu'(u) written by kEpiBiasGeluBf16)
   int max_ctas = 0;            // SM budget cap (0 = all SMs)
   int split_k = 1;             // >1: K range split across CTAs; -1: auto; requires kEpiAtomicF32
+  float* colsum = nullptr;     // bf16 epilogues: += column sums of the output (fp32 [N]; bias grad)
 };
 
 // Returns cudaSuccess or the launch/encode error.

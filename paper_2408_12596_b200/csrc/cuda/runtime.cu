@@ -356,7 +356,7 @@ struct Runtime {
   }
   void mm(int M, int N, int K, const bf16* A, int amaj, int64_t lda, const bf16* B, int bmaj,
           int64_t ldb, void* C, int64_t ldc, int epi, float alpha = 1.f, const bf16* bias = nullptr,
-          const bf16* aux = nullptr, bf16* aux_out = nullptr, int split_k = 1) {
+          const bf16* aux = nullptr, bf16* aux_out = nullptr, int split_k = 1, float* colsum = nullptr) {
     GemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.a.ptr = A; g.a.major = amaj; g.a.ld = lda;
@@ -365,6 +365,7 @@ struct Runtime {
     g.alpha = alpha; g.epilogue = epi; g.bias = bias; g.aux = aux; g.aux_out = aux_out;
     g.max_ctas = ctas;
     g.split_k = split_k;
+    g.colsum = colsum;
     launch_gemm(g, 2.0 * M * double(N) * K);
   }
   // Weight gradient dW[M, N] = sum over the T tokens: few output tiles, very long K. Split K
@@ -808,8 +809,11 @@ struct Runtime {
       // MLP
       sum_partials(cs_part, ncs, int(h), Gp(P.b_proj), st);
       wgrad(h, f, T, A.dx, h, L.g, f, Gp(P.w_proj));
-      mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_proj), kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u);
-      colsum_bf16(A.du, T, int(f), int(f), col_work, Gp(P.b_fc), ctas, st);
+      // dgrad through GELU'; its epilogue also sums the columns of du (the b_fc gradient)
+      CK(cudaMemsetAsync(col_work, 0, size_t(f) * 4, st));
+      mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_proj), kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u, nullptr,
+         1, col_work);
+      sum_partials(col_work, 1, int(f), Gp(P.b_fc), st);
       wgrad(f, h, T, A.du, f, L.ln2, h, Gp(P.w_fc));
       mm(T, h, f, A.du, kKMajor, f, Wp(P.w_fc), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h),

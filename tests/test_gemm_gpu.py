@@ -19,7 +19,8 @@ def _lib():
 
 def run_gemm(A_store, a_major, B_store, b_major, M, N, K, out_dtype=torch.float32, epilogue=None,
              alpha=1.0, causal=0, nb=(1, 1), a_bs=(0, 0), b_bs=(0, 0), c=None, ldc=None, c_bs=(0, 0),
-             bias=None, aux=None, aux_out=None, lda=None, ldb=None, max_ctas=0, sync=True, split_k=1):
+             bias=None, aux=None, aux_out=None, lda=None, ldb=None, max_ctas=0, sync=True, split_k=1,
+             colsum=None):
     L = _lib()
     if c is None:
         c = torch.zeros(nb[1] * nb[0] * M * N, dtype=out_dtype, device=A_store.device)
@@ -44,6 +45,7 @@ def run_gemm(A_store, a_major, B_store, b_major, M, N, K, out_dtype=torch.float3
     d.aux_out = aux_out.data_ptr() if aux_out is not None else None
     d.max_ctas = max_ctas
     d.split_k = split_k
+    d.colsum = colsum.data_ptr() if colsum is not None else None
     rc = L.lib.zp_gemm(d, torch.cuda.current_stream().cuda_stream)
     assert rc == 0
     if sync:
@@ -119,6 +121,11 @@ def test_gemm_bias_resid_gelu(cuda, M, N, K):
     assert relerr(Dg, gp) < 1e-2  # aux_out = GELU'(pre-activation)
     D = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, epilogue=6, aux=Dg).view(M, N)
     assert relerr(D, acc * Dg.float()) < 1e-2
+    # the same with the column sums of the output (the bias gradient) from the epilogue
+    cs = torch.zeros(N, device=cuda)
+    D2 = run_gemm(A, 0, B, 0, M, N, K, out_dtype=torch.bfloat16, epilogue=6, aux=Dg, colsum=cs).view(M, N)
+    assert torch.equal(D2, D)
+    assert relerr(cs, (acc * Dg.float()).sum(0)) < 1e-2
 
 
 @pytest.mark.parametrize("M,f,K", [(256, 256, 128), (640, 5504, 512)])
