@@ -670,17 +670,25 @@ __global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_
 }
 
 // out[c] = sum over k of part[k, c]: block (32 columns x 8 row stripes), coalesced 128-byte rows.
-__global__ void sum_partials_k(const float* part, int nparts, int N, bf16* out) {
-  __shared__ float sh[8][33];
+// 32 columns per CTA, 32 row groups: a few independent loads per thread (latency-bound size)
+__global__ void __launch_bounds__(1024) sum_partials_k(const float* part, int nparts, int N, bf16* out) {
+  __shared__ float sh[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
-  float s = 0.f;
-  if (c < N)
-    for (int k = threadIdx.y; k < nparts; k += 8) s += part[int64_t(k) * N + c];
-  sh[threadIdx.y][threadIdx.x] = s;
+  float s0 = 0.f, s1 = 0.f;
+  if (c < N) {
+    int k = threadIdx.y;
+    for (; k + 32 < nparts; k += 64) {
+      s0 += part[int64_t(k) * N + c];
+      s1 += part[int64_t(k + 32) * N + c];
+    }
+    if (k < nparts) s0 += part[int64_t(k) * N + c];
+  }
+  sh[threadIdx.y][threadIdx.x] = s0 + s1;
   __syncthreads();
   if (threadIdx.y == 0 && c < N) {
+    float s = 0.f;
 #pragma unroll
-    for (int k = 1; k < 8; ++k) s += sh[k][threadIdx.x];
+    for (int k = 0; k < 32; ++k) s += sh[k][threadIdx.x];
     out[c] = __float2bfloat16_rn(s);
   }
 }
@@ -1037,10 +1045,10 @@ void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* 
   const int64_t chunk = (rows + chunks - 1) / chunks;
   chunks = int((rows + chunk - 1) / chunk);
   colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work); note_launch();
-  sum_partials_k<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(work, chunks, N, out); note_launch();
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(work, chunks, N, out); note_launch();
 }
 void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s) {
-  sum_partials_k<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(part, nparts, N, out); note_launch();
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(part, nparts, N, out); note_launch();
 }
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
   cast_k<<<grid_for(n / 4 + 1, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();
