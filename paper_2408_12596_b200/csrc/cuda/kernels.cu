@@ -636,6 +636,126 @@ __global__ void __launch_bounds__(kCeThreads, 1) ce_smem_k(bf16* logits, const i
   }
 }
 
+// The same cross-entropy with each thread's share of the row held in registers (MAXC 16-byte
+// chunks): one shared-memory read pass instead of three, and the row's buffer is handed back to
+// the bulk-copy engine as soon as the block has read it (two rows in flight while one computes).
+template <int MAXC>
+__global__ void __launch_bounds__(kCeThreads, 1) ce_reg_k(bf16* logits, const int32_t* tok, int seq, int64_t rows,
+                                                          int vocab, int ldv, float gscale, float* row_loss) {
+  constexpr float kL2e = 1.4426950408889634f;
+  extern __shared__ __align__(128) uint8_t ce_smem[];
+  __shared__ uint64_t bar[2];
+  __shared__ float shm[kCeThreads / 32], shs[kCeThreads / 32];
+  const uint32_t row_bytes = uint32_t(ldv) * 2;
+  const uint32_t stride = (row_bytes + 127) & ~127u;
+  const int nvec = ldv / 8, nfull = vocab / 8;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t r, int buf) {
+    ptx::mbar_arrive_expect_tx(&bar[buf], row_bytes);
+    ptx::bulk_load(ce_smem + buf * stride, logits + r * ldv, row_bytes, &bar[buf]);
+  };
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < rows) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < rows) issue(blockIdx.x + gridDim.x, 1);
+  }
+  uint32_t it = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
+    const uint4* row = reinterpret_cast<const uint4*>(ce_smem + buf * stride);
+    const int64_t smp = r / seq;
+    const int pos = int(r % seq);
+    const int target = tok[smp * (seq + 1) + pos + 1];
+    float tl = 0.f;
+    if (threadIdx.x == 0) tl = __bfloat162float(reinterpret_cast<const bf16*>(row)[target]);
+    uint4 q[MAXC];
+    __nv_bfloat162 mx2 = __float2bfloat162_rn(-INFINITY);
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = threadIdx.x + c * kCeThreads;
+      q[c] = i < nvec ? row[i] : make_uint4(0, 0, 0, 0);
+      if (i < nfull) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[c]);
+        mx2 = __hmax2(mx2, __hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])));
+      }
+    }
+    float m = fmaxf(__low2float(mx2), __high2float(mx2));
+    if (nfull < nvec && threadIdx.x == (nfull % kCeThreads)) {  // ragged tail chunk (vocab % 8)
+      const bf16* t = reinterpret_cast<const bf16*>(row) + nfull * 8;
+      for (int k = 0; k < vocab - nfull * 8; ++k) m = fmaxf(m, __bfloat162float(t[k]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) shm[w] = m;
+    __syncthreads();  // every thread has read the row: the buffer takes the row after next
+    if (threadIdx.x == 0 && r + 2 * int64_t(gridDim.x) < rows) {
+      ptx::fence_proxy_async_smem();
+      issue(r + 2 * int64_t(gridDim.x), buf);
+    }
+    m = shm[0];
+#pragma unroll
+    for (int k = 1; k < kCeThreads / 32; ++k) m = fmaxf(m, shm[k]);
+    m *= kL2e;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = threadIdx.x + c * kCeThreads;
+      if (i < nvec) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[c]);
+        float f[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 t = __bfloat1622float2(h[k]);
+          f[2 * k] = ex2_fast(fmaf(t.x, kL2e, -m));
+          f[2 * k + 1] = ex2_fast(fmaf(t.y, kL2e, -m));
+        }
+        if (i >= nfull) {
+          const int valid = vocab - i * 8;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = k < valid ? f[k] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          s0 += f[k];
+          s1 += f[k + 1];
+        }
+        q[c] = pack8(f);  // e rounded to bf16, as the shared-memory kernel stores it
+      }
+    }
+    float sum = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) shs[w] = sum;
+    __syncthreads();
+    sum = shs[0];
+#pragma unroll
+    for (int k = 1; k < kCeThreads / 32; ++k) sum += shs[k];
+    const float coef = gscale / sum;
+    uint4* out = reinterpret_cast<uint4*>(logits + r * ldv);
+    const int tchunk = target / 8, tk = target - tchunk * 8;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int i = threadIdx.x + c * kCeThreads;
+      if (i < nvec) {
+        float f[8];
+        unpack8(q[c], f);
+        const float sub = i == tchunk ? gscale : 0.f;  // one-hot term, branch-free
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = f[k] * coef - (k == tk ? sub : 0.f);
+        out[i] = pack8(f);
+      }
+    }
+    if (threadIdx.x == 0) row_loss[r] = (m + __log2f(sum)) / kL2e - tl;
+    __syncthreads();  // shm / shs reused by the next row
+  }
+}
+
 // ------------------------------------------------------------------ reductions
 
 // Partial column sums: block (32, 8) covers 256 columns (8 per thread, 16-byte loads) x one
@@ -1021,6 +1141,28 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
 void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t rows, int vocab,
                            int ldv, float grad_scale, float* row_loss, int ctas, cudaStream_t s) {
   const size_t stride = (size_t(ldv) * 2 + 127) & ~size_t(127);
+  const int nvec = ldv / 8;
+  if (2 * stride <= 200 * 1024 && nvec <= 16 * kCeThreads) {
+    const int grid = int(rows < ctas ? rows : ctas);
+#define ZP_CE(C)                                                                                        \
+  {                                                                                                     \
+    static bool attr = false;                                                                           \
+    if (!attr) {                                                                                        \
+      cudaFuncSetAttribute(ce_reg_k<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);       \
+      attr = true;                                                                                      \
+    }                                                                                                   \
+    ce_reg_k<C><<<grid, kCeThreads, 2 * stride, s>>>(logits, tokens, seq, rows, vocab, ldv, grad_scale, row_loss); \
+  }
+    if (nvec <= 8 * kCeThreads)
+      ZP_CE(8)
+    else if (nvec <= 13 * kCeThreads)
+      ZP_CE(13)
+    else
+      ZP_CE(16)
+#undef ZP_CE
+    note_launch();
+    return;
+  }
   if (2 * stride <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {

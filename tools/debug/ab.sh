@@ -10,6 +10,6 @@ for v in B A B2 A2; do
   case $v in A|A2) cp alt_lib/libA.so paper_2408_12596_b200/lib/libzp.so;; *) cp alt_lib/libB.so paper_2408_12596_b200/lib/libzp.so;; esac
   ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ab/l_$v.csv python tools/profile_step.py --b 64 > gpurun_out/ab/ncu_$v.log 2>&1
   python tools/launch_summary.py gpurun_out/ab/l_$v.csv "$v" > gpurun_out/ab/l_$v.md
-  echo "== $v"; grep -E "launches,|attn_bwd|dq_cast|colsum|sum_partials|gemm_tc_kernel<256, 0, 0" gpurun_out/ab/l_$v.md
+  echo "== $v"; grep -E "launches,|ce_|gemm_tc_kernel<256, 0, 0" gpurun_out/ab/l_$v.md
 done
 cp alt_lib/libB.so paper_2408_12596_b200/lib/libzp.so
