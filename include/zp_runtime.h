@@ -108,6 +108,12 @@ int zp_runtime_keep_grads(zp_runtime* rt, int32_t on);
  * all-gather kernel at the ZeRO-1/2 synchronisation point),
  * 0 when they run over NCCL (world size 1, ZP_PEER=0, or a rank that cannot map its peers). */
 int zp_runtime_peer_collectives(zp_runtime* rt, int32_t* on);
+/* NVLink microbenchmark on the ZeRO-2 layout (every rank calls it with the same arguments):
+ * which 0 = pull reduce-scatter of the bf16 gradient (peer_rs_acc_k), 1 = pull all-gather of the
+ * bf16 parameter shards (peer_ag_k), 2 = copy-engine pulls of every peer's shard (the ZeRO-3
+ * prefetch path). *seconds = mean device time per call over reps (CUDA events on the runtime
+ * stream, after one warm-up call); *pulled = bytes this rank reads from its peers per call. */
+int zp_runtime_bench_collective(zp_runtime* rt, int32_t which, int32_t reps, double* seconds, int64_t* pulled);
 /* Flat-layout ranges this rank owns, as (flat_begin, flat_end, shard_begin) triples: one range
  * at stages 0-2, one per parameter group (embedding, each layer, final LN) at stage 3, where the
  * shard buffers of zp_runtime_get_state are the concatenation of the owned slices. */

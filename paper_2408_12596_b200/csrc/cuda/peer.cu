@@ -92,7 +92,35 @@ __global__ void __launch_bounds__(kThreads) peer_rs_acc_k(PeerView pv, int64_t s
                                                           uint32_t epoch) {
   entry_barrier(pv, epoch);
   const int64_t n8 = len / 8;
-  for (int64_t i = blockIdx.x * int64_t(kThreads) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * kThreads) {
+  const int64_t step = int64_t(gridDim.x) * kThreads;
+  int64_t i0 = blockIdx.x * int64_t(kThreads) + threadIdx.x;
+  // two items per thread: 2n remote loads in flight before the sums (same per-element order)
+  for (; i0 + step < n8; i0 += 2 * step) {
+    float g[2][8];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) g[t][k] = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < pv.n; ++j) {
+      const uint4* p = reinterpret_cast<const uint4*>(pv.base[j] + src_off) + shard_off / 8;
+      const uint4 u0 = p[i0], u1 = p[i0 + step];
+      add_bf16x8(g[0], u0);
+      add_bf16x8(g[1], u1);
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      float4* a = reinterpret_cast<float4*>(acc) + 2 * (i0 + t * step);
+      if (!overwrite) {
+        const float4 x = a[0], y = a[1];
+        g[t][0] += x.x; g[t][1] += x.y; g[t][2] += x.z; g[t][3] += x.w;
+        g[t][4] += y.x; g[t][5] += y.y; g[t][6] += y.z; g[t][7] += y.w;
+      }
+      a[0] = make_float4(g[t][0], g[t][1], g[t][2], g[t][3]);
+      a[1] = make_float4(g[t][4], g[t][5], g[t][6], g[t][7]);
+    }
+  }
+  for (int64_t i = i0; i < n8; i += step) {
     float g[8];
     pull_sum8<false>(pv, src_off, shard_off + i * 8, g);
     float4* a = reinterpret_cast<float4*>(acc) + 2 * i;
@@ -164,10 +192,31 @@ __global__ void __launch_bounds__(kThreads) peer_ag_k(PeerView pv, int64_t src_o
                                                       int64_t len, uint32_t epoch) {
   entry_barrier(pv, epoch);
   const int64_t n8 = len / 8, total8 = n8 * pv.n;
-  for (int64_t i = blockIdx.x * int64_t(kThreads) + threadIdx.x; i < total8; i += int64_t(gridDim.x) * kThreads) {
-    const int j = int(i / n8);
-    const int64_t e = i - int64_t(j) * n8;
-    reinterpret_cast<uint4*>(dst)[i] = *(reinterpret_cast<const uint4*>(pv.base[j] + src_off) + e);
+  const int64_t step = int64_t(gridDim.x) * kThreads;
+  int64_t i = blockIdx.x * int64_t(kThreads) + threadIdx.x;
+  // Item i is element e of the c-th shard in this rank's visiting order, which starts at the next
+  // rank: at any moment every GPU is read by one peer instead of all ranks reading rank 0 first.
+  // Four remote 16-byte loads in flight per thread before their stores (NVLink latency).
+  for (; i + 3 * step < total8; i += 4 * step) {
+    uint4 u[4];
+    int64_t d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ii = i + k * step;
+      const int c = int(ii / n8);
+      const int64_t e = ii - int64_t(c) * n8;
+      const int j = (c + pv.rank + 1) % pv.n;
+      u[k] = *(reinterpret_cast<const uint4*>(pv.base[j] + src_off) + e);
+      d[k] = int64_t(j) * n8 + e;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) reinterpret_cast<uint4*>(dst)[d[k]] = u[k];
+  }
+  for (; i < total8; i += step) {
+    const int c = int(i / n8);
+    const int64_t e = i - int64_t(c) * n8;
+    const int j = (c + pv.rank + 1) % pv.n;
+    reinterpret_cast<uint4*>(dst)[int64_t(j) * n8 + e] = *(reinterpret_cast<const uint4*>(pv.base[j] + src_off) + e);
   }
   exit_barrier(pv, epoch);
 }

@@ -590,9 +590,11 @@ struct Runtime {
   void z3_pull(int g, cudaStream_t s) {
     const int64_t part = lay.groups[g].len / n;
     bf16* dst = gather_dst(g);
-    for (int j = 0; j < n; ++j)
+    for (int k = 1; k <= n; ++k) {  // start at the next rank: no GPU is read by every peer at once
+      const int j = (rank + k) % n;
       CK(cudaMemcpyAsync(dst + part * j, pv.base[j] + off(p16s + shoff[g]), size_t(part) * 2,
                          cudaMemcpyDeviceToDevice, s));
+    }
   }
   void z3_note(int g) {
     if (g == 0)
@@ -1521,6 +1523,46 @@ int zp_runtime_owned_ranges(zp_runtime* h, int64_t* triples, int32_t cap, int32_
 int zp_runtime_peer_collectives(zp_runtime* h, int32_t* on) {
   *on = h->rt.peer ? 1 : 0;
   return ZP_OK;
+}
+
+int zp_runtime_bench_collective(zp_runtime* h, int32_t which, int32_t reps, double* seconds, int64_t* pulled) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.n < 2 || !R.peer || which < 0 || which > 2 || reps < 1)
+      zp::fail(ZP_EINVAL, "bench_collective needs >= 2 ranks on the NVLink peer path, which in 0..2, reps >= 1");
+    R.configure(2);  // flat bf16 params/grads, fp32 shard accumulator
+    const int64_t S = R.shard();
+    auto once = [&] {
+      if (which == 0) {  // pull reduce-scatter: every peer's bf16 gradient shard summed in fp32
+        CK(zp::peer_rs_accumulate(R.pv, R.off(R.g16), R.shard_begin(), R.acc, S, true, ++R.epoch, R.ctas, R.st));
+      } else if (which == 1) {  // pull all-gather: every peer's bf16 parameter shard (scratch dst)
+        CK(zp::peer_all_gather(R.pv, R.off(R.p16 + R.shard_begin()), R.g16, S, ++R.epoch, R.ctas, R.st));
+      } else {  // copy-engine pulls of every peer's shard (the ZeRO-3 prefetch path)
+        for (int k = 1; k < R.n; ++k) {
+          const int j = (R.rank + k) % R.n;
+          CK(cudaMemcpyAsync(R.g16 + S * j, R.pv.base[j] + R.off(R.p16 + S * j), size_t(S) * 2,
+                             cudaMemcpyDeviceToDevice, R.st));
+        }
+      }
+    };
+    once();
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaStreamSynchronize(R.st));
+    R.agree(1, ncclMin);  // start together
+    CK(cudaEventRecord(e0, R.st));
+    for (int i = 0; i < reps; ++i) once();
+    CK(cudaEventRecord(e1, R.st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *seconds = double(ms) * 1e-3 / reps;
+    *pulled = int64_t(R.n - 1) * S * 2;
+    return ZP_OK;
+  });
 }
 
 int zp_runtime_keep_grads(zp_runtime* h, int32_t on) {

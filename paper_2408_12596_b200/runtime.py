@@ -61,6 +61,8 @@ _SIGS = {
     "zp_runtime_set_params": ([_P, _P], C.c_int),
     "zp_runtime_keep_grads": ([_P, C.c_int32], C.c_int),
     "zp_runtime_peer_collectives": ([_P, C.POINTER(C.c_int32)], C.c_int),
+    "zp_runtime_bench_collective": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)],
+                                    C.c_int),
     "zp_runtime_owned_ranges": ([_P, C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_tensor_info": ([_P, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)], C.c_int),
@@ -214,6 +216,13 @@ class Runtime:
         on = C.c_int32(0)
         _check(lib.zp_runtime_peer_collectives(self.h, C.byref(on)))
         return bool(on.value)
+
+    def bench_collective(self, which: int, reps: int = 10):
+        """NVLink microbenchmark (all ranks call it together): which 0 pull reduce-scatter,
+        1 pull all-gather, 2 copy-engine pulls. Returns (seconds per call, bytes pulled per call)."""
+        sec, pulled = C.c_double(), C.c_int64()
+        _check(lib.zp_runtime_bench_collective(self.h, which, reps, C.byref(sec), C.byref(pulled)))
+        return sec.value, pulled.value
 
     def get_state(self, kind: int):
         """kind 0 master, 1 m, 2 v, 3 summed grad. Returns (begin, end, float32 array)."""
