@@ -288,12 +288,10 @@ __global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __rest
       const uint4 qda = *reinterpret_cast<const uint4*>(da + 256 * j);
       const uint4 qxb = *reinterpret_cast<const uint4*>(xb + 256 * j);
       const uint4 qdb = *reinterpret_cast<const uint4*>(db + 256 * j);
-#ifdef ZP_LNB_PREFETCH
       if (dres) {  // the residual gradient is read in the second pass: start its HBM fetch now
         asm volatile("prefetch.global.L2 [%0];" ::"l"(dres + ra * h + lane * 8 + 256 * j));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(dres + rb * h + lane * 8 + 256 * j));
       }
-#endif
       float gg[8], xv[8], dv[8];
       unpack8(*reinterpret_cast<const uint4*>(g + lane * 8 + 256 * j), gg);
       unpack8(qxa, xv);
