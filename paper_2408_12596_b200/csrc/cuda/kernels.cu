@@ -158,6 +158,11 @@ __global__ void __launch_bounds__(kThreads) ln_fwd_k(const bf16* __restrict__ x,
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (kThreads / 32);
   for (int64_t r = blockIdx.x * int64_t(kThreads / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    if (r + warps < rows) {  // this warp's next row, toward L2
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (r + warps) * h + (c * 32 + lane) * 8));
+    }
     float v[NC][8];
     float s = 0.f;
 #pragma unroll
@@ -291,6 +296,13 @@ __global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __rest
       if (dres) {  // the residual gradient is read in the second pass: start its HBM fetch now
         asm volatile("prefetch.global.L2 [%0];" ::"l"(dres + ra * h + lane * 8 + 256 * j));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(dres + rb * h + lane * 8 + 256 * j));
+      }
+      if (ra + 2 * (kThreads / 32) + 1 < r1) {  // the warp's next two rows, toward L2
+        const int64_t rn = ra + 2 * (kThreads / 32);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + rn * h + lane * 8 + 256 * j));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(dy + rn * h + lane * 8 + 256 * j));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (rn + 1) * h + lane * 8 + 256 * j));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(dy + (rn + 1) * h + lane * 8 + 256 * j));
       }
       float gg[8], xv[8], dv[8];
       unpack8(*reinterpret_cast<const uint4*>(g + lane * 8 + 256 * j), gg);

@@ -6,7 +6,7 @@ for rep in 1 2; do
 for f in alt_lib/lib_*.so; do
   v=$(basename $f .so)_$rep
   cp $f paper_2408_12596_b200/lib/libzp.so
-  if [ $rep = 1 ]; then timeout 600 python -m pytest tests/test_attention_gpu.py -x -q > gpurun_out/abn/pt_$v.log 2>&1; echo "$v pytest rc=$? $(tail -1 gpurun_out/abn/pt_$v.log)"; fi
+  if [ $rep = 1 ]; then timeout 600 python -m pytest tests/test_attention_gpu.py tests/test_step_gpu.py -x -q > gpurun_out/abn/pt_$v.log 2>&1; echo "$v pytest rc=$? $(tail -1 gpurun_out/abn/pt_$v.log)"; fi
   ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/abn/l_$v.csv python tools/profile_step.py --b 64 > gpurun_out/abn/ncu_$v.log 2>&1
   python tools/launch_summary.py gpurun_out/abn/l_$v.csv "$v" > gpurun_out/abn/l_$v.md
   echo "== $v $(grep -E 'launches,' gpurun_out/abn/l_$v.md)"; grep -E "${ABN_GREP:-attn_fwd}" gpurun_out/abn/l_$v.md
