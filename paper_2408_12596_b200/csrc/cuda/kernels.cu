@@ -786,6 +786,7 @@ __global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_
   for (int k = 0; k < 8; ++k) a[k] = 0.f;
   if (c < N) {
     for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      if (r + 32 < r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(X + (r + 32) * ld + c));  // 4 rows ahead
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(X + r * ld + c), f);
 #pragma unroll
