@@ -13,5 +13,5 @@ print(round(d['value'],1), d['config']['plan'], 'gemm', round(d['roofline']['ach
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/f1/bench_ref.json 2> gpurun_out/f1/bench_ref.err; echo "ref rc=$?"; tail -c 400 gpurun_out/f1/bench_ref.json
 python tools/profile_step.py --b 64 > gpurun_out/f1/plain.log 2>&1 || { echo plain failed; exit 1; }
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/f1/launch.csv python tools/profile_step.py --b 64 > gpurun_out/f1/ncu.log 2>&1
-python tools/launch_summary.py gpurun_out/f1/launch.csv "v15 (b=64 micro-step, 132-SM budget)" > gpurun_out/f1/launch.md
+python tools/launch_summary.py gpurun_out/f1/launch.csv "v16 (b=64 micro-step, 132-SM budget)" > gpurun_out/f1/launch.md
 head -24 gpurun_out/f1/launch.md
