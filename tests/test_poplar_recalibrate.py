@@ -31,3 +31,18 @@ def test_recalibrate_keeps_idle_rank():
     out = poplar.recalibrate(prof, plan, [{"compute": 0.0}, {"compute": 0.1}])
     assert out["devices"][0]["samples"] == prof["devices"][0]["samples"]
     assert out["devices"][1]["samples"][3][1] == pytest.approx(0.066)
+
+
+def test_recalibrate_passes_compose():
+    """bench.py repeats the correction (--recalibrate-passes): a second pass whose measured
+    compute matches the corrected prediction leaves the profile unchanged, and two partial
+    corrections compose to the product of their ratios."""
+    prof = _profile()
+    plan = {"stage": 2, "gas": 2, "devices": [{"predicted_time": 0.100}, {"predicted_time": 0.200}]}
+    once = poplar.recalibrate(prof, plan, [{"compute": 0.105}, {"compute": 0.190}])
+    plan2 = {"stage": 2, "gas": 2, "devices": [{"predicted_time": 0.105}, {"predicted_time": 0.190}]}
+    twice = poplar.recalibrate(once, plan2, [{"compute": 0.105}, {"compute": 0.190}])
+    assert twice["devices"] == once["devices"]
+    third = poplar.recalibrate(once, plan2, [{"compute": 0.1155}, {"compute": 0.190}])
+    for (b, t0), (_, t2) in zip(prof["devices"][0]["samples"], third["devices"][0]["samples"]):
+        assert t2 == pytest.approx(t0 * 1.05 * 1.1)
