@@ -56,8 +56,16 @@ typedef struct zp_rank_timing {
   double wall;           /* first event to last event of the iteration on this rank */
   double loss_sum;       /* sum over this rank's tokens of CE / (B * seq) */
   int64_t micro_steps;   /* micro-steps with batch > 0 */
-  int32_t n_collectives;
-  double coll_times[512]; /* per-collective event durations, in issue order */
+  int32_t n_collectives; /* collectives issued in the iteration (every one, never truncated) */
+  int32_t coll_capacity; /* caller: entries available at coll_times (0 = do not record) */
+  double* coll_times;    /* caller-owned [coll_capacity]: per-collective event durations in issue
+                            order; the first min(n_collectives, coll_capacity) are filled and
+                            coll_truncated is set when the buffer was too small */
+  int32_t coll_truncated;
+  int32_t pad_;
+  double ag_fwd, ag_bwd, rs; /* sums of the ZeRO-3 forward / backward gathers and reduce-scatters */
+  double sync;           /* synchronisation-point collective time (Z0/1 all-reduce, Z2 gather, or the
+                            fused reduce-scatter + AdamW + all-gather kernel) */
 } zp_rank_timing;
 
 const char* zp_runtime_last_error(void);
@@ -114,6 +122,12 @@ int zp_runtime_peer_collectives(zp_runtime* rt, int32_t* on);
  * prefetch path). *seconds = mean device time per call over reps (CUDA events on the runtime
  * stream, after one warm-up call); *pulled = bytes this rank reads from its peers per call. */
 int zp_runtime_bench_collective(zp_runtime* rt, int32_t which, int32_t reps, double* seconds, int64_t* pulled);
+/* Measured alpha-beta link model for the planner's collective_time (reference comm.cpp:88-99:
+ * latency + volume / min(link_bandwidths)), collective over ranks: the stage's reduce-scatter
+ * path (NVLink pull kernel, or NCCL without peer access) timed on a 1 GiB bf16 buffer and on
+ * n*256 elements, max over ranks. *latency = small-buffer time (s); *bandwidth = buffer bytes /
+ * (large-buffer time - latency) (B/s), i.e. the reference's per-launch volume convention. */
+int zp_runtime_link_model(zp_runtime* rt, int32_t stage, int32_t reps, double* bandwidth, double* latency);
 /* Flat-layout ranges this rank owns, as (flat_begin, flat_end, shard_begin) triples: one range
  * at stages 0-2, one per parameter group (embedding, each layer, final LN) at stage 3, where the
  * shard buffers of zp_runtime_get_state are the concatenation of the owned slices. */

@@ -137,7 +137,7 @@ def rel_err(a, b):
 
 
 # ----------------------------------------------------------------------------- Llama family
-# RMSNorm (eps 1e-5), rotary Q/K (rotate-half, theta 1e4, head_dim 64), SwiGLU MLP whose fused
+# RMSNorm (eps 1e-5), rotary Q/K (rotate-half, theta 1e4, any even head_dim), SwiGLU MLP whose fused
 # gate/up weight interleaves 32-row blocks (rows r with r % 64 < 32 are gate rows), no biases,
 # untied LM head. Same global-batch loss normalisation as the GPT step.
 
@@ -154,18 +154,58 @@ def rms_bwd(dy, g, cache):
     return rs * (gd - xh * m2), (dy * xh).sum(0)
 
 
-def rope_tables(s, theta=10000.0):
-    j = np.arange(32, dtype=np.float64)
-    inv = theta ** (-2.0 * j / 64.0)
+def rope_tables(s, dh=64, theta=10000.0):
+    j = np.arange(dh // 2, dtype=np.float64)
+    inv = theta ** (-2.0 * j / dh)
     ang = np.arange(s, dtype=np.float64)[:, None] * inv[None, :]
     return np.cos(ang), np.sin(ang)
 
 
 def rope_apply(x, cos, sin, inverse=False):
-    """x: [b, H, s, 64]."""
+    """x: [..., s, dh], rotate-half pairing (i, i + dh/2)."""
     sn = -sin if inverse else sin
-    a, b = x[..., :32], x[..., 32:]
+    half = x.shape[-1] // 2
+    a, b = x[..., :half], x[..., half:]
     return np.concatenate([a * cos - b * sn, b * cos + a * sn], axis=-1)
+
+
+def causal_attention_fwd(q, k, v):
+    """Causal softmax attention per (sample, head), one head at a time so no [b, H, s, s] array is
+    ever held (the B200 kernel keeps scores on chip too). q, k, v: [b, H, s, dh].
+    Returns o [b, H, s, dh] and the row log-sum-exp [b, H, s] of the scaled scores."""
+    b, H, s, dh = q.shape
+    mask = np.triu(np.ones((s, s), dtype=bool), 1)
+    o = np.empty_like(q)
+    lse = np.empty((b, H, s))
+    for i in range(b):
+        for j in range(H):
+            S = (q[i, j] @ k[i, j].T) / np.sqrt(dh)
+            S[mask] = -np.inf
+            mx = S.max(-1, keepdims=True)
+            E = np.exp(S - mx)
+            l = E.sum(-1, keepdims=True)
+            o[i, j] = (E / l) @ v[i, j]
+            lse[i, j] = (mx + np.log(l))[:, 0]
+    return o, lse
+
+
+def causal_attention_bwd(q, k, v, o, lse, do):
+    """Gradients of causal_attention_fwd, recomputing P from the saved log-sum-exp."""
+    b, H, s, dh = q.shape
+    mask = np.triu(np.ones((s, s), dtype=bool), 1)
+    dq, dk, dv = np.empty_like(q), np.empty_like(k), np.empty_like(v)
+    for i in range(b):
+        for j in range(H):
+            S = (q[i, j] @ k[i, j].T) / np.sqrt(dh)
+            S[mask] = -np.inf
+            P = np.exp(S - lse[i, j][:, None])
+            dv[i, j] = P.T @ do[i, j]
+            dP = do[i, j] @ v[i, j].T
+            D = (do[i, j] * o[i, j]).sum(-1, keepdims=True)
+            dS = P * (dP - D) / np.sqrt(dh)
+            dq[i, j] = dS @ k[i, j]
+            dk[i, j] = dS.T @ q[i, j]
+    return dq, dk, dv
 
 
 def gu_split(w):
@@ -190,9 +230,8 @@ def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int,
     h = P["wte"].shape[1]
     dh = h // n_head
     T = b * s
-    cos, sin = rope_tables(s)
+    cos, sin = rope_tables(s, dh)
     x = P["wte"][inp.reshape(-1)].copy()
-    mask = np.triu(np.ones((s, s), dtype=bool), 1)
     caches = []
     heads = lambda m: m.reshape(b, s, n_head, dh).transpose(0, 2, 1, 3)  # noqa: E731
     for i in range(n_layer):
@@ -203,12 +242,8 @@ def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int,
         q = rope_apply(heads(qkv[:, :h]), cos, sin)
         k = rope_apply(heads(qkv[:, h:2 * h]), cos, sin)
         v = heads(qkv[:, 2 * h:])
-        S = (q @ k.transpose(0, 1, 3, 2)) / np.sqrt(dh)
-        S = np.where(mask, -np.inf, S)
-        S = S - S.max(-1, keepdims=True)
-        Pm = np.exp(S)
-        Pm /= Pm.sum(-1, keepdims=True)
-        o = (Pm @ v).transpose(0, 2, 1, 3).reshape(T, h)
+        oh, lse_a = causal_attention_fwd(q, k, v)
+        o = oh.transpose(0, 2, 1, 3).reshape(T, h)
         x_mid = x_in + o @ p("w_o").T
         m, c2 = rms_fwd(x_mid, p("ln2_g")[0])
         wg, wu = gu_split(p("w_gu"))
@@ -216,7 +251,7 @@ def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int,
         sg = 1.0 / (1.0 + np.exp(-ga))
         hh = ga * sg * ub
         x = x_mid + hh @ p("w_down").T
-        caches.append((x_in, a, c1, q, k, v, Pm, o, x_mid, m, c2, ga, ub, sg, hh))
+        caches.append((x_in, a, c1, q, k, v, (oh, lse_a), o, x_mid, m, c2, ga, ub, sg, hh))
     xf, cf = rms_fwd(x, P["lnf_g"][0])
     W = P["lm_head"][:vocab]
     logits = xf @ W.T
@@ -234,7 +269,7 @@ def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int,
     unheads = lambda m: m.transpose(0, 2, 1, 3).reshape(T, h)  # noqa: E731
     for i in reversed(range(n_layer)):
         p = lambda n: P[f"h{i}.{n}"]  # noqa: E731
-        x_in, a, c1, q, k, v, Pm, o, x_mid, m, c2, ga, ub, sg, hh = caches[i]
+        x_in, a, c1, q, k, v, (oh, lse_a), o, x_mid, m, c2, ga, ub, sg, hh = caches[i]
         G[f"h{i}.w_down"] = dx.T @ hh
         dhh = dx @ p("w_down")
         silu = ga * sg
@@ -247,11 +282,9 @@ def llama_loss_and_grads(P: dict, tokens: np.ndarray, n_layer: int, n_head: int,
         dx_mid = dx + d2
         G[f"h{i}.w_o"] = dx_mid.T @ o
         dO = heads(dx_mid @ p("w_o"))
-        dV = Pm.transpose(0, 1, 3, 2) @ dO
-        dP = dO @ v.transpose(0, 1, 3, 2)
-        dS = Pm * (dP - (Pm * dP).sum(-1, keepdims=True)) / np.sqrt(dh)
-        dQ = rope_apply(dS @ k, cos, sin, inverse=True)
-        dK = rope_apply(dS.transpose(0, 1, 3, 2) @ q, cos, sin, inverse=True)
+        dQr, dKr, dV = causal_attention_bwd(q, k, v, oh, lse_a, dO)
+        dQ = rope_apply(dQr, cos, sin, inverse=True)
+        dK = rope_apply(dKr, cos, sin, inverse=True)
         dqkv = np.concatenate([unheads(dQ), unheads(dK), unheads(dV)], axis=1)
         G[f"h{i}.w_qkv"] = dqkv.T @ a
         d1, G[f"h{i}.ln1_g"][0] = rms_bwd(dqkv @ p("w_qkv"), p("ln1_g")[0], c1)

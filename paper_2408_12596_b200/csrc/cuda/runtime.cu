@@ -206,7 +206,7 @@ struct Acts {
 };
 
 // ------------------------------------------------------------------ event timing
-enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4, kAgF = 5, kAgB = 6, kRs = 7 };
+enum SpanKind { kFwd = 0, kBwd = 1, kComm = 2, kOpt = 3, kWall = 4, kAgF = 5, kAgB = 6, kRs = 7, kSync = 8 };
 struct Span {
   int kind, start, end;
   bool nested;  // a collective issued inside a forward/backward span (ZeRO-3 gathers / scatters)
@@ -228,13 +228,19 @@ struct Timer {
     next = 0;
     spans.clear();
   }
+  // The pool grows on demand (event creation is host-only and does not synchronise), so a plan
+  // with many micro-steps or ZeRO-3 groups never runs out of events mid-iteration.
   int mark(cudaStream_t s) {
-    if (next >= int(ev.size())) fail(ZP_EINTERNAL, "event pool exhausted");
+    if (next >= int(ev.size())) {
+      const size_t old = ev.size();
+      ev.resize(std::max<size_t>(256, 2 * old));
+      for (size_t i = old; i < ev.size(); ++i) CK(cudaEventCreate(&ev[i]));
+    }
     CK(cudaEventRecord(ev[next], s));
     return next++;
   }
   void close(int kind, int start, cudaStream_t s) {
-    const bool coll = kind == kComm || kind == kAgF || kind == kAgB || kind == kRs;
+    const bool coll = kind == kComm || kind == kAgF || kind == kAgB || kind == kRs || kind == kSync;
     spans.push_back({kind, start, mark(s), coll && in_compute});
   }
 };
@@ -855,18 +861,18 @@ struct Runtime {
   void reduce_scatter_f32(const float* in, float* out) {
     const int s0 = tm.mark(st);
     NK(ncclReduceScatter(in, out, size_t(shard()), ncclFloat, ncclSum, comm, st));
-    tm.close(kComm, s0, st);
+    tm.close(kSync, s0, st);
   }
   void all_reduce_f32(float* buf, int64_t count) {
     const int s0 = tm.mark(st);
     NK(ncclAllReduce(buf, buf, size_t(count), ncclFloat, ncclSum, comm, st));
-    tm.close(kComm, s0, st);
+    tm.close(kSync, s0, st);
   }
   void all_gather_params() {
     if (n == 1) return;
     const int s0 = tm.mark(st);
     NK(ncclAllGather(p16 + shard() * rank, p16, size_t(shard()), ncclBfloat16, comm, st));
-    tm.close(kComm, s0, st);
+    tm.close(kSync, s0, st);
   }
 
   // Map every rank's arena and flag block (CUDA IPC handles exchanged over NCCL). All ranks
@@ -944,7 +950,7 @@ struct Runtime {
     const int s0 = tm.mark(st);
     CK(peer_rs_adam_ag(pv, off(src), f32, shard_begin(), a, p32, m32, v32, off(p16), gkeep, shard(), ap, ++epoch,
                        ctas, st));
-    tm.close(kComm, s0, st);
+    tm.close(kSync, s0, st);
   }
 
   AdamParams adam_params() {
@@ -1112,26 +1118,53 @@ struct Runtime {
     return p;
   }
 
+  // On the NVLink path the ZeRO-1/2 optimizer runs inside the fused reduce-scatter + AdamW +
+  // all-gather kernel, so a probe step has no separate optimizer span. The probe's optimizer time
+  // (the planner's tail, reference planner.cpp:335-338) is then one AdamW pass over the owned
+  // shard with lr 0 and beta1 = beta2 = 1: the same bytes and instructions, state unchanged
+  // (m' = m, v' = v, p' = p - 0).
+  double time_noop_adam() {
+    AdamParams a;
+    a.lr = 0.f;
+    a.beta1 = a.beta2 = 1.f;
+    a.eps = d.eps;
+    a.weight_decay = 0.f;
+    a.bc1 = a.bc2 = 1.f;
+    const int64_t L = state_len();
+    // a zero gradient keeps every product finite (acc is dead between iterations: the next one
+    // overwrites it on its first micro-step)
+    CK(cudaMemsetAsync(acc, 0, size_t(L) * 4, st));
+    const int s0 = tm.mark(st);
+    adam_update(p32, m32, v32, p16 + shard_begin(), nullptr, nullptr, acc, L, a, ctas, st);
+    const int s1 = tm.mark(st);
+    CK(cudaEventSynchronize(tm.ev[s1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, tm.ev[s0], tm.ev[s1]));
+    return double(ms) * 1e-3;
+  }
+
   int run_step(int64_t b, int stg, int64_t global_batch, zp_step_trace* out) {
     configure(stg);
     if (b > tokens_count) load_tokens(nullptr, 0, b, uint64_t(adam_t), false);
     int oom = -1;
     const int64_t active = iterate({b}, global_batch > 0 ? global_batch : std::max<int64_t>(b, 1), &oom);
-    zp_rank_timing t;
+    zp_rank_timing t{};
     collect(&t, active, 1);
     std::memset(out, 0, sizeof(*out));
     out->forward_compute = t.forward;
     out->backward_compute = t.backward;
     out->optimizer_step = t.optimizer;
+    if (peer && (stg == 1 || stg == 2)) out->optimizer_step = time_noop_adam();
+    // StepTrace fields per stage (reference hardware.cpp:171-185)
     if (stg <= 1) {
       out->allreduce = t.comm;
     } else if (stg == 2) {
-      out->reduce_scatter = t.n_collectives > 0 ? t.coll_times[0] : 0.0;
-      out->allreduce = t.n_collectives > 1 ? t.coll_times[1] : 0.0;
+      out->reduce_scatter = t.comm - t.sync;  // micro-step reduce-scatter
+      out->allreduce = t.sync;                // synchronisation-point gather (or the fused kernel)
     } else {
-      out->fwd_allgather = t_agf;
-      out->bwd_allgather = t_agb;
-      out->reduce_scatter = t_rs;
+      out->fwd_allgather = t.ag_fwd;
+      out->bwd_allgather = t.ag_bwd;
+      out->reduce_scatter = t.rs;
     }
     return oom >= 0 ? ZP_OOM : ZP_OK;
   }
@@ -1148,8 +1181,20 @@ struct Runtime {
       const int64_t g = (dv.gmbs + dv.b - 1) / dv.b;
       for (int64_t k = 0; k < g; ++k) steps.push_back(k + 1 < g ? dv.b : dv.lbs);
     }
-    if (int64_t(steps.size()) > kMaxSteps) fail(ZP_EINVAL, "too many micro-steps");
-    if (dv.gmbs > tokens_count) fail(ZP_EINVAL, "token pool holds fewer samples than the plan assigns");
+    // Validate before the first collective and agree on the outcome, so a rank that rejects the
+    // plan never leaves its peers blocked inside a collective.
+    int bad = 0;
+    for (int r = 0; r < plan->n; ++r) {
+      const zp_device_alloc& q = plan->devices[r];
+      const int64_t ns = stg >= 2 ? plan->gas : (q.gmbs > 0 && q.b > 0 ? (q.gmbs + q.b - 1) / q.b : 0);
+      if (ns > kMaxSteps || (q.gmbs > 0 && q.b < 1)) bad = 1;
+    }
+    const int local_bad = dv.gmbs > tokens_count ? 2 : 0;
+    const int64_t verdict = n > 1 ? agree(std::max(bad, local_bad), ncclMax) : std::max(bad, local_bad);
+    if (verdict == 1) fail(ZP_EINVAL, "plan has too many micro-steps (> 4096) or a zero step batch");
+    if (verdict == 2)
+      fail(ZP_EINVAL, local_bad ? "token pool holds fewer samples than the plan assigns"
+                                : "a peer rank's token pool holds fewer samples than the plan assigns");
     int oom = -1;
     const int64_t active = iterate(steps, plan->gbs, &oom);
     if (oom >= 0) {
@@ -1157,7 +1202,7 @@ struct Runtime {
       fail(ZP_EINTERNAL, "plan exceeds device capacity: rank " + std::to_string(rank) +
                              " OOMs at micro-step " + std::to_string(oom));
     }
-    zp_rank_timing t;
+    zp_rank_timing t{};
     collect(timing ? timing : &t, active, steps.size());
   }
 
@@ -1252,11 +1297,13 @@ struct Runtime {
     fail(ZP_EINFEASIBLE, "model too large: a single batch does not fit on every rank");
   }
 
-  double t_agf = 0, t_agb = 0, t_rs = 0;  // ZeRO-3 split of the last collect()
   void collect(zp_rank_timing* t, int64_t active, size_t nsteps) {
     CK(cudaStreamSynchronize(st));
+    double* buf = t->coll_times;
+    const int32_t cap = buf ? t->coll_capacity : 0;
     std::memset(t, 0, sizeof(*t));
-    t_agf = t_agb = t_rs = 0;
+    t->coll_times = buf;
+    t->coll_capacity = cap;
     for (const Span& sp : tm.spans) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, tm.ev[sp.start], tm.ev[sp.end]));
@@ -1268,6 +1315,7 @@ struct Runtime {
         case kAgF:
         case kAgB:
         case kRs:
+        case kSync:
           // Collectives nested in a forward/backward span are not the rank's own compute: on a
           // fast rank they include the wait for the slowest rank (reference profiler.cpp:25-47
           // subtracts them; with lockstep ZeRO-3 they would otherwise hide the heterogeneity).
@@ -1278,10 +1326,15 @@ struct Runtime {
               t->backward -= sec;
           }
           t->comm += sec;
-          if (t->n_collectives < 512) t->coll_times[t->n_collectives++] = sec;
-          if (sp.kind == kAgF) t_agf += sec;
-          if (sp.kind == kAgB) t_agb += sec;
-          if (sp.kind == kRs) t_rs += sec;
+          if (t->n_collectives < cap)
+            t->coll_times[t->n_collectives] = sec;
+          else if (cap > 0)
+            t->coll_truncated = 1;
+          ++t->n_collectives;
+          if (sp.kind == kAgF) t->ag_fwd += sec;
+          if (sp.kind == kAgB) t->ag_bwd += sec;
+          if (sp.kind == kRs) t->rs += sec;
+          if (sp.kind == kSync) t->sync += sec;
           break;
         case kOpt: t->optimizer += sec; break;
         case kWall: t->wall = sec; break;
@@ -1561,6 +1614,57 @@ int zp_runtime_bench_collective(zp_runtime* h, int32_t which, int32_t reps, doub
     cudaEventDestroy(e1);
     *seconds = double(ms) * 1e-3 / reps;
     *pulled = int64_t(R.n - 1) * S * 2;
+    return ZP_OK;
+  });
+}
+
+int zp_runtime_link_model(zp_runtime* h, int32_t stage, int32_t reps, double* bandwidth, double* latency) {
+  return guarded([&] {
+    zp::Runtime& R = h->rt;
+    if (R.n < 2 || reps < 1) zp::fail(ZP_EINVAL, "link_model needs >= 2 ranks and reps >= 1");
+    R.configure(stage);
+    // Scratch from the activation region of the arena (mapped by every peer at the same offset):
+    // a "model" of V bf16 elements (V/n per rank) reduce-scattered into an fp32 shard.
+    const int64_t unit = int64_t(R.n) * 256;
+    const int64_t big = std::max<int64_t>(unit, (int64_t(1) << 29) / unit * unit);  // 1 GiB of bf16
+    R.arena.used = R.resident_mark;
+    zp::bf16* src = R.arena.take_n<zp::bf16>(big);
+    float* dst = R.arena.take_n<float>(big / R.n);
+    if (!src || !dst) zp::fail(ZP_OOM, "link_model scratch does not fit above the resident state");
+    CK(cudaMemsetAsync(src, 0, size_t(big) * 2, R.st));
+    auto once = [&](int64_t V) {
+      const int64_t S = V / R.n;
+      if (R.peer)
+        CK(zp::peer_rs_accumulate(R.pv, R.off(src), S * R.rank, dst, S, true, ++R.epoch, R.ctas, R.st));
+      else
+        NK(ncclReduceScatter(src, dst, size_t(S), ncclBfloat16, ncclSum, R.comm, R.st));
+    };
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto timed = [&](int64_t V) {
+      once(V);
+      CK(cudaStreamSynchronize(R.st));
+      R.agree(1, ncclMin);  // start together
+      CK(cudaEventRecord(e0, R.st));
+      for (int i = 0; i < reps; ++i) once(V);
+      CK(cudaEventRecord(e1, R.st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      // the slowest rank's view (the reference's collective time is uniform across devices)
+      const int64_t us = R.agree(int64_t(double(ms) * 1e3 / reps * 1e3), ncclMax);  // ns
+      return double(us) * 1e-9;
+    };
+    const double t_small = timed(unit);
+    const double t_big = timed(big);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    R.arena.used = R.resident_mark;
+    // reference collective_time = latency + volume / bandwidth with volume = the whole buffer's
+    // bytes (comm.cpp:88-99: one launch moves param_count * bytes_per_param)
+    *latency = t_small;
+    *bandwidth = double(big) * 2.0 / std::max(t_big - t_small, 1e-9);
     return ZP_OK;
   });
 }

@@ -15,9 +15,11 @@ from typing import Optional, Sequence
 from . import host
 from .host import ClusterSpec, Device, ModelSpec
 
-# NVLink 5 per-direction bandwidth measured on this pool (peer copy, B200_PROFILING.md) and a
-# typical NCCL launch latency; they parameterise the planner's alpha-beta collective model
-# (reference comm.cpp:88-99), which on NVSwitch is uniform across ranks.
+# Fallback link model when none was measured (one rank, or a caller that skips the measurement):
+# NVLink 5 per-direction peer-copy bandwidth on this pool and a typical collective launch latency.
+# bench.py measures both per run (Runtime.link_model: the stage's reduce-scatter path timed at two
+# sizes, max over ranks) and passes them in; they parameterise the planner's alpha-beta collective
+# model (reference comm.cpp:88-99), which on NVSwitch is uniform across ranks.
 NVLINK_BPS = 770e9
 NCCL_ALPHA = 25e-6
 
@@ -31,9 +33,12 @@ def planner_inputs(rt, n: int, link_bw: float = NVLINK_BPS, alpha: float = NCCL_
     return model, cluster
 
 
-def poplar_plan(rt, profile: dict, gbs: int, stage: int, n: int, uniform: bool = False) -> dict:
-    api = host.product()
-    model, cluster = planner_inputs(rt, n)
+def poplar_plan(rt, profile: dict, gbs: int, stage: int, n: int, uniform: bool = False,
+                link=None, api=None) -> dict:
+    """Alg. 2 through the product planner (or `api`, e.g. the compiled reference for parity).
+    link = (bandwidth B/s, latency s) of the measured alpha-beta model."""
+    api = api or host.product()
+    model, cluster = planner_inputs(rt, n, *(link or ()))
     if not uniform:
         return api.plan(gbs, profile, stage, model, cluster)
     comm = api.make_comm_profile(model, stage, cluster)
@@ -71,8 +76,10 @@ def iteration_report(timings: Sequence[dict], gbs: int) -> dict:
     (simulator.cpp:104-114). Collective k costs every rank min_j t_j(k) (the last rank to
     arrive does not wait); anything above that on a faster rank is synchronisation idle.
     busy_i = compute_i + sum_k min_j t_j(k) + optimizer_i; T = max_i wall_i; idle_i = T - busy_i."""
-    n = len(timings)
-    ncoll = min(len(t["coll_times"]) for t in timings)
+    counts = {len(t["coll_times"]) for t in timings}
+    if len(counts) != 1:
+        raise ValueError(f"ranks issued different collective counts {sorted(counts)}")
+    ncoll = counts.pop()
     floor = sum(min(t["coll_times"][k] for t in timings) for k in range(ncoll))
     T = max(t["wall"] for t in timings)
     busy = [t["compute"] + floor + t["optimizer"] for t in timings]

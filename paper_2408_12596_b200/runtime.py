@@ -7,12 +7,12 @@ The profiler / planner / executor on top of it live in `poplar.py`.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
 
 from . import _lib
+from .models import GPT, MODELS  # noqa: F401  (re-exported)
 from .host import (Plan, Probe, Profile, StepTrace, plan_from_py, profile_to_py, ZeroplanError, _ERR, OK, OOM)
 
 lib = _lib.lib
@@ -31,16 +31,31 @@ class RuntimeDesc(C.Structure):
 
 
 class RankTiming(C.Structure):
+    """zp_rank_timing (include/zp_runtime.h). The per-collective durations go to a caller-owned
+    buffer; `n_collectives` always counts every collective, and `to_py` refuses a truncated list
+    (the idle metric would silently undercount busy time)."""
     _fields_ = [("compute", C.c_double), ("forward", C.c_double), ("backward", C.c_double),
                 ("comm", C.c_double), ("optimizer", C.c_double), ("wall", C.c_double),
                 ("loss_sum", C.c_double), ("micro_steps", C.c_int64), ("n_collectives", C.c_int32),
-                ("coll_times", C.c_double * 512)]
+                ("coll_capacity", C.c_int32), ("coll_times", C.POINTER(C.c_double)),
+                ("coll_truncated", C.c_int32), ("pad_", C.c_int32),
+                ("ag_fwd", C.c_double), ("ag_bwd", C.c_double), ("rs", C.c_double), ("sync", C.c_double)]
+
+    def __init__(self, capacity: int = 1 << 16):
+        super().__init__()
+        self._buf = (C.c_double * capacity)()
+        self.coll_times = C.cast(self._buf, C.POINTER(C.c_double))
+        self.coll_capacity = capacity
 
     def to_py(self) -> dict:
+        if self.coll_truncated or self.n_collectives > self.coll_capacity:
+            raise ZeroplanError(f"{self.n_collectives} collectives exceed the timing buffer "
+                                f"({self.coll_capacity}); pass a larger RankTiming(capacity)")
         return {"compute": self.compute, "forward": self.forward, "backward": self.backward,
                 "comm": self.comm, "optimizer": self.optimizer, "wall": self.wall,
                 "loss_sum": self.loss_sum, "micro_steps": self.micro_steps,
-                "coll_times": list(self.coll_times[:self.n_collectives])}
+                "ag_fwd": self.ag_fwd, "ag_bwd": self.ag_bwd, "rs": self.rs, "sync": self.sync,
+                "coll_times": list(self._buf[:self.n_collectives])}
 
 
 _P = C.c_void_p
@@ -63,6 +78,7 @@ _SIGS = {
     "zp_runtime_peer_collectives": ([_P, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_bench_collective": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)],
                                     C.c_int),
+    "zp_runtime_link_model": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "zp_runtime_owned_ranges": ([_P, C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_tensor_info": ([_P, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                 C.POINTER(C.c_int64)], C.c_int),
@@ -88,40 +104,8 @@ def _check(rc, allow_oom=False):
     raise _ERR.get(rc, ZeroplanError)(msg or f"zp runtime error {rc}")
 
 
-@dataclass
-class GPT:
-    n_layer: int
-    d_model: int
-    n_head: int
-    vocab: int
-    seq_len: int
-    d_ff: int = 0
-    arch: int = 0  # 0 = GPT-2 family, 1 = Llama family
-
-    def __post_init__(self):
-        if not self.d_ff:
-            self.d_ff = 4 * self.d_model
-
-    def to_c(self) -> GptConfig:
-        return GptConfig(self.n_layer, self.d_model, self.n_head, self.d_ff, self.vocab, self.seq_len, self.arch)
-
-    def flops_per_sample(self) -> float:
-        """Training FLOPs of one sample: 6 * N_matmul * s + 12 * L * h * s^2 (dense attention
-        accounting)."""
-        h, f, L, s = self.d_model, self.d_ff, self.n_layer, self.seq_len
-        mlp = 3 * h * f if self.arch == 1 else 2 * h * f
-        n_mm = L * (4 * h * h + mlp) + self.vocab * h
-        return 6.0 * n_mm * s + 12.0 * L * h * s * s
-
-
-MODELS = {
-    "gpt-tiny": GPT(4, 256, 4, 8192, 256, 1024),
-    "gpt2-small": GPT(12, 768, 12, 50257, 1024),
-    "gpt2-medium": GPT(24, 1024, 16, 50257, 1024),
-    # Llama-style configs of BASELINE.json (head_dim 64: 32 heads at h=2048, 64 heads at h=4096)
-    "llama-1.3b": GPT(24, 2048, 32, 32000, 2048, 5504, arch=1),
-    "llama-7b": GPT(32, 4096, 64, 32000, 4096, 11008, arch=1),
-}
+def gpt_config_c(m: GPT) -> GptConfig:
+    return GptConfig(m.n_layer, m.d_model, m.n_head, m.d_ff, m.vocab, m.seq_len, m.arch)
 
 
 def nccl_unique_id() -> bytes:
@@ -142,7 +126,7 @@ class Runtime:
             for i, b in enumerate(nccl_id):
                 d.nccl_id[i] = b
         d.sm_budget, d.hbm_cap_bytes = sm_budget, int(hbm_cap_bytes)
-        d.model = model.to_c()
+        d.model = gpt_config_c(model)
         d.seed = seed
         d.lr, d.beta1, d.beta2, d.eps, d.weight_decay = lr, betas[0], betas[1], eps, weight_decay
         self.desc = d
@@ -223,6 +207,13 @@ class Runtime:
         sec, pulled = C.c_double(), C.c_int64()
         _check(lib.zp_runtime_bench_collective(self.h, which, reps, C.byref(sec), C.byref(pulled)))
         return sec.value, pulled.value
+
+    def link_model(self, stage: int, reps: int = 10):
+        """Measured (bandwidth B/s, latency s) of the stage's reduce-scatter path, collective over
+        ranks (zp_runtime_link_model): the alpha-beta inputs of the planner's collective_time."""
+        bw, lat = C.c_double(), C.c_double()
+        _check(lib.zp_runtime_link_model(self.h, stage, reps, C.byref(bw), C.byref(lat)))
+        return bw.value, lat.value
 
     def get_state(self, kind: int):
         """kind 0 master, 1 m, 2 v, 3 summed grad. Returns (begin, end, float32 array)."""

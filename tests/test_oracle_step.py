@@ -84,12 +84,13 @@ def torch_llama(P, tokens, n_layer, n_head, vocab, B):
     inp, tgt = tok[:, :s], tok[:, 1:]
     h = T["wte"].shape[1]
     dh = h // n_head
-    j = torch.arange(32, dtype=torch.float64)
-    ang = torch.arange(s, dtype=torch.float64)[:, None] * (10000.0 ** (-2.0 * j / 64.0))[None]
+    half = dh // 2
+    j = torch.arange(half, dtype=torch.float64)
+    ang = torch.arange(s, dtype=torch.float64)[:, None] * (10000.0 ** (-2.0 * j / dh))[None]
     cos, sin = torch.cos(ang), torch.sin(ang)
 
     def rope(x):
-        a, b_ = x[..., :32], x[..., 32:]
+        a, b_ = x[..., :half], x[..., half:]
         return torch.cat([a * cos - b_ * sin, b_ * cos + a * sin], -1)
 
     def rms(x, g):
@@ -115,9 +116,10 @@ def torch_llama(P, tokens, n_layer, n_head, vocab, B):
     return loss.item(), {k: v.grad.numpy() for k, v in T.items()}
 
 
-def test_llama_oracle_matches_autograd():
+@pytest.mark.parametrize("H", [2, 1])  # head_dim 64 and 128
+def test_llama_oracle_matches_autograd(H):
     rng = np.random.default_rng(4)
-    L, h, H, ff, V, Vp, s = 2, 128, 2, 64, 50, 64, 16
+    L, h, ff, V, Vp, s = 2, 128, 64, 50, 64, 16
     P = {"wte": rng.normal(0, 0.1, (Vp, h)), "lnf_g": 1 + rng.normal(0, 0.1, (1, h)),
          "lm_head": rng.normal(0, 0.1, (Vp, h))}
     for i in range(L):

@@ -16,7 +16,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2408_12596_b200 import poplar, spec as specmod  # noqa: E402
-from paper_2408_12596_b200.runtime import MODELS, Runtime, nccl_unique_id  # noqa: E402
+from paper_2408_12596_b200.models import MODELS  # noqa: E402
+from paper_2408_12596_b200.runtime import Runtime, nccl_unique_id  # noqa: E402
 
 
 def main():
