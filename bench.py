@@ -372,8 +372,10 @@ def main():
     rt = Runtime(model, rank=rank, world_size=world, device=local, nccl_id=nid, sm_budget=tier,
                  hbm_cap_bytes=int(cap_gib * (1 << 30)), seed=0, lr=1e-4)
 
-    # Measured alpha-beta link model of the stage's collectives (reference comm.cpp:88-99)
-    link = rt.link_model(stage) if world > 1 else None
+    # Measured alpha-beta link model of the stage's collectives (reference comm.cpp:88-99). One
+    # rank launches no collectives: latency 0 and infinite bandwidth make collective_time 0 in the
+    # reference's own formula (validate() only requires bandwidth > 0).
+    link = rt.link_model(stage) if world > 1 else (float("inf"), 0.0)
 
     # Poplar: Alg. 1 on the devices, Alg. 2 on the host (bit-exact planner)
     t0 = time.perf_counter()
@@ -532,7 +534,7 @@ def main():
                        "mbs": [d["mbs"] for d in profile["devices"]],
                        "link_model": ({"bandwidth_GBps": link[0] / 1e9, "latency_us": link[1] * 1e6,
                                        "source": "measured (zp_runtime_link_model, max over ranks)"}
-                                      if link else "n/a (one rank: no collectives)"),
+                                      if world > 1 else "one rank: no collectives (latency 0, bandwidth inf)"),
                        "profile_seconds": t_profile, "parallelism": f"zero{stage}-dp{world}",
                        "collectives": (("nvlink-peer (pull RS/AG; fused RS+AdamW+AG at sync)" if stage in (1, 2) else "nvlink-peer (pull RS, copy-engine AG prefetch)" if stage == 3 else "nccl (all-reduce)") if rt.peer_collectives() else "nccl") if world > 1 else "none",
                        "l2": "inputs larger than L2 (per-step activations are tens of GB)"},

@@ -58,6 +58,36 @@ int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const f
                      float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t max_ctas,
                      void* stream);
 
+/* ---- NVLink peer-memory collectives (csrc/cuda/peer.cu), drivable on ONE device for parity.
+ * A peer group is n "rank arenas" given as n base pointers (any device memory the calling
+ * process can address: regions of one allocation on one GPU, or peer-mapped arenas of n GPUs)
+ * plus n flag blocks the group allocates (zeroed). Offsets are byte offsets from each base, the
+ * same for every rank, exactly as the runtime uses them. The kernels synchronise through
+ * epoch-stamped flags, so the n rank instances of one call must run CONCURRENTLY (one stream per
+ * rank, `ctas` small enough that all instances are co-resident); epochs must increase by one per
+ * call. Bounded spin: an instance whose peers never arrive traps after 20 s instead of hanging.
+ * Reference counterpart: none (the reference models these collectives as
+ * collective_time(param_count * bytes_per_param), proj/core/src/comm.cpp:88-99). */
+typedef struct zp_peer_group zp_peer_group;
+typedef struct zp_adam_params {
+  float lr, beta1, beta2, eps, weight_decay;
+  float bc1, bc2; /* 1 - beta^t */
+} zp_adam_params;
+int zp_peer_group_create(int32_t n, void* const* bases, zp_peer_group** out);
+int zp_peer_group_destroy(zp_peer_group* g);
+/* acc[i] = (overwrite ? 0 : acc[i]) + sum_{j=0..n-1} bf16 src_j[shard_off + i] (fp32, rank order) */
+int zp_peer_rs_accumulate(zp_peer_group* g, int32_t rank, int64_t src_off, int64_t shard_off, float* acc,
+                          int64_t len, int32_t overwrite, uint32_t epoch, int32_t ctas, void* stream);
+/* g = (acc ? acc : 0) + sum_j src_j[shard_off + i] (bf16, or fp32 when src_f32); AdamW on
+ * (p32, m, v); bf16(p32) pushed to element shard_off + i of every rank's p16 (byte offset p16_off);
+ * gout (optional) receives g. */
+int zp_peer_rs_adam_ag(zp_peer_group* g, int32_t rank, int64_t src_off, int32_t src_f32, int64_t shard_off,
+                       const float* acc, float* p32, float* m, float* v, int64_t p16_off, float* gout,
+                       int64_t len, const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream);
+/* dst[j*len + e] = bf16 src_j[e] (byte offset shard_src_off in every arena), every rank j */
+int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_src_off, void* dst, int64_t len,
+                       uint32_t epoch, int32_t ctas, void* stream);
+
 /* Number of kernels launched by this library since load (all entry points). */
 int64_t zp_launch_count(void);
 

@@ -3,6 +3,7 @@
 #include "attention.h"
 #include "gemm.h"
 #include "kernels.h"
+#include "peer.h"
 
 extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
   if (!d) return 1;
@@ -41,4 +42,68 @@ extern "C" int zp_attention_bwd(const void* qkv, const void* out, const void* do
                                           static_cast<zp::bf16*>(dqkv), batch, seq, heads, max_ctas,
                                           static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : 5;
+}
+
+// ---- peer-memory collectives on caller-given arenas (include/zp_kernels.h)
+struct zp_peer_group {
+  zp::PeerView pv;  // rank is set per call
+  zp::PeerFlags* flags = nullptr;
+};
+
+extern "C" int zp_peer_group_create(int32_t n, void* const* bases, zp_peer_group** out) {
+  if (!out || !bases || n < 1 || n > zp::kMaxPeers) return 1;
+  auto* g = new zp_peer_group();
+  if (cudaMalloc(&g->flags, sizeof(zp::PeerFlags) * n) != cudaSuccess ||
+      cudaMemset(g->flags, 0, sizeof(zp::PeerFlags) * n) != cudaSuccess) {
+    delete g;
+    return 5;
+  }
+  g->pv.n = n;
+  for (int j = 0; j < n; ++j) {
+    g->pv.base[j] = static_cast<char*>(bases[j]);
+    g->pv.flags[j] = g->flags + j;
+  }
+  *out = g;
+  return 0;
+}
+
+extern "C" int zp_peer_group_destroy(zp_peer_group* g) {
+  if (!g) return 0;
+  cudaFree(g->flags);
+  delete g;
+  return 0;
+}
+
+static zp::PeerView view_of(const zp_peer_group* g, int rank) {
+  zp::PeerView v = g->pv;
+  v.rank = rank;
+  return v;
+}
+
+extern "C" int zp_peer_rs_accumulate(zp_peer_group* g, int32_t rank, int64_t src_off, int64_t shard_off, float* acc,
+                                     int64_t len, int32_t overwrite, uint32_t epoch, int32_t ctas, void* stream) {
+  if (!g || rank < 0 || rank >= g->pv.n) return 1;
+  const cudaError_t e = zp::peer_rs_accumulate(view_of(g, rank), src_off, shard_off, acc, len, overwrite != 0, epoch,
+                                               ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+}
+
+extern "C" int zp_peer_rs_adam_ag(zp_peer_group* g, int32_t rank, int64_t src_off, int32_t src_f32, int64_t shard_off,
+                                  const float* acc, float* p32, float* m, float* v, int64_t p16_off, float* gout,
+                                  int64_t len, const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream) {
+  if (!g || !ap || rank < 0 || rank >= g->pv.n) return 1;
+  zp::AdamParams a;
+  a.lr = ap->lr; a.beta1 = ap->beta1; a.beta2 = ap->beta2; a.eps = ap->eps; a.weight_decay = ap->weight_decay;
+  a.bc1 = ap->bc1; a.bc2 = ap->bc2;
+  const cudaError_t e = zp::peer_rs_adam_ag(view_of(g, rank), src_off, src_f32 != 0, shard_off, acc, p32, m, v,
+                                            p16_off, gout, len, a, epoch, ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+}
+
+extern "C" int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_src_off, void* dst, int64_t len,
+                                  uint32_t epoch, int32_t ctas, void* stream) {
+  if (!g || rank < 0 || rank >= g->pv.n) return 1;
+  const cudaError_t e = zp::peer_all_gather(view_of(g, rank), shard_src_off, static_cast<zp::bf16*>(dst), len, epoch,
+                                            ctas, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
 }

@@ -10,9 +10,10 @@ pytestmark = pytest.mark.gpu
 
 
 def ref_attention(qkv, b, s, H):
-    h = H * 64
-    q, k, v = (qkv[:, j * h:(j + 1) * h].float().view(b, s, H, 64).transpose(1, 2) for j in range(3))
-    S = (q @ k.transpose(-1, -2)) / 8.0
+    h = qkv.shape[1] // 3
+    d = h // H
+    q, k, v = (qkv[:, j * h:(j + 1) * h].float().view(b, s, H, d).transpose(1, 2) for j in range(3))
+    S = (q @ k.transpose(-1, -2)) / math.sqrt(d)
     S = S.masked_fill(torch.triu(torch.ones(s, s, dtype=torch.bool, device=qkv.device), 1), float("-inf"))
     lse = torch.logsumexp(S, -1)
     o = torch.softmax(S, -1) @ v
@@ -25,9 +26,13 @@ def relerr(a, b):
 
 @pytest.mark.parametrize("b,s,H,ctas", [(1, 128, 1, 0), (2, 256, 2, 0), (2, 1024, 12, 0), (3, 512, 4, 37)])
 def test_attention_fwd_bwd(cuda, b, s, H, ctas):
+    check_attention(cuda, b, s, H, ctas)
+
+
+def check_attention(cuda, b, s, H, ctas, d=64):
     from paper_2408_12596_b200 import _lib
     L = _lib.lib
-    h = H * 64
+    h = H * d
     T = b * s
     g = torch.Generator(device="cpu").manual_seed(b * 1000 + s + H)
     qkv = torch.randn(T, 3 * h, generator=g).to(torch.bfloat16).to(cuda)
