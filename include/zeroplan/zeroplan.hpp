@@ -6,7 +6,9 @@
 // `run_step` / `memory_probe` seam (reference hardware.hpp:111-120):
 //   * ClusterGroundTruth  — the reference's latent closed-form device model, kept as the
 //                           test double that lets the host stack be parity-checked on CPU;
-//   * zp::DeviceRuntime   — real sm_100a execution (csrc/cuda), see include/zp_runtime.h.
+//   * the B200 runtime    — real sm_100a execution (csrc/cuda) behind the C ABI of
+//                           include/zp_runtime.h; integration/hardware_b200.{hpp,cpp} binds it to
+//                           the reference's own run_step / memory_probe signatures.
 // Planner arithmetic (spline, curves, Alg. 2) reproduces the reference bit-for-bit:
 // every floating-point operation keeps the reference's order.
 #ifndef ZEROPLAN_B200_ZEROPLAN_HPP_

@@ -91,12 +91,14 @@ def build(verbose: bool = False) -> str:
         for o in outs:
             if o.strip():
                 print(o)
-    if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+    emap = os.path.join(CSRC, "exports.map")
+    if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs + [emap]):
         nccl = _nccl_libdir()
         nccl_flags = ["-L", nccl, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl] if nccl else ["-lnccl"]
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + nccl_flags + [
             "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart",
-            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64"), "-Xlinker", "-Bsymbolic"]
+            "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64"), "-Xlinker", "-Bsymbolic",
+            "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
         _compile(cmd)
     return LIB
 

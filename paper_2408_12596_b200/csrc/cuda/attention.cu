@@ -964,12 +964,11 @@ int device_sms() {
 cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
                           int ctas, cudaStream_t s) {
   if (seq % kT || batch < 1) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          FwdSmem::kBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   CUtensorMap m;
   const int h = heads * kD;
@@ -986,12 +985,11 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
 cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
                           float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s) {
   if (seq % kT || batch < 1) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          BwdSmem::kBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int h = heads * kD;
   const int64_t T = batch * seq;

@@ -726,8 +726,8 @@ template <int BN, int A_MN, int B_MN, int CG>
 cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   using C = Cfg<BN, CG>;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  if (first_on_device(attr_set)) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e != cudaSuccess) return e;
@@ -735,7 +735,6 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
       (void)e;
     }
-    attr_set = true;
   }
   CUtensorMap ma, mb, mc;
   const bool ok_a = A_MN ? make_map(&ma, a.a, a.M, a.K, a.nb1, a.nb2, 64)

@@ -7,6 +7,8 @@
 #include <cstdlib>
 
 #include "kernels.h"
+
+#include <mutex>
 #include "ptx.cuh"
 
 namespace zp {
@@ -1048,18 +1050,32 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
                                                                           rows, h); note_launch();
 }
 void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s) {
-  // per-process cos/sin table for the largest sequence seen (one process drives one GPU)
-  static float2* tab = nullptr;
-  static int tab_seq = 0;
-  static float tab_theta = 0.f;
-  if (seq > tab_seq || theta != tab_theta) {
-    if (tab) cudaFree(tab);
-    tab = nullptr;
-    if (cudaMalloc(&tab, size_t(seq) * 32 * sizeof(float2)) != cudaSuccess) return;
-    rope_table_k<<<(seq * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(tab, seq, std::log(double(theta)));
-    note_launch();
-    tab_seq = seq;
-    tab_theta = theta;
+  // per-device cos/sin table for the largest sequence seen on that device (a process may drive
+  // several GPUs, one host thread each)
+  struct Table {
+    float2* tab = nullptr;
+    int seq = 0;
+    float theta = 0.f;
+  };
+  static Table tables[64];
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  float2* tab = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    Table& t = tables[dev & 63];
+    if (seq > t.seq || theta != t.theta) {
+      if (t.tab) cudaFree(t.tab);
+      t.tab = nullptr;
+      t.seq = 0;
+      if (cudaMalloc(&t.tab, size_t(seq) * 32 * sizeof(float2)) != cudaSuccess) return;
+      rope_table_k<<<(seq * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(t.tab, seq, std::log(double(theta)));
+      note_launch();
+      t.seq = seq;
+      t.theta = theta;
+    }
+    tab = t.tab;
   }
   rope_k<<<grid_for(tokens * 2 * (h / 64) * 4, kThreads, ctas), kThreads, 0, s>>>(qkv, tab, tokens, seq, h,
                                                                                   inverse ? -1.f : 1.f);
@@ -1114,10 +1130,9 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
     *nblk = grid;
 #define ZP_LNB(R, C, NV)                                                                               \
   {                                                                                                    \
-    static bool attr = false;                                                                          \
-    if (!attr) {                                                                                       \
+    static std::atomic<uint64_t> attr{0};                                                                          \
+    if (first_on_device(attr)) {                                                                                       \
       cudaFuncSetAttribute(ln_bwd_fused_k<R, C, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      attr = true;                                                                                     \
     }                                                                                                  \
     ln_bwd_fused_k<R, C, NV><<<grid, kThreads, smem, s>>>(dy, x, mean, rstd, g, dres, dx, rows, h, chunk, part, cs); \
   }
@@ -1163,10 +1178,9 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
     const int grid = int(rows < ctas ? rows : ctas);
 #define ZP_CE(C)                                                                                        \
   {                                                                                                     \
-    static bool attr = false;                                                                           \
-    if (!attr) {                                                                                        \
+    static std::atomic<uint64_t> attr{0};                                                                           \
+    if (first_on_device(attr)) {                                                                                        \
       cudaFuncSetAttribute(ce_reg_k<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);       \
-      attr = true;                                                                                      \
     }                                                                                                   \
     ce_reg_k<C><<<grid, kCeThreads, 2 * stride, s>>>(logits, tokens, seq, rows, vocab, ldv, grad_scale, row_loss); \
   }
@@ -1181,10 +1195,9 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
     return;
   }
   if (2 * stride <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr)) {
       cudaFuncSetAttribute(ce_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
     }
     const int grid = int(rows < ctas ? rows : ctas);
     ce_smem_k<<<grid, kCeThreads, 2 * stride, s>>>(logits, tokens, seq, rows, vocab, ldv, grad_scale, row_loss);

@@ -1,6 +1,7 @@
 // HBM-bound kernels of the GPT training step and of the ZeRO reduce/update path.
 // All launchers take the rank's CTA cap (`ctas`, its emulated SM budget) and a stream.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -11,6 +12,15 @@ using bf16 = __nv_bfloat16;
 
 // Count of kernels this library has launched (bench.py's gpu_launches claim).
 void note_launch(int64_t k = 1);
+// True the first time it is called on the calling thread's current device for this flag word:
+// per-device one-time setup (cudaFuncSetAttribute applies to the current device only, and one
+// process may drive several GPUs, e.g. the single-process device-seam backend).
+inline bool first_on_device(std::atomic<uint64_t>& flags) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  return !(flags.fetch_or(bit) & bit);
+}
 int64_t launch_count();
 
 // ---- initialisation / data

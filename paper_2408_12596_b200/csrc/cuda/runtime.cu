@@ -18,6 +18,8 @@
 // reduce-scatter + AdamW + all-gather (peer.cu). ZP_PEER=0 selects the NCCL path instead.
 #include <nccl.h>
 
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -883,6 +885,10 @@ struct Runtime {
     struct Handles {
       cudaIpcMemHandle_t arena, flags;
       int ok;
+      int device;
+      long long pid;
+      void* raw_arena;  // same-process ranks (one process driving several GPUs) use these with
+      void* raw_flags;  // peer access instead of IPC, which cannot reopen its own allocations
     };
     CK(cudaMalloc(&flags, sizeof(PeerFlags)));
     CK(cudaMemset(flags, 0, sizeof(PeerFlags)));
@@ -890,6 +896,10 @@ struct Runtime {
     mine.ok = cudaIpcGetMemHandle(&mine.arena, arena.base) == cudaSuccess &&
               cudaIpcGetMemHandle(&mine.flags, flags) == cudaSuccess;
     cudaGetLastError();
+    mine.device = d.device;
+    mine.pid = (long long)getpid();
+    mine.raw_arena = arena.base;
+    mine.raw_flags = flags;
     std::vector<Handles> all(n);
     void* dbuf = nullptr;
     CK(cudaMalloc(&dbuf, sizeof(Handles) * (n + 1)));
@@ -910,6 +920,22 @@ struct Runtime {
         continue;
       }
       if (!ok) break;
+      if (all[j].pid == mine.pid) {  // same process: direct peer access to the raw allocation
+        if (all[j].device == d.device) {
+          ok = 0;  // two ranks on one GPU in one process are not supported
+          break;
+        }
+        const cudaError_t e = cudaDeviceEnablePeerAccess(all[j].device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+          ok = 0;
+          break;
+        }
+        cudaGetLastError();
+        pv.base[j] = static_cast<char*>(all[j].raw_arena);
+        pv.flags[j] = static_cast<PeerFlags*>(all[j].raw_flags);
+        continue;
+      }
       void* a = nullptr;
       void* f = nullptr;
       if (cudaIpcOpenMemHandle(&a, all[j].arena, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
@@ -1436,6 +1462,7 @@ int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
 int zp_runtime_destroy(zp_runtime* h) {
   if (!h) return ZP_OK;
   zp::Runtime& R = h->rt;
+  cudaSetDevice(R.d.device);
   cudaStreamSynchronize(R.st);
   R.close_peers();
   if (R.flags) cudaFree(R.flags);
@@ -1465,6 +1492,7 @@ int zp_runtime_param_count(zp_runtime* h, int64_t* padded, int64_t* logical) {
 
 int zp_runtime_activation_bytes(zp_runtime* h, int64_t batch, int64_t* out) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     *out = int64_t(h->rt.plan_acts(batch, nullptr, nullptr));
     return ZP_OK;
   });
@@ -1472,6 +1500,7 @@ int zp_runtime_activation_bytes(zp_runtime* h, int64_t batch, int64_t* out) {
 
 int zp_runtime_resident_bytes(zp_runtime* h, int32_t stage, int64_t* out) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     h->rt.configure(stage);
     *out = int64_t(h->rt.resident_mark);
     return ZP_OK;
@@ -1480,6 +1509,7 @@ int zp_runtime_resident_bytes(zp_runtime* h, int32_t stage, int64_t* out) {
 
 int zp_runtime_memory_probe(zp_runtime* h, int32_t stage, zp_probe* out) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     *out = h->rt.memory_probe(stage);
     return ZP_OK;
   });
@@ -1488,6 +1518,7 @@ int zp_runtime_memory_probe(zp_runtime* h, int32_t stage, zp_probe* out) {
 int zp_runtime_load_tokens(zp_runtime* h, const int32_t* host, int64_t first, int64_t count,
                            uint64_t iteration, int32_t from_host) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     h->rt.load_tokens(host, first, count, iteration, from_host != 0);
     return ZP_OK;
   });
@@ -1496,6 +1527,7 @@ int zp_runtime_load_tokens(zp_runtime* h, const int32_t* host, int64_t first, in
 int zp_runtime_run_step(zp_runtime* h, int64_t batch, int32_t stage, int64_t global_batch,
                         zp_step_trace* out) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     if (batch < 0) zp::fail(ZP_EINVAL, "batch_size must be >= 0");
     return h->rt.run_step(batch, stage, global_batch, out);
   });
@@ -1504,6 +1536,7 @@ int zp_runtime_run_step(zp_runtime* h, int64_t batch, int32_t stage, int64_t glo
 int zp_runtime_execute_iteration(zp_runtime* h, const zp_allocation_plan* plan, int32_t stage,
                                  zp_rank_timing* timing) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     h->rt.execute(plan, stage, timing);
     return ZP_OK;
   });
@@ -1511,6 +1544,7 @@ int zp_runtime_execute_iteration(zp_runtime* h, const zp_allocation_plan* plan, 
 
 int zp_runtime_get_state(zp_runtime* h, int32_t kind, float* out, int64_t* begin, int64_t* end) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
     const float* src = kind == 0 ? R.p32 : kind == 1 ? R.m32 : kind == 2 ? R.v32 : R.gkeep;
@@ -1525,6 +1559,7 @@ int zp_runtime_get_state(zp_runtime* h, int32_t kind, float* out, int64_t* begin
 
 int zp_runtime_get_params_bf16(zp_runtime* h, uint16_t* out) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
     CK(cudaStreamSynchronize(R.st));
@@ -1541,6 +1576,7 @@ int zp_runtime_get_params_bf16(zp_runtime* h, uint16_t* out) {
 
 int zp_runtime_set_params(zp_runtime* h, const float* full) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
     float* tmp = nullptr;
@@ -1561,6 +1597,7 @@ int zp_runtime_set_params(zp_runtime* h, const float* full) {
 
 int zp_runtime_owned_ranges(zp_runtime* h, int64_t* triples, int32_t cap, int32_t* count) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.stage < 0) zp::fail(ZP_EINVAL, "runtime not configured (run a step first)");
     *count = int32_t(R.owned.size());
@@ -1580,6 +1617,7 @@ int zp_runtime_peer_collectives(zp_runtime* h, int32_t* on) {
 
 int zp_runtime_bench_collective(zp_runtime* h, int32_t which, int32_t reps, double* seconds, int64_t* pulled) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.n < 2 || !R.peer || which < 0 || which > 2 || reps < 1)
       zp::fail(ZP_EINVAL, "bench_collective needs >= 2 ranks on the NVLink peer path, which in 0..2, reps >= 1");
@@ -1620,6 +1658,7 @@ int zp_runtime_bench_collective(zp_runtime* h, int32_t which, int32_t reps, doub
 
 int zp_runtime_link_model(zp_runtime* h, int32_t stage, int32_t reps, double* bandwidth, double* latency) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (R.n < 2 || reps < 1) zp::fail(ZP_EINVAL, "link_model needs >= 2 ranks and reps >= 1");
     R.configure(stage);
@@ -1688,11 +1727,15 @@ int zp_runtime_tensor_info(zp_runtime* h, const char* name, int64_t* offset, int
 }
 
 int zp_runtime_profile(zp_runtime* h, int32_t stage_request, zp_profile* out) {
-  return guarded([&] { return h->rt.profile(stage_request, out); });
+  return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));
+    return h->rt.profile(stage_request, out);
+  });
 }
 
 int zp_runtime_mark(zp_runtime* h, int32_t slot) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (slot < 0 || slot >= 8) zp::fail(ZP_EINVAL, "slot must be in [0, 8)");
     if (!R.marks[slot]) CK(cudaEventCreate(&R.marks[slot]));
@@ -1703,6 +1746,7 @@ int zp_runtime_mark(zp_runtime* h, int32_t slot) {
 
 int zp_runtime_elapsed(zp_runtime* h, int32_t a, int32_t b, double* seconds) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     CK(cudaEventSynchronize(R.marks[b]));
     float ms = 0.f;
@@ -1714,6 +1758,7 @@ int zp_runtime_elapsed(zp_runtime* h, int32_t a, int32_t b, double* seconds) {
 
 int zp_runtime_gemm_stats(zp_runtime* h, int32_t mode, double* flops, double* seconds, int64_t* launches) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     zp::Runtime& R = h->rt;
     if (mode == 1) {
       if (R.gtm.ev.empty()) R.gtm.init(1 << 15);
@@ -1741,6 +1786,7 @@ int zp_runtime_gemm_stats(zp_runtime* h, int32_t mode, double* flops, double* se
 
 int zp_runtime_sync(zp_runtime* h) {
   return guarded([&] {
+    CK(cudaSetDevice(h->rt.d.device));  // one process may drive several GPUs
     CK(cudaStreamSynchronize(h->rt.st));
     return ZP_OK;
   });
