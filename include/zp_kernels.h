@@ -52,6 +52,10 @@ int zp_gemm(const zp_gemm_desc* d, void* stream);
  * lse [batch*heads*seq] fp32 (natural log of the row sum of exp(scores / 8)). */
 int zp_attention_fwd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq, int32_t heads,
                      int32_t max_ctas, void* stream);
+/* Same with an explicit head_dim (64 or 128; qkv heads of head_dim contiguous, lse scale
+ * 1/sqrt(head_dim)). head_dim 128: two 128-query tiles per CTA sharing every K/V tile. */
+int zp_attention_fwd_hd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq, int32_t heads,
+                        int32_t head_dim, int32_t max_ctas, void* stream);
 /* Gradients of the above: dout [batch*seq, heads*64] -> dqkv [batch*seq, 3*heads*64] bf16.
  * Workspaces: dvec [batch*heads*seq] fp32, dq32 [batch*seq, heads*64] fp32. */
 int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,

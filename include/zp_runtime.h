@@ -111,6 +111,10 @@ int zp_runtime_get_state(zp_runtime* rt, int32_t kind, float* out, int64_t* begi
 int zp_runtime_get_params_bf16(zp_runtime* rt, uint16_t* out); /* full bf16 params (Z3: owned slices) */
 int zp_runtime_set_params(zp_runtime* rt, const float* full_fp32); /* resets master + bf16 copy */
 int zp_runtime_keep_grads(zp_runtime* rt, int32_t on);
+/* SM confinement of the rank: *sms = SMs its kernels may use, *green = 1 when a green context
+ * (driver SM partition, a multiple of 8 SMs <= sm_budget) confines every kernel on the rank's
+ * stream, including NCCL's and the HBM-bound ones; 0 = grid caps only (ZP_GREEN=0 or no support). */
+int zp_runtime_sm_info(zp_runtime* rt, int32_t* sms, int32_t* green);
 /* *on = 1 when the ZeRO-1/2/3 collectives run over NVLink peer memory (CUDA IPC mappings of every
  * rank's arena: pull reduce-scatter and all-gather, and the fused reduce-scatter + AdamW +
  * all-gather kernel at the ZeRO-1/2 synchronisation point),

@@ -55,6 +55,9 @@ lib.zp_launch_count.restype = C.c_int64
 lib.zp_attention_fwd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                  C.c_int32, C.c_void_p]
 lib.zp_attention_fwd.restype = C.c_int
+lib.zp_attention_fwd_hd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_void_p]
+lib.zp_attention_fwd_hd.restype = C.c_int
 lib.zp_attention_bwd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
 lib.zp_attention_bwd.restype = C.c_int

@@ -851,6 +851,319 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 }
 
+// ============================================================================ forward, head_dim 128
+// One CTA task = a block of two consecutive 128-query tiles (Q0, Q1) of one (head, sample); the two
+// tiles share every K/V tile the TMA warp streams in, and their softmax warp groups ping-pong
+// with the single MMA warp:
+//   S0(0) S1(0) | PV0(0) S0(1) | PV1(0) S1(1) | PV0(1) S0(2) | ...
+// so the tensor pipe computes one tile's products while the other tile's eight softmax warps turn
+// scores into probabilities. TMEM: S0/P0 [0,128), S1/P1 [128,256), O0 [256,384), O1 [384,512).
+// P (packed bf16 pairs) overwrites the S columns of the key half that produced it: a thread that
+// owns keys 64*kh.. writes P columns 64*kh..64*kh+31, so the two halves of a row never touch each
+// other's scores. S(j+1) is issued after P.V(j) in the same tensor pipe (in-order execution), so
+// it only overwrites P(j) once P.V(j) has consumed it. Causal: Q0 = queries 256b..+127 needs key
+// tiles 0..2b (2b diagonal), Q1 needs 0..2b+1 (2b+1 diagonal).
+// Warp roles: 0-7 softmax of Q0, 8-15 softmax of Q1 (lane quarter w % 4, key half (w / 4) % 2),
+// 16 TMA producer, 17 MMA issuer.
+constexpr int kD2 = 128;
+constexpr int kBlk = kT * 64 * 2;  // [128, 64] bf16 SWIZZLE_128B block = 16 KiB
+constexpr int kTile2 = 2 * kBlk;   // [128, 128] tile (two blocks along the head dim)
+constexpr int kF2Threads = 18 * 32;
+constexpr int kF2Producer = 16, kF2Mma = 17;
+
+struct F2Smem {
+  static constexpr int kQ = 0;                     // Q0, Q1
+  static constexpr int kK = kQ + 2 * kTile2;       // 2 stages
+  static constexpr int kV = kK + 2 * kTile2;       // 2 stages
+  static constexpr int kRed = kV + 2 * kTile2;     // [2 groups][2 halves][128 rows] fp32
+  static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+static_assert(F2Smem::kBytes <= 232448, "forward d128 shared memory");
+
+__device__ unsigned int g_sched2[4];  // [fwd counter, fwd done, bwd counter, bwd done] (head_dim 128)
+
+// K-major [128, 128] tile stored as two 64-wide SWIZZLE_128B blocks, k16 step 0..7.
+__device__ __forceinline__ uint64_t kdesc128(uint32_t base, int k16) {
+  return ptx::smem_desc_sw128(base + (k16 >> 2) * kBlk + (k16 & 3) * 32, 16, 1024);
+}
+
+__global__ void __launch_bounds__(kF2Threads, 1)
+    attn_fwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, bf16* __restrict__ out,
+                         float* __restrict__ lse, int seq, int heads, int nz, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + F2Smem::kBar);
+  uint64_t* q_full = bar + 0;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;   // [2]
+  uint64_t* kv_empty = bar + 4;  // [2]
+  uint64_t* s_full = bar + 6;    // [2 groups] S in TMEM (MMA -> softmax)
+  uint64_t* p_full = bar + 8;    // [2] P in TMEM, O rescaled (softmax -> MMA)
+  uint64_t* pv_done = bar + 10;  // [2] P.V complete (MMA -> softmax epilogue)
+  uint64_t* o_free = bar + 12;   // [2] O read out (softmax -> MMA)
+  const TaskRing ring{reinterpret_cast<int*>(bar + 14), bar + 16, bar + 20};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
+
+  const int warp = int(ptx::warp_id());
+  const int lane = threadIdx.x & 31;
+  const int nt = seq / kT;
+  const int nb = (nt + 1) / 2;  // query blocks of two tiles
+  const int ntasks = nb * nz;
+  const int h = heads * kD2;
+
+  if (warp == kF2Producer && lane == 0) {
+    ptx::tma_prefetch_desc(&map_qkv);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&p_full[i], 256);
+      ptx::mbar_init(&pv_done[i], 1);
+      ptx::mbar_init(&o_free[i], 256);
+    }
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&ring.full[i], 1);
+      ptx::mbar_init(&ring.empty[i], 17);  // MMA thread + 16 softmax warps
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == kF2Producer) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kF2Producer) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint32_t item = 0;; ++item) {
+        const int t = ring.produce(item, &g_sched2[0]);
+        if (t >= ntasks) break;
+        const AttnTask tk = group_task(t, nz, nb, true);
+        const int smp = tk.z / heads, head = tk.z % heads;
+        const int row0 = smp * seq;
+        const bool has1 = 2 * tk.tile + 1 < nt;
+        const int q0 = row0 + 2 * tk.tile * kT;
+        ptx::mbar_wait(q_empty, (item & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * kTile2);
+        for (int q = 0; q < (has1 ? 2 : 1); ++q)
+          for (int c = 0; c < 2; ++c)
+            ptx::tma_load_4d(sm + F2Smem::kQ + q * kTile2 + c * kBlk, &map_qkv, q_full, head * kD2 + 64 * c,
+                             q0 + q * kT, 0, 0);
+        const int nj = 2 * tk.tile + (has1 ? 2 : 1);
+        for (int j = 0; j < nj; ++j) {
+          ptx::mbar_wait(&kv_empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&kv_full[stage], 2 * kTile2);
+          for (int c = 0; c < 2; ++c) {
+            ptx::tma_load_4d(sm + F2Smem::kK + stage * kTile2 + c * kBlk, &map_qkv, &kv_full[stage],
+                             h + head * kD2 + 64 * c, row0 + j * kT, 0, 0);
+            ptx::tma_load_4d(sm + F2Smem::kV + stage * kTile2 + c * kBlk, &map_qkv, &kv_full[stage],
+                             2 * h + head * kD2 + 64 * c, row0 + j * kT, 0, 0);
+          }
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      sched_finish(&g_sched2[0], 1);
+    }
+  } else if (warp == kF2Mma) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, 128, 0, 1);
+      int kw = 0;           // K/V tiles waited for (full barrier phases), as a running count
+      int kd = 0;           // K/V tiles released
+      uint32_t gp[2] = {0, 0};    // P.V issues per group (p_full phases)
+      uint32_t ntask[2] = {0, 0}; // tasks per group (o_free phases)
+      auto wait_kv = [&](int upto) {  // make sure K/V tile number `upto` (running count) has landed
+        while (kw <= upto) {
+          ptx::mbar_wait(&kv_full[kw & 1], (kw >> 1) & 1);
+          ++kw;
+        }
+      };
+      auto issue_s = [&](int g, int kvi) {
+        const uint32_t sq = ptx::smem_u32(sm + F2Smem::kQ + g * kTile2);
+        const uint32_t sk = ptx::smem_u32(sm + F2Smem::kK + (kvi & 1) * kTile2);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + 128 * g, kdesc128(sq, k), kdesc128(sk, k), id_s, k > 0);
+        ptx::umma_commit(&s_full[g]);
+      };
+      auto issue_pv = [&](int g, int kvi, bool acc) {
+        ptx::mbar_wait(&p_full[g], gp[g] & 1);
+        ++gp[g];
+        ptx::tc_fence_after();
+        const uint32_t sv = ptx::smem_u32(sm + F2Smem::kV + (kvi & 1) * kTile2);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t pcol = 128 * g + (k < 4 ? 8 * k : 64 + 8 * (k - 4));
+          ptx::umma_bf16_ts(tmem + 256 + 128 * g, tmem + pcol, mndesc(sv, k), id_o, acc || k > 0);
+        }
+        ptx::umma_commit(&pv_done[g]);
+      };
+      for (uint32_t item = 0;; ++item) {
+        const int t = ring.consume1(item);
+        if (t >= ntasks) break;
+        const AttnTask tk = group_task(t, nz, nb, true);
+        const bool has1 = 2 * tk.tile + 1 < nt;
+        const int nj0 = 2 * tk.tile + 1, nj1 = has1 ? 2 * tk.tile + 2 : 0;
+        const int nj = has1 ? nj1 : nj0;
+        const int kv0 = kd;  // running index of this task's key tile 0
+        ptx::mbar_wait(q_full, item & 1);
+        wait_kv(kv0);
+        issue_s(0, kv0);
+        if (has1) issue_s(1, kv0);
+        if (nj == 1) ptx::umma_commit(q_empty);
+        for (int j = 0; j < nj; ++j) {
+          const int kv = kv0 + j;
+          if (j < nj0) {
+            if (j == 0) ptx::mbar_wait(&o_free[0], (ntask[0] & 1) ^ 1);  // previous O0 read out
+            issue_pv(0, kv, j > 0);
+            if (j + 1 < nj0) {
+              wait_kv(kv + 1);
+              issue_s(0, kv + 1);
+            }
+          }
+          if (j < nj1) {
+            if (j == 0) ptx::mbar_wait(&o_free[1], (ntask[1] & 1) ^ 1);
+            issue_pv(1, kv, j > 0);
+            if (j + 1 < nj1) {
+              wait_kv(kv + 1);
+              issue_s(1, kv + 1);
+            }
+          }
+          if (j + 2 == nj) ptx::umma_commit(q_empty);  // the task's last S has been issued
+          ptx::umma_commit(&kv_empty[kv & 1]);
+          ++kd;
+        }
+        ++ntask[0];
+        if (has1) ++ntask[1];
+      }
+    }
+  } else {  // -------------------------------------------------------------- softmax warps 0-15
+    const int g = warp >> 3;                 // query tile of the block
+    const int q4 = warp & 3, kh = (warp >> 2) & 1;
+    const int nbar = 1 + g * 4 + q4;         // named barrier of the row quarter's two halves
+    const int r = q4 * 32 + lane;            // query row within the tile == TMEM lane
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    float* red = reinterpret_cast<float*>(sm + F2Smem::kRed) + g * 256;  // [2 halves][128]
+    const uint32_t t_s = tmem + 128 * g + lane_off + kh * 64;
+    const uint32_t t_p = tmem + 128 * g + lane_off + kh * 64;  // packed P over this half's S columns
+    const uint32_t t_o = tmem + 256 + 128 * g + lane_off + kh * 64;
+    uint32_t cnt = 0, ntk = 0;
+    for (uint32_t item = 0;; ++item) {
+      const int t = ring.consume(item);
+      if (t >= ntasks) break;
+      const AttnTask tk = group_task(t, nz, nb, true);
+      const bool has1 = 2 * tk.tile + 1 < nt;
+      if (g == 1 && !has1) continue;
+      const int smp = tk.z / heads, head = tk.z % heads;
+      const int qt = 2 * tk.tile + g;  // this group's query tile
+      const int nj = qt + 1;           // key tiles 0..qt, qt diagonal
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nj; ++j, ++cnt) {
+        ptx::mbar_wait(&s_full[g], cnt & 1);
+        ptx::tc_fence_after();
+        float sv[64];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          ptx::tmem_ld_32x32b_x32(t_s + c * 32, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
+        }
+        if (j == qt) {  // diagonal tile: key > query is masked
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (kh * 64 + i > r) sv[i] = -INFINITY;
+        }
+        float pm[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pm[i] = fmaxf(sv[i], sv[i + 8]);
+#pragma unroll
+        for (int i = 16; i < 64; i += 8) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], sv[i + k]);
+        }
+        sts_f32(&red[kh * 128 + r], fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                          fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))));
+        asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+        const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
+        asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+        const bool raise = mx > m + kRescaleLog2;
+        const float alpha = raise ? ex2(m - mx) : 1.f;
+        if (raise) m = mx;
+        uint32_t pk[32];
+        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const float p0 = ex2(fmaf(sv[i], scale_log2, -m)), p1 = ex2(fmaf(sv[i + 1], scale_log2, -m));
+          ps[(i >> 1) & 7] += p0 + p1;
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
+        // O += P.V of the previous tile is complete (it precedes this tile's S in the tensor pipe)
+        if (j > 0 && __any_sync(0xffffffffu, raise)) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x32(t_o + c * 32, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            ptx::tmem_st_32x32b_x32(t_o + c * 32, v);
+          }
+        }
+        l = l * alpha + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
+        ptx::tmem_st_32x32b_x32(t_p, pk);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[g]);
+      }
+      // epilogue: the last P.V, the halves' row sums, O / l -> bf16, LSE
+      ptx::mbar_wait(&pv_done[g], (cnt - 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t o[2][32];
+      ptx::tmem_ld_32x32b_x32(t_o, o[0]);
+      ptx::tmem_ld_32x32b_x32(t_o + 32, o[1]);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&o_free[g]);
+      ++ntk;
+      sts_f32(&red[kh * 128 + r], l);
+      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+      const float lt = lds_f32(&red[r]) + lds_f32(&red[128 + r]);
+      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+      const float inv = 1.f / lt;
+      const int64_t row = int64_t(smp) * seq + int64_t(qt) * kT + r;
+      bf16* dst = out + row * h + head * kD2 + kh * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(o[c][e]) * inv, __uint_as_float(o[c][e + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(o[c][e + 2]) * inv, __uint_as_float(o[c][e + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(o[c][e + 4]) * inv, __uint_as_float(o[c][e + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(o[c][e + 6]) * inv, __uint_as_float(o[c][e + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + e) = u;
+        }
+      if (kh == 0) lse[int64_t(tk.z) * seq + int64_t(qt) * kT + r] = (m + log2f(lt)) / kLog2e;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kF2Producer) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 // D[z, q] = sum_d dO[q, head*64 + d] * O[q, head*64 + d]. One warp per token row: lane l reads
 // 16-byte chunks l, l+32, ... (8 lanes per head per pass), reduced over groups of 8 lanes.
 __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __restrict__ O, float* __restrict__ dvec,
@@ -961,9 +1274,31 @@ int device_sms() {
 
 }  // namespace
 
+cudaError_t attention_fwd_d128(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
+                               int ctas, cudaStream_t s) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         F2Smem::kBytes);
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap m;
+  const int h = heads * kD2;
+  if (!map_rows(&m, qkv, batch * seq, 3 * h)) return cudaErrorInvalidValue;
+  const int nz = int(batch) * heads;
+  const int nb = (seq / kT + 1) / 2;
+  const int ntasks = nb * nz;
+  const int grid = std::min(ntasks, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
+  const float scale_log2 = (1.0f / std::sqrt(float(kD2))) * kLog2e;
+  attn_fwd_d128_kernel<<<grid, kF2Threads, F2Smem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
-                          int ctas, cudaStream_t s) {
-  if (seq % kT || batch < 1) return cudaErrorInvalidValue;
+                          int ctas, cudaStream_t s, int head_dim) {
+  if (seq % kT || batch < 1 || (head_dim != 64 && head_dim != 128)) return cudaErrorInvalidValue;
+  if (head_dim == 128) return attention_fwd_d128(qkv, out, lse, batch, seq, heads, ctas, s);
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

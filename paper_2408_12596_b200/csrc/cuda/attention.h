@@ -1,4 +1,4 @@
-// Fused causal attention (head_dim 64) on tcgen05: the s x s scores never reach HBM.
+// Fused causal attention (head_dim 64 or 128) on tcgen05: the s x s scores never reach HBM.
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -11,7 +11,7 @@ using bf16 = __nv_bfloat16;
 // qkv: [batch*seq, 3h] (Q | K | V, heads of 64 contiguous); out: [batch*seq, h];
 // lse: [batch*heads*seq] fp32 natural-log row log-sum-exp of the scaled scores.
 cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
-                          int ctas, cudaStream_t s);
+                          int ctas, cudaStream_t s, int head_dim = 64);
 
 // dout: [batch*seq, h]; writes dqkv [batch*seq, 3h]. Workspaces: dvec [batch*heads*seq] fp32,
 // dq32 [batch*seq, h] fp32.

@@ -34,6 +34,13 @@ extern "C" int zp_attention_fwd(const void* qkv, void* out, float* lse, int64_t 
   return e == cudaSuccess ? 0 : 5;
 }
 
+extern "C" int zp_attention_fwd_hd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq,
+                                   int32_t heads, int32_t head_dim, int32_t max_ctas, void* stream) {
+  const cudaError_t e = zp::attention_fwd(static_cast<const zp::bf16*>(qkv), static_cast<zp::bf16*>(out), lse,
+                                          batch, seq, heads, max_ctas, static_cast<cudaStream_t>(stream), head_dim);
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+}
+
 extern "C" int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                                 float* dvec, float* dq32, void* dqkv, int64_t batch, int32_t seq,
                                 int32_t heads, int32_t max_ctas, void* stream) {

@@ -16,6 +16,7 @@
 // With NVLink peer access (the default when every rank can map every other rank's arena),
 // the Z1/Z2 reduce-scatters are peer-memory pulls and the synchronisation point is one kernel:
 // reduce-scatter + AdamW + all-gather (peer.cu). ZP_PEER=0 selects the NCCL path instead.
+#include <cuda.h>
 #include <nccl.h>
 
 #include <unistd.h>
@@ -247,6 +248,68 @@ struct Timer {
   }
 };
 
+// ------------------------------------------------------------------ green contexts
+// An SM budget is enforced with a green context (driver API, resolved at run time): the rank's
+// stream belongs to an SM partition of `budget` SMs (rounded down to the hardware granularity of
+// 8), so every kernel on it — GEMMs, attention, the HBM-bound elementwise kernels, the peer
+// collectives and NCCL's own kernels — runs on those SMs only. Grid caps stay as the fallback
+// (ZP_GREEN=0, or a driver without green contexts).
+struct GreenCtx {
+  CUgreenCtx ctx = nullptr;
+  int sms = 0;
+};
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+bool make_green_stream(int device, int budget, GreenCtx* g, cudaStream_t* st) {
+  using GetDev = CUresult (*)(CUdevice*, int);
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                             unsigned int);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+  using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+  using MkStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+  using Destroy = CUresult (*)(CUgreenCtx);
+  auto get_dev = driver_fn<GetDev>("cuDeviceGet");
+  auto get_res = driver_fn<GetRes>("cuDeviceGetDevResource");
+  auto split = driver_fn<Split>("cuDevSmResourceSplitByCount");
+  auto gen = driver_fn<GenDesc>("cuDevResourceGenerateDesc");
+  auto create = driver_fn<Create>("cuGreenCtxCreate");
+  auto mk = driver_fn<MkStream>("cuGreenCtxStreamCreate");
+  auto destroy = driver_fn<Destroy>("cuGreenCtxDestroy");
+  if (!get_dev || !get_res || !split || !gen || !create || !mk || !destroy) return false;
+  CUdevice dev;
+  CUdevResource all{}, part{}, rest{};
+  if (get_dev(&dev, device) != CUDA_SUCCESS || get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    return false;
+  const unsigned want = unsigned(std::max(8, budget / 8 * 8));
+  unsigned groups = 1;
+  if (split(&part, &groups, &all, &rest, 0, want) != CUDA_SUCCESS || groups != 1) return false;
+  CUdevResourceDesc desc = nullptr;
+  if (gen(&desc, &part, 1) != CUDA_SUCCESS) return false;
+  if (create(&g->ctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return false;
+  CUstream s = nullptr;
+  if (mk(&s, g->ctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    destroy(g->ctx);
+    g->ctx = nullptr;
+    return false;
+  }
+  g->sms = int(part.sm.smCount);
+  *st = reinterpret_cast<cudaStream_t>(s);
+  return true;
+}
+void destroy_green(GreenCtx* g) {
+  using Destroy = CUresult (*)(CUgreenCtx);
+  if (!g->ctx) return;
+  if (auto destroy = driver_fn<Destroy>("cuGreenCtxDestroy")) destroy(g->ctx);
+  g->ctx = nullptr;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ runtime
@@ -256,6 +319,7 @@ struct Runtime {
   int vocab_pad = 0;
   int n = 1, rank = 0;
   int ctas = 148;
+  GreenCtx green;  // SM partition of the rank (green.ctx == nullptr: grid caps only)
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   Layout lay;
@@ -1433,7 +1497,13 @@ int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc->device));
       R.ctas = (desc->sm_budget > 0 && desc->sm_budget < sms) ? desc->sm_budget : sms;
-      CK(cudaStreamCreateWithFlags(&R.st, cudaStreamNonBlocking));
+      const char* genv = std::getenv("ZP_GREEN");
+      if (R.ctas < sms && !(genv && genv[0] == '0') && zp::make_green_stream(desc->device, R.ctas, &R.green, &R.st)) {
+        R.ctas = R.green.sms;  // the partition the hardware granted (a multiple of 8 SMs)
+      } else {
+        cudaGetLastError();
+        CK(cudaStreamCreateWithFlags(&R.st, cudaStreamNonBlocking));
+      }
       R.vocab_pad = int(zp::round_up(c.vocab, 128));
       R.lay = zp::make_layout(c, R.vocab_pad, R.n);
       size_t fr = 0, tot = 0;
@@ -1476,6 +1546,7 @@ int zp_runtime_destroy(zp_runtime* h) {
   if (R.cst) cudaStreamSynchronize(R.cst);
   if (R.arena.base) cudaFree(R.arena.base);
   if (R.st) cudaStreamDestroy(R.st);
+  zp::destroy_green(&R.green);
   if (R.cst) cudaStreamDestroy(R.cst);
   if (R.ev_free) cudaEventDestroy(R.ev_free);
   for (auto e : R.ev_done)
@@ -1608,6 +1679,12 @@ int zp_runtime_owned_ranges(zp_runtime* h, int64_t* triples, int32_t cap, int32_
     }
     return ZP_OK;
   });
+}
+
+int zp_runtime_sm_info(zp_runtime* h, int32_t* sms, int32_t* green) {
+  *sms = h->rt.ctas;
+  *green = h->rt.green.ctx ? 1 : 0;
+  return ZP_OK;
 }
 
 int zp_runtime_peer_collectives(zp_runtime* h, int32_t* on) {

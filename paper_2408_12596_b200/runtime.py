@@ -75,6 +75,7 @@ _SIGS = {
     "zp_runtime_get_params_bf16": ([_P, _P], C.c_int),
     "zp_runtime_set_params": ([_P, _P], C.c_int),
     "zp_runtime_keep_grads": ([_P, C.c_int32], C.c_int),
+    "zp_runtime_sm_info": ([_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_peer_collectives": ([_P, C.POINTER(C.c_int32)], C.c_int),
     "zp_runtime_bench_collective": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)],
                                     C.c_int),
@@ -194,6 +195,12 @@ class Runtime:
     # ---- state
     def keep_grads(self, on=True):
         _check(lib.zp_runtime_keep_grads(self.h, 1 if on else 0))
+
+    def sm_info(self):
+        """(SMs the rank's kernels may use, True when a green context confines them)."""
+        n, g = C.c_int32(), C.c_int32()
+        _check(lib.zp_runtime_sm_info(self.h, C.byref(n), C.byref(g)))
+        return n.value, bool(g.value)
 
     def peer_collectives(self) -> bool:
         """True when the ZeRO-1/2 collectives run over NVLink peer memory (peer.cu)."""

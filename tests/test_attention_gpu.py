@@ -88,3 +88,44 @@ def test_attention_perf_smoke(cuda):
     flops = 4.0 * b * H * s * s * 64 / 2  # causal half of QK^T + PV
     print(f"\n[attention b={b} s={s} H={H}] fwd {f:.3f} ms ({flops / f / 1e9:.0f} TFLOP/s) "
           f"bwd {bw:.3f} ms ({2.5 * flops / bw / 1e9:.0f} TFLOP/s)")
+
+
+@pytest.mark.parametrize("b,s,H,ctas", [(1, 128, 1, 0), (1, 256, 2, 0), (2, 384, 3, 0), (2, 1024, 8, 0),
+                                        (1, 2048, 16, 37), (1, 4096, 32, 0)])
+def test_attention_fwd_head_dim_128(cuda, b, s, H, ctas):
+    """head_dim 128 forward (two query tiles per CTA sharing K/V; P over the S columns in TMEM)."""
+    from paper_2408_12596_b200 import _lib
+    L = _lib.lib
+    d = 128
+    h, T = H * d, b * s
+    g = torch.Generator(device="cpu").manual_seed(b * 1000 + s + H + 7)
+    qkv = torch.randn(T, 3 * h, generator=g).to(torch.bfloat16).to(cuda)
+    out = torch.empty(T, h, dtype=torch.bfloat16, device=cuda)
+    lse = torch.empty(b * H * s, dtype=torch.float32, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    assert L.zp_attention_fwd_hd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), b, s, H, d, ctas, st) == 0
+    torch.cuda.synchronize()
+    ro, rl = ref_attention(qkv, b, s, H)
+    assert relerr(lse, rl) < 1e-5
+    assert relerr(out, ro) < 2e-2
+
+
+def test_attention_d128_perf_smoke(cuda):
+    """Not a gate: fused attention forward at the Llama-7B shape with head_dim 128 (32 heads)."""
+    from paper_2408_12596_b200 import _lib
+    L = _lib.lib
+    b, s, H, d = 2, 4096, 32, 128
+    h, T = H * d, b * s
+    qkv = torch.randn(T, 3 * h, device=cuda).to(torch.bfloat16)
+    out = torch.empty(T, h, dtype=torch.bfloat16, device=cuda)
+    lse = torch.empty(b * H * s, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for rep in range(3):
+        ev[0].record()
+        L.zp_attention_fwd_hd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), b, s, H, d, 0, st)
+        ev[1].record()
+    torch.cuda.synchronize()
+    f = ev[0].elapsed_time(ev[1])
+    flops = 4.0 * b * H * s * s * d / 2
+    print(f"\n[attention d128 b={b} s={s} H={H}] fwd {f:.3f} ms ({flops / f / 1e9:.0f} TFLOP/s causal)")

@@ -31,6 +31,10 @@ def _seam():
 def _run(args, timeout=900):
     r = subprocess.run([_seam()] + args, capture_output=True, text=True, timeout=timeout)
     out = r.stdout.strip()
+    # NCCL may print its version banner to stdout first; the report starts at the first '{' / '['
+    starts = [i for i in (out.find("\n{"), out.find("\n[")) if i >= 0]
+    if out[:1] not in "{[" and starts:
+        out = out[min(starts) + 1:]
     try:
         data = json.loads(out.replace('"inf"', "Infinity"))
     except json.JSONDecodeError:

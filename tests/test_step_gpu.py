@@ -159,3 +159,27 @@ def test_llama_step_matches_fp64_oracle(cuda, stage, b, lbs, gas, sm):
     worst = max((so.rel_err(g[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
     assert worst[0] < 2e-2, worst
     rt.close()
+
+
+@pytest.mark.parametrize("budget,expect", [(66, 64), (74, 72), (132, 128), (0, 148)])
+def test_green_context_confinement(cuda, budget, expect):
+    """An SM budget below the device's SM count becomes a green-context partition (a multiple of 8
+    SMs, rounded down) that every kernel of the rank runs in; the step still matches the oracle."""
+    import os
+    if os.environ.get("ZP_GREEN", "1") == "0":
+        pytest.skip("green contexts disabled")
+    rt = runtime(cuda, sm_budget=budget)
+    sms, green = rt.sm_info()
+    assert sms == expect and green == (budget != 0)
+    rt.resident_bytes(2)
+    from paper_2408_12596_b200.runtime import bf16_to_f32
+    from oracle import step as so
+    P16 = bf16_to_f32(rt.params_bf16())
+    tok = tokens_for(4)
+    rt.load_tokens(tok)
+    rt.execute_iteration(make_plan(2, 4, 4, 4, 1), 2)
+    loss, G = oracle_grads(rt, P16, tok, 4)
+    g, _ = rt.state_flat(3)
+    Gg = rt.unflatten(g)
+    assert max(so.rel_err(Gg[k], G[k]) for k in G if np.linalg.norm(G[k]) > 0) < 2e-2
+    rt.close()
