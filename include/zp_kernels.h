@@ -92,6 +92,11 @@ int zp_peer_rs_adam_ag(zp_peer_group* g, int32_t rank, int64_t src_off, int32_t 
 int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_src_off, void* dst, int64_t len,
                        uint32_t epoch, int32_t ctas, void* stream);
 
+/* Same with an explicit head_dim (64 or 128). */
+int zp_attention_bwd_hd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
+                        float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                        int32_t max_ctas, void* stream);
+
 /* Number of kernels launched by this library since load (all entry points). */
 int64_t zp_launch_count(void);
 

@@ -61,3 +61,6 @@ lib.zp_attention_fwd_hd.restype = C.c_int
 lib.zp_attention_bwd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
 lib.zp_attention_bwd.restype = C.c_int
+lib.zp_attention_bwd_hd.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+lib.zp_attention_bwd_hd.restype = C.c_int

@@ -1164,14 +1164,350 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   }
 }
 
-// D[z, q] = sum_d dO[q, head*64 + d] * O[q, head*64 + d]. One warp per token row: lane l reads
-// 16-byte chunks l, l+32, ... (8 lanes per head per pass), reduced over groups of 8 lanes.
+// ============================================================================ backward, head_dim 128
+// Transposed formulation as for head_dim 64: one CTA task = 128 keys of one (head, sample); for
+// every query tile i at or above the diagonal the single MMA warp computes S^T = K Q^T and
+// dP^T = V dO^T into TMEM (keys on the lanes). TMEM has room for exactly four 128-column fp32
+// tiles, so every region is reused in place:
+//   ST [0,128)   S^T, then P^T packed (each query half over its own S^T columns)
+//   DP [128,256) dP^T, then dS'^T packed (likewise), then dQ = dS' K (fp32, queries on the lanes)
+//   DV [256,384), DK [384,512) the task's accumulators.
+// MMA issue order per tile: dV(i) | S^T(i+1) | dK(i) | dQ(i) | dP^T(i+1): S^T of the next tile is
+// issued as soon as dV has consumed P^T (the tensor pipe executes in order), so the eight builder
+// warps compute the next tile's exponentials while dK / dQ run; dP^T(i+1) waits until the four dQ
+// warps have read dQ(i) out of TMEM. dS'^T also goes to shared memory for the dQ product (MN-major
+// A operand); the dQ warps stage dQ through that same region and add it into fp32 dQ with TMA
+// bulk reduce-add, then release it to the builders of the next tile.
+// Warp roles: 0-7 builders (lane quarter w % 4, query half w / 4), 8-11 dQ out + dK/dV epilogue,
+// 12 TMA producer, 13 MMA issuer. K/V single-buffered per task; Q/dO(+LSE, D) two stages.
+constexpr int kB2Threads = 14 * 32;
+constexpr int kB2TS = 0, kB2TDP = 128, kB2TDV = 256, kB2TDK = 384;
+
+struct B2Smem {
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTile2;
+  static constexpr int kQ = kV + kTile2;           // 2 stages
+  static constexpr int kDO = kQ + 2 * kTile2;      // 2 stages
+  static constexpr int kDS = kDO + 2 * kTile2;     // dS'^T [128 keys, 128 queries]; dQ staging
+  static constexpr int kLD = kDS + kTile2;         // 2 stages x {LSE, D}[128] fp32
+  static constexpr int kBar = kLD + 2 * 1024;
+  static constexpr int kBytes = kBar + 256;        // dynamic smem is 1 KiB aligned (checked)
+};
+static_assert(B2Smem::kBytes <= 232448, "backward d128 shared memory");
+
+__global__ void __launch_bounds__(kB2Threads, 1)
+    attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
+                         const __grid_constant__ CUtensorMap map_dq, const float* __restrict__ lse,
+                         const float* __restrict__ dvec, bf16* __restrict__ dqkv, int seq, int heads, int nz,
+                         float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  if (ptx::smem_u32(smem_raw) & 1023) __trap();  // the SWIZZLE_128B tiles need 1 KiB alignment
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + B2Smem::kBar);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* kv_empty = bar + 1;
+  uint64_t* qd_full = bar + 2;    // [2]
+  uint64_t* qd_empty = bar + 4;   // [2]
+  uint64_t* s_full = bar + 6;     // S^T in TMEM
+  uint64_t* dp_full = bar + 7;    // dP^T in TMEM
+  uint64_t* pt_full = bar + 8;    // P^T packed in TMEM (builders, 256)
+  uint64_t* dst_full = bar + 9;   // dS'^T packed in TMEM (builders, 256)
+  uint64_t* ds_full = bar + 10;   // dS'^T in shared memory (builders, 256)
+  uint64_t* mm_done = bar + 11;   // dQ in TMEM (MMA)
+  uint64_t* dq_free = bar + 12;   // dQ read out of TMEM (dQ warps, 128)
+  uint64_t* stg_free = bar + 13;  // dQ staging drained (dQ warps, 4)
+  uint64_t* acc_full = bar + 14;  // dK, dV complete (MMA)
+  uint64_t* acc_free = bar + 15;  // dK, dV read out (epilogue, 128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = int(ptx::warp_id());
+  const int lane = threadIdx.x & 31;
+  const int nt = seq / kT;
+  const int ntasks = nt * nz;
+  const int h = heads * kD2;
+
+  if (warp == 12 && lane == 0) {
+    ptx::tma_prefetch_desc(&map_qkv);
+    ptx::tma_prefetch_desc(&map_do);
+    ptx::tma_prefetch_desc(&map_dq);
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&qd_full[i], 1);
+      ptx::mbar_init(&qd_empty[i], 1);
+    }
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(dp_full, 1);
+    ptx::mbar_init(pt_full, 256);
+    ptx::mbar_init(dst_full, 256);
+    ptx::mbar_init(ds_full, 256);
+    ptx::mbar_init(mm_done, 1);
+    ptx::mbar_init(dq_free, 128);
+    ptx::mbar_init(stg_free, 4);
+    ptx::mbar_init(acc_full, 1);
+    ptx::mbar_init(acc_free, 128);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 12) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 12) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0, item = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = bwd_task_static(t, nz);
+        const int smp = tk.z / heads, head = tk.z % heads;
+        const int row0 = smp * seq;
+        ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * kTile2);
+        for (int c = 0; c < 2; ++c) {
+          ptx::tma_load_4d(sm + B2Smem::kK + c * kBlk, &map_qkv, kv_full, h + head * kD2 + 64 * c,
+                           row0 + tk.tile * kT, 0, 0);
+          ptx::tma_load_4d(sm + B2Smem::kV + c * kBlk, &map_qkv, kv_full, 2 * h + head * kD2 + 64 * c,
+                           row0 + tk.tile * kT, 0, 0);
+        }
+        for (int i = tk.tile; i < nt; ++i) {
+          ptx::mbar_wait(&qd_empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&qd_full[stage], 2 * kTile2 + 2 * 128 * 4);
+          for (int c = 0; c < 2; ++c) {
+            ptx::tma_load_4d(sm + B2Smem::kQ + stage * kTile2 + c * kBlk, &map_qkv, &qd_full[stage],
+                             head * kD2 + 64 * c, row0 + i * kT, 0, 0);
+            ptx::tma_load_4d(sm + B2Smem::kDO + stage * kTile2 + c * kBlk, &map_do, &qd_full[stage],
+                             head * kD2 + 64 * c, row0 + i * kT, 0, 0);
+          }
+          const int64_t q0 = int64_t(tk.z) * seq + int64_t(i) * kT;
+          ptx::bulk_load(sm + B2Smem::kLD + stage * 1024, lse + q0, 512, &qd_full[stage]);
+          ptx::bulk_load(sm + B2Smem::kLD + stage * 1024 + 512, dvec + q0, 512, &qd_full[stage]);
+          if (++stage == 2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 13) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_ss = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T: K-major both
+      constexpr uint32_t id_t = ptx::idesc_bf16_f32(128, 128, 0, 1);   // dV, dK: A in TMEM, B MN-major
+      constexpr uint32_t id_q = ptx::idesc_bf16_f32(128, 128, 1, 1);   // dQ: A = dS' (MN-major), B = K
+      const uint32_t sk = ptx::smem_u32(sm + B2Smem::kK), sv = ptx::smem_u32(sm + B2Smem::kV);
+      const uint32_t sds = ptx::smem_u32(sm + B2Smem::kDS);
+      uint32_t item = 0, it = 0;
+      auto sq = [&](uint32_t i) { return ptx::smem_u32(sm + B2Smem::kQ + (i & 1) * kTile2); };
+      auto sdo = [&](uint32_t i) { return ptx::smem_u32(sm + B2Smem::kDO + (i & 1) * kTile2); };
+      auto issue_st = [&](uint32_t i) {  // S^T(i) = K Q(i)^T
+        ptx::mbar_wait(&qd_full[i & 1], (i >> 1) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TS, kdesc128(sk, k), kdesc128(sq(i), k), id_ss, k > 0);
+        ptx::umma_commit(s_full);
+      };
+      auto issue_dpt = [&](uint32_t i) {  // dP^T(i) = V dO(i)^T, once dQ(i-1) has left the columns
+        ptx::mbar_wait(dq_free, (i & 1) ^ 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, kdesc128(sv, k), kdesc128(sdo(i), k), id_ss, k > 0);
+        ptx::umma_commit(dp_full);
+      };
+      auto tcol = [](int k) { return uint32_t(k < 4 ? 8 * k : 64 + 8 * (k - 4)); };  // packed query columns
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+        const AttnTask tk = bwd_task_static(t, nz);
+        const int n = nt - tk.tile;  // query tiles of this key tile
+        ptx::mbar_wait(kv_full, item & 1);
+        issue_st(it);
+        issue_dpt(it);
+        for (int q = 0; q < n; ++q, ++it) {
+          const bool first = q == 0, last = q + 1 == n;
+          if (first) ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // previous task's dK/dV read out
+          ptx::mbar_wait(pt_full, it & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_ts(tmem + kB2TDV, tmem + kB2TS + tcol(k), mndesc(sdo(it), k), id_t, !first || k > 0);
+          if (!last) issue_st(it + 1);  // overwrites P^T only after dV (in-order tensor pipe)
+          ptx::mbar_wait(dst_full, it & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::umma_bf16_ts(tmem + kB2TDK, tmem + kB2TDP + tcol(k), mndesc(sq(it), k), id_t, !first || k > 0);
+          ptx::mbar_wait(ds_full, it & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
+          ptx::umma_commit(mm_done);
+          ptx::umma_commit(&qd_empty[it & 1]);
+          if (last) {
+            ptx::umma_commit(acc_full);
+            ptx::umma_commit(kv_empty);
+          } else {
+            issue_dpt(it + 1);
+          }
+        }
+      }
+    }
+  } else if (warp < 8) {  // ------------------------------------------ P^T / dS'^T builders
+    const int q4 = warp & 3, qh = warp >> 2;
+    const int r = q4 * 32 + lane;  // key row of the tile == TMEM lane
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    const uint32_t sds = ptx::smem_u32(sm + B2Smem::kDS);
+    const float sl2 = scale * kLog2e;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+      const AttnTask tk = bwd_task_static(t, nz);
+      for (int i = tk.tile; i < nt; ++i, ++it) {
+        const float* ld = reinterpret_cast<const float*>(sm + B2Smem::kLD + (it & 1) * 1024);
+        ptx::mbar_wait(s_full, it & 1);  // S^T(i) landed; Q(i) / LSE(i) are in this stage
+        ptx::tc_fence_after();
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t vs[32];
+          ptx::tmem_ld_32x32b_x32(tmem + kB2TS + lane_off + qh * 64 + c * 32, vs);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int q = qh * 64 + c * 32 + e;
+            float p0 = ex2(fmaf(__uint_as_float(vs[e]), sl2, -lds_f32(ld + q) * kLog2e));
+            float p1 = ex2(fmaf(__uint_as_float(vs[e + 1]), sl2, -lds_f32(ld + q + 1) * kLog2e));
+            if (i == tk.tile) {  // diagonal tile: key r > query q gives P = 0
+              if (r > q) p0 = 0.f;
+              if (r > q + 1) p1 = 0.f;
+            }
+            pk[c * 16 + e / 2] = pack_bf16(p0, p1);
+          }
+        }
+        ptx::tmem_st_32x32b_x32(tmem + kB2TS + lane_off + qh * 64, pk);  // P^T over this half's S^T
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(pt_full);
+        // dS'^T = P^T (dP^T - D), from the bf16 P (the value the dV product also uses)
+        ptx::mbar_wait(dp_full, it & 1);
+        ptx::tc_fence_after();
+        uint32_t dk[32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t vp[32];
+          ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64 + c * 32, vp);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int q = qh * 64 + c * 32 + e;
+            const uint32_t pp = pk[c * 16 + e / 2];
+            const float p0 = __uint_as_float(pp << 16), p1 = __uint_as_float(pp & 0xffff0000u);
+            dk[c * 16 + e / 2] = pack_bf16(p0 * (__uint_as_float(vp[e]) - lds_f32(ld + 128 + q)),
+                                           p1 * (__uint_as_float(vp[e + 1]) - lds_f32(ld + 128 + q + 1)));
+          }
+        }
+        ptx::tmem_st_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64, dk);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(dst_full);
+        // dS'^T into shared memory for dQ = dS' K, once the previous tile's dQ staging drained
+        ptx::mbar_wait(stg_free, (it & 1) ^ 1);
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          st_shared_v4(sds + p_off(r, qh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
+        fence_proxy_async();
+        ptx::mbar_arrive(ds_full);
+      }
+    }
+  } else if (warp < 12) {  // ------------------------------------------ warps 8-11: dQ + dK/dV out
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    uint8_t* stg = sm + B2Smem::kDS + q4 * (2 * 32 * 32 * 4);  // two [32 x 32] fp32 boxes per warp
+    uint32_t it = 0, item = 0;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
+      const AttnTask tk = bwd_task_static(t, nz);
+      const int smp = tk.z / heads, head = tk.z % heads;
+      for (int i = tk.tile; i < nt; ++i, ++it) {
+        ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; dS' shared memory consumed
+        ptx::tc_fence_after();
+        uint32_t v[4][32];
+        ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off, v[0]);
+        ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + 32, v[1]);
+        ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + 64, v[2]);
+        ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + 96, v[3]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(dq_free);  // the MMA warp may put dP^T(i+1) into these columns
+        const int row = smp * seq + i * kT + q4 * 32;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint8_t* box = stg + (c & 1) * (32 * 32 * 4);
+          if (lane == 0 && c >= 2) ptx::bulk_wait_read<1>();  // this box's previous reduce read it
+          __syncwarp();
+          const uint32_t rowa = ptx::smem_u32(box) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + ((j ^ (lane & 7)) << 4)),
+                         "r"(v[c][4 * j]), "r"(v[c][4 * j + 1]), "r"(v[c][4 * j + 2]), "r"(v[c][4 * j + 3])
+                         : "memory");
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_reduce_add_2d(&map_dq, box, head * kD2 + 32 * c, row);
+            ptx::bulk_commit();
+          }
+        }
+        if (lane == 0) {
+          ptx::bulk_wait_read<0>();
+          ptx::mbar_arrive(stg_free);  // the builders may write the next dS'^T over the boxes
+        }
+        __syncwarp();
+      }
+      // epilogue: dK (scaled), dV rows of this key tile -> bf16 into dqkv
+      ptx::mbar_wait(acc_full, item & 1);
+      ptx::tc_fence_after();
+      const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        bf16* dst = dqkv + krow * 3 * h + (which == 0 ? h : 2 * h) + head * kD2;
+        const uint32_t src = tmem + (which == 0 ? kB2TDK : kB2TDV) + lane_off;
+        const float f = which == 0 ? scale : 1.f;  // dK = scale * dS'^T Q
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t w[32];
+          ptx::tmem_ld_32x32b_x32(src + c * 32, w);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 u;
+            u.x = pack_bf16(__uint_as_float(w[e]) * f, __uint_as_float(w[e + 1]) * f);
+            u.y = pack_bf16(__uint_as_float(w[e + 2]) * f, __uint_as_float(w[e + 3]) * f);
+            u.z = pack_bf16(__uint_as_float(w[e + 4]) * f, __uint_as_float(w[e + 5]) * f);
+            u.w = pack_bf16(__uint_as_float(w[e + 6]) * f, __uint_as_float(w[e + 7]) * f);
+            *reinterpret_cast<uint4*>(dst + c * 32 + e) = u;
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(acc_free);
+    }
+    if (lane == 0) ptx::bulk_wait<0>();  // dQ reductions complete before the kernel ends
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+// D[z, q] = sum_d dO[q, head*D + d] * O[q, head*D + d]. One warp per token row: lane l reads
+// 16-byte chunks l, l+32, ... (D/8 lanes per head per pass), reduced over groups of D/8 lanes.
+template <int D>
 __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __restrict__ O, float* __restrict__ dvec,
                                  int64_t tokens, int seq, int heads) {
+  static_assert(D == 64 || D == 128, "head_dim");
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
-  const int h = heads * kD;
-  const int nchunks = h / 8;  // 16-byte chunks per row; 8 chunks per head
+  const int h = heads * D;
+  const int nchunks = h / 8;  // 16-byte chunks per row; D / 8 chunks per head
   for (int64_t tok = blockIdx.x * int64_t(blockDim.x / 32) + threadIdx.x / 32; tok < tokens; tok += warps) {
     const int64_t smp = tok / seq;
     const int q = int(tok % seq);
@@ -1192,8 +1528,9 @@ __global__ void attn_dvec_kernel(const bf16* __restrict__ dO, const bf16* __rest
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 4);
-      if ((lane & 7) == 0 && chunk < nchunks) {
-        const int head = chunk / 8;
+      if (D == 128) v += __shfl_xor_sync(0xffffffffu, v, 8);
+      if ((lane & (D / 8 - 1)) == 0 && chunk < nchunks) {
+        const int head = chunk / (D / 8);
         dvec[(smp * heads + head) * seq + q] = v;
       }
     }
@@ -1317,9 +1654,40 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
   return cudaGetLastError();
 }
 
+cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
+                               float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         B2Smem::kBytes);
+    if (e != cudaSuccess) return e;
+  }
+  const int h = heads * kD2;
+  const int64_t T = batch * seq;
+  CUtensorMap mq, md, mdq;
+  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h) || !map_f32_rows(&mdq, dq32, T, h))
+    return cudaErrorInvalidValue;
+  const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
+  attn_dvec_kernel<128><<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
+  note_launch();
+  cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
+  if (e != cudaSuccess) return e;
+  const int nz = int(batch) * heads;
+  const int ntasks = (seq / kT) * nz;
+  const float scale = 1.0f / std::sqrt(float(kD2));
+  attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, mdq, lse, dvec, dqkv, seq,
+                                                                                heads, nz, scale);
+  note_launch();
+  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h, scale);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
-                          float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s) {
-  if (seq % kT || batch < 1) return cudaErrorInvalidValue;
+                          float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
+                          int head_dim) {
+  if (seq % kT || batch < 1 || (head_dim != 64 && head_dim != 128)) return cudaErrorInvalidValue;
+  if (head_dim == 128) return attention_bwd_d128(qkv, out, dout, lse, dvec, dq32, dqkv, batch, seq, heads, ctas, s);
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1332,7 +1700,7 @@ cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, co
   if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h) || !map_f32_rows(&mdq, dq32, T, h))
     return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
-  attn_dvec_kernel<<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
+  attn_dvec_kernel<64><<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
   note_launch();
   cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
   if (e != cudaSuccess) return e;

@@ -8,7 +8,7 @@ namespace zp {
 
 using bf16 = __nv_bfloat16;
 
-// qkv: [batch*seq, 3h] (Q | K | V, heads of 64 contiguous); out: [batch*seq, h];
+// qkv: [batch*seq, 3h] (Q | K | V, heads of head_dim contiguous); out: [batch*seq, h];
 // lse: [batch*heads*seq] fp32 natural-log row log-sum-exp of the scaled scores.
 cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
                           int ctas, cudaStream_t s, int head_dim = 64);
@@ -16,6 +16,7 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
 // dout: [batch*seq, h]; writes dqkv [batch*seq, 3h]. Workspaces: dvec [batch*heads*seq] fp32,
 // dq32 [batch*seq, h] fp32.
 cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
-                          float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s);
+                          float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
+                          int head_dim = 64);
 
 }  // namespace zp

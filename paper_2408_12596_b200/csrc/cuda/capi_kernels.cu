@@ -114,3 +114,13 @@ extern "C" int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_
                                             ctas, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
 }
+
+extern "C" int zp_attention_bwd_hd(const void* qkv, const void* out, const void* dout, const float* lse,
+                                   float* dvec, float* dq32, void* dqkv, int64_t batch, int32_t seq,
+                                   int32_t heads, int32_t head_dim, int32_t max_ctas, void* stream) {
+  const cudaError_t e = zp::attention_bwd(static_cast<const zp::bf16*>(qkv), static_cast<const zp::bf16*>(out),
+                                          static_cast<const zp::bf16*>(dout), lse, dvec, dq32,
+                                          static_cast<zp::bf16*>(dqkv), batch, seq, heads, max_ctas,
+                                          static_cast<cudaStream_t>(stream), head_dim);
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+}

@@ -937,33 +937,36 @@ __global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, floa
 
 // cos / sin of pos * theta^(-2j/64) for pos < seq, j < 32 (computed once per (seq, theta) in
 // double precision, kept in a small per-process table).
-__global__ void rope_table_k(float2* tab, int seq, double log_theta) {
-  const int n = seq * 32;
+// cos/sin of position pos and rotation pair j (frequency theta^(-2j/dh)), [seq][dh/2].
+__global__ void rope_table_k(float2* tab, int seq, int half, double log_theta) {
+  const int n = seq * half;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int pos = i / 32, j = i % 32;
-    const double ang = double(pos) * exp(-double(2 * j) / 64.0 * log_theta);
+    const int pos = i / half, j = i % half;
+    const double ang = double(pos) * exp(-double(2 * j) / double(2 * half) * log_theta);
     tab[i] = make_float2(float(cos(ang)), float(sin(ang)));
   }
 }
 
 // In place on the Q and K column blocks of qkv [T, 3h]; inverse = rotation by -theta (backward).
-// One thread per (token, Q|K, head, group of 8 rotation pairs): two 16-byte loads / stores.
-__global__ void rope_k(bf16* qkv, const float2* __restrict__ tab, int64_t tokens, int seq, int h, float sign) {
-  const int heads = h / 64;
-  const int per_tok = 2 * heads * 4;
+// Rotate-half pairing (i, i + dh/2) inside every head of dh columns. One thread per
+// (token, Q|K, head, group of 8 rotation pairs): two 16-byte loads / stores.
+__global__ void rope_k(bf16* qkv, const float2* __restrict__ tab, int64_t tokens, int seq, int h, int dh,
+                       float sign) {
+  const int heads = h / dh, half = dh / 2, groups = half / 8;
+  const int per_tok = 2 * heads * groups;
   const int64_t total = tokens * per_tok;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t t = i / per_tok;
     const int r = int(i - t * per_tok);
-    const int blk = r / (heads * 4), rem = r - blk * (heads * 4);
-    const int head = rem >> 2, j0 = (rem & 3) * 8;
+    const int blk = r / (heads * groups), rem = r - blk * (heads * groups);
+    const int head = rem / groups, j0 = (rem % groups) * 8;
     const int pos = int(t % seq);
-    bf16* v = qkv + t * 3 * h + blk * h + head * 64 + j0;
+    bf16* v = qkv + t * 3 * h + blk * h + head * dh + j0;
     float a[8], b[8];
     unpack8(*reinterpret_cast<const uint4*>(v), a);
-    unpack8(*reinterpret_cast<const uint4*>(v + 32), b);
-    const float4* cs4 = reinterpret_cast<const float4*>(tab + pos * 32 + j0);
+    unpack8(*reinterpret_cast<const uint4*>(v + half), b);
+    const float4* cs4 = reinterpret_cast<const float4*>(tab + pos * half + j0);
     float o0[8], o1[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -975,7 +978,7 @@ __global__ void rope_k(bf16* qkv, const float2* __restrict__ tab, int64_t tokens
       o1[2 * k + 1] = b[2 * k + 1] * c1 + a[2 * k + 1] * s1;
     }
     *reinterpret_cast<uint4*>(v) = pack8(o0);
-    *reinterpret_cast<uint4*>(v + 32) = pack8(o1);
+    *reinterpret_cast<uint4*>(v + half) = pack8(o1);
   }
 }
 
@@ -1049,12 +1052,12 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
   embed_fwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, wte, wpe, x,
                                                                           rows, h); note_launch();
 }
-void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s) {
+void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s, int dh) {
   // per-device cos/sin table for the largest sequence seen on that device (a process may drive
   // several GPUs, one host thread each)
   struct Table {
     float2* tab = nullptr;
-    int seq = 0;
+    int seq = 0, half = 0;
     float theta = 0.f;
   };
   static Table tables[64];
@@ -1065,20 +1068,22 @@ void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, 
   {
     std::lock_guard<std::mutex> lock(mu);
     Table& t = tables[dev & 63];
-    if (seq > t.seq || theta != t.theta) {
+    if (seq > t.seq || theta != t.theta || dh / 2 != t.half) {
       if (t.tab) cudaFree(t.tab);
       t.tab = nullptr;
       t.seq = 0;
-      if (cudaMalloc(&t.tab, size_t(seq) * 32 * sizeof(float2)) != cudaSuccess) return;
-      rope_table_k<<<(seq * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(t.tab, seq, std::log(double(theta)));
+      if (cudaMalloc(&t.tab, size_t(seq) * (dh / 2) * sizeof(float2)) != cudaSuccess) return;
+      rope_table_k<<<(seq * (dh / 2) + kThreads - 1) / kThreads, kThreads, 0, s>>>(t.tab, seq, dh / 2,
+                                                                                 std::log(double(theta)));
       note_launch();
       t.seq = seq;
+      t.half = dh / 2;
       t.theta = theta;
     }
     tab = t.tab;
   }
-  rope_k<<<grid_for(tokens * 2 * (h / 64) * 4, kThreads, ctas), kThreads, 0, s>>>(qkv, tab, tokens, seq, h,
-                                                                                  inverse ? -1.f : 1.f);
+  rope_k<<<grid_for(tokens * 2 * (h / dh) * (dh / 16), kThreads, ctas), kThreads, 0, s>>>(qkv, tab, tokens, seq, h,
+                                                                                        dh, inverse ? -1.f : 1.f);
   note_launch();
 }
 void swiglu_fwd(const bf16* gu, bf16* out, int64_t tokens, int f, int ctas, cudaStream_t s) {

@@ -371,6 +371,7 @@ struct Runtime {
   Timer tm;
   static constexpr int kMaxSteps = 4096;
 
+  int hd() const { return c.d_model / c.n_head; }  // head_dim (64 or 128)
   int64_t shard() const { return lay.total / n; }
   int64_t shard_begin() const { return stage == 0 ? 0 : (stage == 3 ? 0 : shard() * rank); }
   int64_t state_len() const { return stage == 0 ? lay.total : shard(); }
@@ -760,7 +761,7 @@ struct Runtime {
       CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), Wp(P.ln1_b), L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
       mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiBiasBf16, 1.f,
          Wp(P.b_qkv));
-      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st));
+      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st, hd()));
       mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f,
          Wp(P.b_o), L.x_in);
       CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), Wp(P.ln2_b), L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
@@ -797,8 +798,8 @@ struct Runtime {
       bf16* x_out = (i + 1 < c.n_layer) ? A.l[i + 1].x_in : A.x_final;
       CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), nullptr, L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
       mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiStoreBf16);
-      rope(L.qkv, T, int(s), int(h), 10000.f, false, ctas, st);
-      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st));
+      rope(L.qkv, T, int(s), int(h), 10000.f, false, ctas, st, hd());
+      CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st, hd()));
       mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_in);
       CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), nullptr, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
       // gate/up projection; its epilogue also writes h = silu(gate) * up (SwiGLU fused)
@@ -842,8 +843,8 @@ struct Runtime {
       // attention
       wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gp(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
-      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st));
-      rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st);  // back to pre-rotation Q, K
+      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd()));
+      rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st, hd());  // back to pre-rotation Q, K
       wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h), ctas, st,
@@ -898,7 +899,7 @@ struct Runtime {
       wgrad(h, h, T, A.dx2, h, L.attn, h, Gp(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
       // fused attention backward (recomputes P from the saved LSE)
-      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st));
+      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd()));
       // QKV projection
       colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, Gp(P.b_qkv), ctas, st);
       wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
@@ -1490,9 +1491,10 @@ int zp_runtime_create(const zp_runtime_desc* desc, zp_runtime** out) {
       R.n = desc->world_size < 1 ? 1 : desc->world_size;
       R.rank = desc->rank;
       const zp_gpt_config& c = R.c;
-      if (c.d_model % 256 || c.d_model / c.n_head != 64 || c.d_model % c.n_head || c.seq_len % 128 ||
-          c.d_ff % 64 || c.vocab < 2 || c.n_layer < 1 || c.arch < 0 || c.arch > 1)
-        zp::fail(ZP_EINVAL, "unsupported model shape (need d_model % 256 == 0, head_dim 64, seq % 128 == 0)");
+      if (c.d_model % 256 || c.n_head < 1 || c.d_model % c.n_head ||
+          (c.d_model / c.n_head != 64 && c.d_model / c.n_head != 128) || c.seq_len % 128 || c.d_ff % 64 ||
+          c.vocab < 2 || c.n_layer < 1 || c.arch < 0 || c.arch > 1)
+        zp::fail(ZP_EINVAL, "unsupported model shape (need d_model % 256 == 0, head_dim 64 or 128, seq % 128 == 0)");
       CK(cudaSetDevice(desc->device));
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc->device));

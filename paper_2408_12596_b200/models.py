@@ -44,7 +44,8 @@ MODELS = {
     "gpt-tiny": GPT(4, 256, 4, 8192, 256, 1024),
     "gpt2-small": GPT(12, 768, 12, 50257, 1024),
     "gpt2-medium": GPT(24, 1024, 16, 50257, 1024),
-    # Llama-style configs of BASELINE.json (head_dim 64: 32 heads at h=2048, 64 heads at h=4096)
-    "llama-1.3b": GPT(24, 2048, 32, 32000, 2048, 5504, arch=1),
-    "llama-7b": GPT(32, 4096, 64, 32000, 4096, 11008, arch=1),
+    # Llama-style configs of BASELINE.json with the standard head layout (head_dim 128: 16 heads at
+    # h=2048, 32 heads at h=4096)
+    "llama-1.3b": GPT(24, 2048, 16, 32000, 2048, 5504, arch=1),
+    "llama-7b": GPT(32, 4096, 32, 32000, 4096, 11008, arch=1),
 }

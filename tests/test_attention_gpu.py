@@ -39,7 +39,7 @@ def check_attention(cuda, b, s, H, ctas, d=64):
     out = torch.empty(T, h, dtype=torch.bfloat16, device=cuda)
     lse = torch.empty(b * H * s, dtype=torch.float32, device=cuda)
     st = torch.cuda.current_stream().cuda_stream
-    assert L.zp_attention_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), b, s, H, ctas, st) == 0
+    assert L.zp_attention_fwd_hd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), b, s, H, d, ctas, st) == 0
     torch.cuda.synchronize()
     ro, rl = ref_attention(qkv, b, s, H)
     assert relerr(lse, rl) < 1e-5
@@ -49,8 +49,8 @@ def check_attention(cuda, b, s, H, ctas, d=64):
     dvec = torch.empty(b * H * s, dtype=torch.float32, device=cuda)
     dq32 = torch.empty(T, h, dtype=torch.float32, device=cuda)
     dqkv = torch.zeros(T, 3 * h, dtype=torch.bfloat16, device=cuda)
-    assert L.zp_attention_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dvec.data_ptr(),
-                              dq32.data_ptr(), dqkv.data_ptr(), b, s, H, ctas, st) == 0
+    assert L.zp_attention_bwd_hd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dvec.data_ptr(),
+                                 dq32.data_ptr(), dqkv.data_ptr(), b, s, H, d, ctas, st) == 0
     torch.cuda.synchronize()
     x = qkv.float().requires_grad_(True)
     o, _ = ref_attention(x, b, s, H)
@@ -129,3 +129,37 @@ def test_attention_d128_perf_smoke(cuda):
     f = ev[0].elapsed_time(ev[1])
     flops = 4.0 * b * H * s * s * d / 2
     print(f"\n[attention d128 b={b} s={s} H={H}] fwd {f:.3f} ms ({flops / f / 1e9:.0f} TFLOP/s causal)")
+
+
+@pytest.mark.parametrize("b,s,H,ctas", [(1, 128, 1, 0), (1, 256, 2, 0), (2, 384, 3, 0), (2, 1024, 8, 0),
+                                        (1, 2048, 16, 37), (1, 4096, 32, 0)])
+def test_attention_fwd_bwd_head_dim_128(cuda, b, s, H, ctas):
+    """head_dim 128 backward (transposed, S^T / dP^T regions reused for P^T, dS'^T and dQ)."""
+    check_attention(cuda, b, s, H, ctas, d=128)
+
+
+def test_attention_d128_bwd_perf_smoke(cuda):
+    """Not a gate: fused attention backward at the Llama-7B shape with head_dim 128."""
+    from paper_2408_12596_b200 import _lib
+    L = _lib.lib
+    b, s, H, d = 2, 4096, 32, 128
+    h, T = H * d, b * s
+    qkv = torch.randn(T, 3 * h, device=cuda).to(torch.bfloat16)
+    out = torch.empty(T, h, dtype=torch.bfloat16, device=cuda)
+    lse = torch.empty(b * H * s, device=cuda)
+    dout = torch.randn(T, h, device=cuda).to(torch.bfloat16)
+    dvec = torch.empty(b * H * s, device=cuda)
+    dq32 = torch.empty(T, h, device=cuda)
+    dqkv = torch.empty(T, 3 * h, dtype=torch.bfloat16, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    L.zp_attention_fwd_hd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), b, s, H, d, 0, st)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for rep in range(3):
+        ev[0].record()
+        L.zp_attention_bwd_hd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(), dvec.data_ptr(),
+                              dq32.data_ptr(), dqkv.data_ptr(), b, s, H, d, 0, st)
+        ev[1].record()
+    torch.cuda.synchronize()
+    bw = ev[0].elapsed_time(ev[1])
+    flops = 10.0 * b * H * s * s * d / 2
+    print(f"\n[attention d128 b={b} s={s} H={H}] bwd {bw:.3f} ms ({flops / bw / 1e9:.0f} TFLOP/s causal)")

@@ -38,8 +38,8 @@ def _relerr(a, b):
 CASES = {
     "c2-gpt2-small-b128": (dict(n_layer=2, d_model=768, n_head=12, vocab=50257, seq_len=1024), 128, 2),
     "c3-gpt2-medium-b32": (dict(n_layer=2, d_model=1024, n_head=16, vocab=50257, seq_len=1024), 32, 3),
-    "c4-llama1.3b-b4": (dict(n_layer=2, d_model=2048, n_head=32, vocab=32000, seq_len=2048, d_ff=5504, arch=1), 4, 3),
-    "c5-llama7b-b2": (dict(n_layer=2, d_model=4096, n_head=64, vocab=32000, seq_len=4096, d_ff=11008, arch=1), 2, 3),
+    "c4-llama1.3b-b4": (dict(n_layer=2, d_model=2048, n_head=16, vocab=32000, seq_len=2048, d_ff=5504, arch=1), 4, 3),
+    "c5-llama7b-b2": (dict(n_layer=2, d_model=4096, n_head=32, vocab=32000, seq_len=4096, d_ff=11008, arch=1), 2, 3),
 }
 
 
@@ -152,7 +152,7 @@ def test_gemm_swiglu_c5_shape(cuda):
 
 
 # ---------------------------------------------------------------- attention at the configs' lengths
-@pytest.mark.parametrize("b,s,H", [(2, 2048, 32), (1, 4096, 64)])
-def test_attention_long_sequences(cuda, b, s, H):
+@pytest.mark.parametrize("b,s,H,d", [(2, 2048, 32, 64), (1, 4096, 64, 64), (2, 2048, 16, 128), (1, 4096, 32, 128)])
+def test_attention_long_sequences(cuda, b, s, H, d):
     from tests.test_attention_gpu import check_attention
-    check_attention(cuda, b, s, H, 0)
+    check_attention(cuda, b, s, H, 0, d=d)

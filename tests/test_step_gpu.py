@@ -140,20 +140,23 @@ def test_step_gpt2_small_shapes(cuda, layers, sm):
 LLAMA = dict(n_layer=2, d_model=256, n_head=4, vocab=1000, seq_len=128, d_ff=512, arch=1)
 
 
-@pytest.mark.parametrize("stage,b,lbs,gas,sm", [(0, 3, 3, 1, 0), (2, 2, 1, 2, 0), (3, 3, 2, 2, 74)])
-def test_llama_step_matches_fp64_oracle(cuda, stage, b, lbs, gas, sm):
-    """Llama family (RMSNorm, RoPE, SwiGLU, untied head) against oracle/step.py."""
+@pytest.mark.parametrize("stage,b,lbs,gas,sm,heads", [(0, 3, 3, 1, 0, 4), (2, 2, 1, 2, 0, 4), (3, 3, 2, 2, 74, 4),
+                                                       (3, 2, 2, 1, 0, 2), (2, 3, 1, 2, 104, 2)])
+def test_llama_step_matches_fp64_oracle(cuda, stage, b, lbs, gas, sm, heads):
+    """Llama family (RMSNorm, RoPE, SwiGLU, untied head) against oracle/step.py; heads 4 = head_dim
+    64, heads 2 = head_dim 128 (the Llama-1.3B / 7B layout)."""
     from paper_2408_12596_b200.runtime import Runtime, GPT, bf16_to_f32
     from oracle import step as so
     B = (gas - 1) * b + lbs
-    rt = Runtime(GPT(**LLAMA), seed=6, lr=1e-3, sm_budget=sm)
+    cfg = dict(LLAMA, n_head=heads)
+    rt = Runtime(GPT(**cfg), seed=6, lr=1e-3, sm_budget=sm)
     rt.keep_grads(True)
     rt.resident_bytes(stage)
     P = {k: v.astype(np.float64) for k, v in rt.unflatten(bf16_to_f32(rt.params_bf16())).items()}
     tok = np.random.default_rng(8).integers(0, LLAMA["vocab"], (B, LLAMA["seq_len"] + 1)).astype(np.int32)
     rt.load_tokens(tok)
     t = rt.execute_iteration(make_plan(stage, B, b, lbs, gas), stage)
-    loss, G = so.llama_loss_and_grads(P, tok, LLAMA["n_layer"], LLAMA["n_head"], LLAMA["vocab"], B)
+    loss, G = so.llama_loss_and_grads(P, tok, LLAMA["n_layer"], heads, LLAMA["vocab"], B)
     assert abs(t["loss_sum"] - loss) <= 1e-2 * abs(loss), (t["loss_sum"], loss)
     g = rt.unflatten(rt.state_flat(3)[0])
     worst = max((so.rel_err(g[k], G[k]), k) for k in G if np.linalg.norm(G[k]) > 0)
