@@ -3,8 +3,9 @@
 * `reference()` loads oracle/_ref/libzpref.so: the reference's own zeroplan sources
   (/root/reference/proj/core/src, compiled in place by oracle/Makefile) behind the
   zp_host.h C ABI with prefix `zpref_`.
-* `planner.py` is a pure-Python restatement of the planner (bit-exact in IEEE doubles),
-  a second, independent oracle pinned against the compiled reference.
+* `_ref/seam_b200` is the reference's own profiler / planner / simulator linked with the
+  device-seam binding (integration/hardware_b200.cpp): the reference pipeline driving B200 ranks
+  through its unchanged run_step / memory_probe signatures (tests/test_seam.py).
 * `step.py` is the numpy fp64 oracle of the GPT training step (the reference has no
   tensors, so gradient/parameter parity is pinned by this restatement).
 

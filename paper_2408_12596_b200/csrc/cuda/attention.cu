@@ -1,20 +1,19 @@
-// Fused causal attention for head_dim 64 on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+// Fused causal attention on sm_100a tensor cores (tcgen05 + TMEM + TMA); the s x s scores never
+// reach HBM. Four kernels:
 //
-// Forward (one CTA task = 128 queries of one (head, sample)): for every 128-key tile at or
-// below the diagonal, S = Q K^T lands in one of two TMEM buffers, eight softmax warps read it
-// (one row half per thread), run the online softmax, write P (bf16) into one of two SWIZZLE_128B
-// shared tiles, and the MMA warp accumulates P V into a TMEM-resident O.
-// Nothing of size s x s ever reaches HBM: the kernel reads Q, K, V once per query tile and
-// writes O and the row log-sum-exp.
-//
-// Backward (one CTA task = 128 keys of one (head, sample)): for every query tile at or above
-// the diagonal, S = Q K^T and dP = dO V^T land in TMEM; the softmax warps rebuild
-// P = exp(S - LSE) and dS = P (dP - D) into shared memory; the MMA warp accumulates
-// dV += P^T dO and dK += dS^T Q in TMEM (the shared P / dS tiles are read as MN-major
-// operands, no transpose) and computes dQ_tile = dS K, which the softmax warps add into an
-// fp32 dQ buffer with vector atomics.
-//
-// Warp roles: 0-3 softmax / epilogue (TMEM lanes 0-127), 4 TMA producer, 5 MMA issuer.
+// head_dim 64  forward  (attn_fwd_kernel): two independent pipelines per CTA (8 softmax warps, a
+//              TMA warp and an MMA warp each, 256 TMEM columns each): S = Q K^T -> TMEM, the softmax
+//              warps write P (bf16) back into TMEM, O += P V with P as the TMEM A operand, O resident
+//              in TMEM with a lazy (> 2^8) rescale.
+// head_dim 64  backward (attn_bwd_kernel): transposed, one CTA task per 128-key tile: S^T = K Q^T
+//              and dP^T = V dO^T -> TMEM, 8 builder warps form P^T and dS'^T into TMEM (dV, dK take
+//              them as TMEM A operands) and dS'^T into shared memory for dQ = dS' K, which four warps
+//              add into an fp32 dQ with TMA bulk reduce-add; separate score / gradient MMA warps.
+// head_dim 128 forward  (attn_fwd_d128_kernel): two query tiles per CTA share every K/V tile and
+//              ping-pong their softmax warp groups with one MMA warp; P overwrites S in TMEM.
+// head_dim 128 backward (attn_bwd_d128_kernel): the transposed scheme with every TMEM region
+//              reused in place (S^T -> P^T, dP^T -> dS'^T -> dQ), see the kernel's comment.
+// Plus D = rowsum(dO * O) (attn_dvec_kernel) and the fp32 dQ -> bf16 cast (attn_dq_cast_kernel).
 #include <cmath>
 
 #include "attention.h"
@@ -24,24 +23,6 @@
 namespace zp {
 namespace {
 
-#ifdef ZP_ATTN_TRACE
-// Debug timeline (tools/debug/attn_trace.cu): CTA 0 records (tag, clock64) per warp role.
-__device__ unsigned long long g_trace[4][8192];
-__device__ unsigned int g_trace_n[4];
-// One writer thread per role; the event index lives in a register (zp_tn) of that thread and
-// the stores are fire-and-forget, so tracing does not perturb the timeline.
-__device__ __forceinline__ void trace(int role, int tag, uint32_t& n) {
-  if (blockIdx.x != 0) return;
-  if (n < 8192) g_trace[role][n] = (static_cast<unsigned long long>(tag) << 56) | (clock64() & ((1ull << 56) - 1));
-  ++n;
-  g_trace_n[role] = n;
-}
-#define ZP_TRACE(role, tag) trace(role, tag, zp_tn)
-#define ZP_TRACE_INIT uint32_t zp_tn = 0
-#else
-#define ZP_TRACE(role, tag) ((void)0)
-#define ZP_TRACE_INIT ((void)0)
-#endif
 
 constexpr int kT = 128;          // query / key tile
 constexpr int kD = 64;           // head dim
@@ -319,7 +300,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         ++gs;
       };
-      ZP_TRACE_INIT;
       for (uint32_t item = 0;; ++item) {
         const int t = ring.consume1(item);
         if (t >= ntasks) break;
@@ -335,9 +315,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             ptx::umma_commit(q_empty);
           }
           if (j == 0) ptx::mbar_wait(o_free, (item & 1) ^ 1);  // previous task's epilogue read O
-          if (pipe == 0) ZP_TRACE(0, 1);
           ptx::mbar_wait(p_full, gp & 1);
-          if (pipe == 0) ZP_TRACE(0, 2);
           ptx::tc_fence_after();
           const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + kp * kTile);
 #pragma unroll
@@ -364,8 +342,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t t_p = tmem + kFwdTmemP + lane_off + kh * 32;
     const uint32_t t_o = tmem + kFwdTmemO + lane_off + kh * 32;
     uint32_t g = 0;  // tiles processed (S / P.V barrier phases)
-    ZP_TRACE_INIT;
-    const bool tr = (pipe == 0 && warp == 0 && lane == 0);
     for (uint32_t item = 0;; ++item) {
       const int t = ring.consume(item);
       if (t >= ntasks) break;
@@ -373,9 +349,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const int smp = tk.z / heads, head = tk.z % heads;
       float m = -INFINITY, l = 0.f;  // m: max used for the exponentials (log2 domain)
       for (int j = 0; j <= tk.tile; ++j, ++g) {
-        if (tr) ZP_TRACE(1, 1);
         ptx::mbar_wait(s_full, g & 1);
-        if (tr) ZP_TRACE(1, 2);
         ptx::tc_fence_after();
         float sv[64];
 #pragma unroll
@@ -388,7 +362,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(s_free);
-        if (tr) ZP_TRACE(1, 3);
         if (j == tk.tile) {  // diagonal tile: key > query is masked
 #pragma unroll
           for (int i = 0; i < 64; ++i)
@@ -407,7 +380,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // the row's two halves
         const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
         asm volatile("bar.sync %0, 64;" ::"r"(nb) : "memory");  // red reusable next tile
-        if (tr) ZP_TRACE(1, 4);
         // lazy rescale: raise m only when the row max outgrows it by more than 2^8
         const bool raise = mx > m + kRescaleLog2;
         const float alpha = raise ? ex2(m - mx) : 1.f;  // 0 on the first tile (m = -inf)
@@ -425,11 +397,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           ps[(i >> 1) & 7] += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
-        if (tr) ZP_TRACE(1, 5);
         // P.V(j-1) must have finished reading P and accumulating into O
         if (j > 0) {
           ptx::mbar_wait(pv_done, (g - 1) & 1);
-          if (tr) ZP_TRACE(1, 6);
           ptx::tc_fence_after();
           if (__any_sync(0xffffffffu, raise)) {
             uint32_t v[32];
@@ -445,7 +415,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full);
-        if (tr) ZP_TRACE(1, 7);
       }
       // epilogue: wait for the last P.V, combine the halves' row sums, O / l -> bf16, LSE
       ptx::mbar_wait(pv_done, (g - 1) & 1);
@@ -688,7 +657,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp < 8) {  // ------------------------------------------ P^T / dS'^T builders
-    ZP_TRACE_INIT;
     const int q4 = warp & 3, kh = warp >> 2;
     const int r = q4 * 32 + lane;  // key row of the tile == TMEM lane
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
@@ -699,12 +667,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const AttnTask tk = bwd_task_static(t, nz);
       for (int i = tk.tile; i < nt; ++i, ++it) {
         ptx::mbar_wait(&qd_full[ss], ss_ph);  // this stage's LSE / D (already complete: S^T needed Q)
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 1);
         ptx::mbar_wait(s_full, it & 1);
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 2);
         ptx::tc_fence_after();
         ptx::mbar_wait(dp_full, it & 1);
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 3);
         ptx::tc_fence_after();
         // per-query LSE and D of this stage (broadcast shared reads), indexed from the __shared__
         // array itself so the compiler emits schedulable LDS
@@ -754,7 +719,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           ptx::tmem_st_32x32b_x16(tmem + kBwdTP + lane_off + kh * 32 + c * 16, pk);
         }
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 4);
         // the dS'^T columns held dQ of the previous tile: read out by the dQ warps
         ptx::mbar_wait(dq_free, (it & 1) ^ 1);
         ptx::tc_fence_after();
@@ -764,13 +728,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::mbar_arrive(pt_full);  // dK / dV may start
         // dS'^T into shared memory for dQ = dS' K, once dQ of the previous tile has read it
         ptx::mbar_wait(mm_done, (it & 1) ^ 1);
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 5);
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           st_shared_v4(sds + p_off(r, kh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
         fence_proxy_async();
         ptx::mbar_arrive(ds_full);
-        if (warp == 0 && lane == 0) ZP_TRACE(1, 6);
         if (++ss == kBwdQD) {
           ss = 0;
           ss_ph ^= 1;

@@ -1,6 +1,6 @@
 // tcgen05.mma throughput microbenchmark (one CTA per SM, one issuing thread, descriptors
 // precomputed, 8 MMAs per unrolled iteration): cycles per MMA instruction per operand shape.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -I include tools/debug/mma_bench.cu -o tools/debug/mma_bench
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -I include tools/microbench/mma_bench.cu -o /tmp/mma_bench
 #include <cstdio>
 #include "../../paper_2408_12596_b200/csrc/cuda/ptx.cuh"
 
