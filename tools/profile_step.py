@@ -1,4 +1,4 @@
-"""One GPT-2-small ZeRO-2 micro-step iteration between cudaProfilerStart/Stop, for
+"""One micro-step iteration (default GPT-2 small ZeRO-2) between cudaProfilerStart/Stop, for
 `ncu --profile-from-start off` launch lists and single-kernel captures.
 
     python tools/profile_step.py [--b 32] [--sm 132] [--model gpt2-small] [--stage 2]
@@ -10,7 +10,8 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from paper_2408_12596_b200.runtime import Runtime, MODELS  # noqa: E402
+from paper_2408_12596_b200.models import MODELS  # noqa: E402
+from paper_2408_12596_b200.runtime import Runtime  # noqa: E402
 
 
 def main():
