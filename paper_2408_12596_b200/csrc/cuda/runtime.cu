@@ -327,6 +327,9 @@ struct Runtime {
   // NVLink peer-memory collectives (peer.h): every rank's arena and flag block mapped here
   PeerView pv;
   bool peer = false;
+  // Z3 gathers are peer-load kernels only (no copy-engine pulls / prefetch): ranks that share one
+  // process (the device-seam backend), or ZP_Z3_KERNEL_GATHER=1
+  bool kernel_gathers = false;
   uint32_t epoch = 0;
   PeerFlags* flags = nullptr;
   std::vector<void*> ipc_open;
@@ -692,7 +695,7 @@ struct Runtime {
       CK(cudaStreamWaitEvent(st, ev_done[b], 0));
       buf_pending[b] = false;
     }
-    if (z3_fresh) {
+    if (z3_fresh || kernel_gathers) {
       CK(peer_all_gather(pv, off(p16s + shoff[g]), gather_dst(g), G.len / n, ++epoch, ctas, st));
       z3_fresh = false;
       z3_note(g);
@@ -702,7 +705,7 @@ struct Runtime {
     }
     tm.close(kind, s0, st);
     const int nx = kind == kAgB ? g - 1 : g + 1;  // next layer group in issue order
-    if (nx >= 1 && nx <= c.n_layer && buf_holds[(nx - 1) & 1] != nx) {
+    if (!kernel_gathers && nx >= 1 && nx <= c.n_layer && buf_holds[(nx - 1) & 1] != nx) {
       const int nb = (nx - 1) & 1;
       CK(cudaEventRecord(ev_free, st));
       CK(cudaStreamWaitEvent(cst, ev_free, 0));
@@ -986,6 +989,7 @@ struct Runtime {
       }
       if (!ok) break;
       if (all[j].pid == mine.pid) {  // same process: direct peer access to the raw allocation
+        kernel_gathers = true;
         if (all[j].device == d.device) {
           ok = 0;  // two ranks on one GPU in one process are not supported
           break;
@@ -1020,6 +1024,8 @@ struct Runtime {
       close_peers();
       return;
     }
+    const char* kg = std::getenv("ZP_Z3_KERNEL_GATHER");
+    if (kg && kg[0] == '1') kernel_gathers = true;
     CK(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ev_free, cudaEventDisableTiming));
     for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -417,6 +417,11 @@ def product() -> HostAPI:
     """The product library (libzp.so)."""
     global _product
     if _product is None:
-        from . import _lib
-        _product = HostAPI(_lib.lib, "zp_")
+        import os
+        alt = os.environ.get("ZP_HOST_LIB")  # sanitizer build of the host code (tools/sanitize)
+        if alt:
+            _product = HostAPI(C.CDLL(alt), "zp_")
+        else:
+            from . import _lib
+            _product = HostAPI(_lib.lib, "zp_")
     return _product
