@@ -15,6 +15,7 @@
 //              reused in place (S^T -> P^T, dP^T -> dS'^T -> dQ), see the kernel's comment.
 // Plus D = rowsum(dO * O) (attn_dvec_kernel) and the fp32 dQ -> bf16 cast (attn_dq_cast_kernel).
 #include <cmath>
+#include <cstdlib>
 
 #include "attention.h"
 #include "kernels.h"
@@ -831,6 +832,7 @@ constexpr int kD2 = 128;
 constexpr int kBlk = kT * 64 * 2;  // [128, 64] bf16 SWIZZLE_128B block = 16 KiB
 constexpr int kTile2 = 2 * kBlk;   // [128, 128] tile (two blocks along the head dim)
 constexpr int kF2Threads = 18 * 32;
+constexpr int kFwdPolyDefault = 0;  // exponential pairs per 4 on the FMA pipe (ZP_ATTN_POLY overrides)
 constexpr int kF2Producer = 16, kF2Mma = 17;
 
 struct F2Smem {
@@ -850,6 +852,10 @@ __device__ __forceinline__ uint64_t kdesc128(uint32_t base, int k16) {
   return ptx::smem_desc_sw128(base + (k16 >> 2) * kBlk + (k16 & 3) * 32, 16, 1024);
 }
 
+// POLY: how many of every 4 exponential pairs run on the FMA pipe (ex2_poly) instead of MUFU. At
+// head_dim 128 a tile's 16384 exponentials take as long on MUFU (16/clk/SM) as its two 128-wide
+// products take on the tensor pipe, so moving a share to the FMA pipe shortens the softmax phase.
+template <int POLY>
 __global__ void __launch_bounds__(kF2Threads, 1)
     attn_fwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, bf16* __restrict__ out,
                          float* __restrict__ lse, int seq, int heads, int nz, float scale_log2) {
@@ -1065,7 +1071,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 64; i += 2) {
-          const float p0 = ex2(fmaf(sv[i], scale_log2, -m)), p1 = ex2(fmaf(sv[i + 1], scale_log2, -m));
+          const bool poly = ((i >> 1) & 3) < POLY;
+          const float x0 = fmaf(sv[i], scale_log2, -m), x1 = fmaf(sv[i + 1], scale_log2, -m);
+          const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
           ps[(i >> 1) & 7] += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
@@ -1134,6 +1142,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 //   ST [0,128)   S^T, then P^T packed (each query half over its own S^T columns)
 //   DP [128,256) dP^T, then dS'^T packed (likewise), then dQ = dS' K (fp32, queries on the lanes)
 //   DV [256,384), DK [384,512) the task's accumulators.
+// Task order: groups of kGroupZ (sample, head) pairs, key tile 0 (the longest) first within a
+// group, dealt round-robin to the CTAs: the key tiles in flight share their heads' Q / dO tiles
+// and dQ rows in L2 instead of streaming every head's from DRAM.
 // MMA issue order per tile: dV(i) | S^T(i+1) | dK(i) | dQ(i) | dP^T(i+1): S^T of the next tile is
 // issued as soon as dV has consumed P^T (the tensor pipe executes in order), so the eight builder
 // warps compute the next tile's exponentials while dK / dQ run; dP^T(i+1) waits until the four dQ
@@ -1221,7 +1232,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       int stage = 0;
       uint32_t phase = 0, item = 0;
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
-        const AttnTask tk = bwd_task_static(t, nz);
+        const AttnTask tk = group_task(t, nz, nt, false);
         const int smp = tk.z / heads, head = tk.z % heads;
         const int row0 = smp * seq;
         ptx::mbar_wait(kv_empty, (item & 1) ^ 1);
@@ -1277,7 +1288,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       };
       auto tcol = [](int k) { return uint32_t(k < 4 ? 8 * k : 64 + 8 * (k - 4)); };  // packed query columns
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
-        const AttnTask tk = bwd_task_static(t, nz);
+        const AttnTask tk = group_task(t, nz, nt, false);
         const int n = nt - tk.tile;  // query tiles of this key tile
         ptx::mbar_wait(kv_full, item & 1);
         issue_st(it);
@@ -1319,7 +1330,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     const float sl2 = scale * kLog2e;
     uint32_t it = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-      const AttnTask tk = bwd_task_static(t, nz);
+      const AttnTask tk = group_task(t, nz, nt, false);
       for (int i = tk.tile; i < nt; ++i, ++it) {
         const float* ld = reinterpret_cast<const float*>(sm + B2Smem::kLD + (it & 1) * 1024);
         ptx::mbar_wait(s_full, it & 1);  // S^T(i) landed; Q(i) / LSE(i) are in this stage
@@ -1384,7 +1395,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     uint8_t* stg = sm + B2Smem::kDS + q4 * (2 * 32 * 32 * 4);  // two [32 x 32] fp32 boxes per warp
     uint32_t it = 0, item = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
-      const AttnTask tk = bwd_task_static(t, nz);
+      const AttnTask tk = group_task(t, nz, nt, false);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
         ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; dS' shared memory consumed
@@ -1575,11 +1586,18 @@ int device_sms() {
 
 cudaError_t attention_fwd_d128(const bf16* qkv, bf16* out, float* lse, int64_t batch, int seq, int heads,
                                int ctas, cudaStream_t s) {
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = std::getenv("ZP_ATTN_POLY");
+    poly = e ? std::max(0, std::min(2, std::atoi(e))) : kFwdPolyDefault;
+  }
+  auto kern = poly == 0 ? attn_fwd_d128_kernel<0> : poly == 1 ? attn_fwd_d128_kernel<1> : attn_fwd_d128_kernel<2>;
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         F2Smem::kBytes);
-    if (e != cudaSuccess) return e;
+    for (auto k : {attn_fwd_d128_kernel<0>, attn_fwd_d128_kernel<1>, attn_fwd_d128_kernel<2>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, F2Smem::kBytes);
+      if (e != cudaSuccess) return e;
+    }
   }
   CUtensorMap m;
   const int h = heads * kD2;
@@ -1589,7 +1607,7 @@ cudaError_t attention_fwd_d128(const bf16* qkv, bf16* out, float* lse, int64_t b
   const int ntasks = nb * nz;
   const int grid = std::min(ntasks, ctas > 0 ? std::min(ctas, device_sms()) : device_sms());
   const float scale_log2 = (1.0f / std::sqrt(float(kD2))) * kLog2e;
-  attn_fwd_d128_kernel<<<grid, kF2Threads, F2Smem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
+  kern<<<grid, kF2Threads, F2Smem::kBytes, s>>>(m, out, lse, seq, heads, nz, scale_log2);
   note_launch();
   return cudaGetLastError();
 }
