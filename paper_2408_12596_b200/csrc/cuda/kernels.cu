@@ -810,7 +810,10 @@ __global__ void colsum_part_k(const bf16* X, int64_t rows, int N, int ld, int64_
 
 // out[c] = sum over k of part[k, c]: block (32 columns x 8 row stripes), coalesced 128-byte rows.
 // 32 columns per CTA, 32 row groups: a few independent loads per thread (latency-bound size)
-__global__ void __launch_bounds__(1024) sum_partials_k(const float* part, int nparts, int N, bf16* out) {
+// Column sums of nparts partial rows: out[c] (bf16) = sum, or, with out32, out32[c] = (acc32 ?
+// out32[c] : 0) + sum (a gradient written straight into the fp32 accumulator).
+__global__ void __launch_bounds__(1024) sum_partials_k(const float* part, int nparts, int N, bf16* out,
+                                                       float* out32, int acc32) {
   __shared__ float sh[32][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
   float s0 = 0.f, s1 = 0.f;
@@ -828,7 +831,10 @@ __global__ void __launch_bounds__(1024) sum_partials_k(const float* part, int np
     float s = 0.f;
 #pragma unroll
     for (int k = 0; k < 32; ++k) s += sh[k][threadIdx.x];
-    out[c] = __float2bfloat16_rn(s);
+    if (out32)
+      out32[c] = acc32 ? out32[c] + s : s;
+    else
+      out[c] = __float2bfloat16_rn(s);
   }
 }
 
@@ -1128,7 +1134,7 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
   if (smem <= 200 * 1024) {
     // one pass; as many CTAs per SM slot of the budget as shared memory allows
     const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, 227 * 1024 / (smem + 1024))));  // 2: registers
-    int grid = int(std::min<int64_t>(int64_t(ctas) * per_sm, (rows + 63) / 64));
+    int grid = int(std::min<int64_t>(int64_t(ctas) * per_sm, (rows + 31) / 32));
     if (grid < 1) grid = 1;
     const int64_t chunk = (rows + grid - 1) / grid;
     grid = int((rows + chunk - 1) / chunk);
@@ -1214,7 +1220,7 @@ void cross_entropy_fwd_bwd(bf16* logits, const int32_t* tokens, int seq, int64_t
 }
 
 void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* out, int ctas,
-                 cudaStream_t s) {
+                 cudaStream_t s, float* out32, bool acc32) {
   const int col_blocks = (N + 255) / 256;
   int chunks = (ctas * 4 + col_blocks - 1) / col_blocks;
   if (chunks < 1) chunks = 1;
@@ -1222,10 +1228,10 @@ void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* 
   const int64_t chunk = (rows + chunks - 1) / chunks;
   chunks = int((rows + chunk - 1) / chunk);
   colsum_part_k<<<dim3(col_blocks, chunks), dim3(32, 8), 0, s>>>(X, rows, N, ld, chunk, work); note_launch();
-  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(work, chunks, N, out); note_launch();
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(work, chunks, N, out, out32, acc32 ? 1 : 0); note_launch();
 }
-void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s) {
-  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(part, nparts, N, out); note_launch();
+void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s, float* out32, bool acc32) {
+  sum_partials_k<<<(N + 31) / 32, dim3(32, 32), 0, s>>>(part, nparts, N, out, out32, acc32 ? 1 : 0); note_launch();
 }
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s) {
   cast_k<<<grid_for(n / 4 + 1, kThreads, ctas), kThreads, 0, s>>>(in, out, n); note_launch();

@@ -58,10 +58,12 @@ void swiglu_bwd(const bf16* gu, const bf16* dh, bf16* dgu, int64_t tokens, int f
 void embed_bwd(const int32_t* tokens, int seq, const bf16* dx, float* dwte32, float* dwpe32,
                int64_t rows, int h, int ctas, cudaStream_t s);
 // out[n] = sum over rows of X[r, n] (X bf16 [rows, ld]); partial workspace [chunks][N] f32.
+// out32 (optional): write / add (acc32) the fp32 sums there instead of bf16 to out
 void colsum_bf16(const bf16* X, int64_t rows, int N, int ld, float* work, bf16* out, int ctas,
-                 cudaStream_t s);
+                 cudaStream_t s, float* out32 = nullptr, bool acc32 = false);
 // out[n] = sum over k of part[k, n] (f32), written as bf16.
-void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s);
+void sum_partials(const float* part, int nparts, int N, bf16* out, cudaStream_t s, float* out32 = nullptr,
+                  bool acc32 = false);
 void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t s);
 
 // ---- ZeRO reduce / update

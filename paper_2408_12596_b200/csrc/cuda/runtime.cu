@@ -407,6 +407,34 @@ struct Runtime {
                      : (t.group == int(lay.groups.size()) - 1 ? gb_fin : gb_layer[(t.group - 1) & 1]);
     return base + (t.off - G.start);
   }
+  // Gradient destination of a tensor. When the rank's fp32 accumulator covers every parameter it
+  // computes (ZeRO-0/1, or a single rank) the gradient producers write the first micro-step's
+  // gradient straight into it and add the later ones (GEMM fp32 epilogues, fp32 column sums), so
+  // no bf16 gradient buffer and no per-micro-step accumulation pass exist; otherwise they write
+  // bf16 (Gp) for the stage's reduce-scatter.
+  struct GradDst {
+    bf16* b16;
+    float* f32;
+    bool first;
+  };
+  bool direct = false;  // set by configure(): stage <= 1 || n == 1
+  bool gfirst = true;   // the current micro-step is the iteration's first with local work
+  GradDst Gd(const Tensor& t) const {
+    if (direct) return {nullptr, acc + t.off, gfirst};
+    return {Gp(t), nullptr, false};
+  }
+  void grad_partials(const float* part, int nparts, int N, GradDst d) {
+    sum_partials(part, nparts, N, d.b16, st, d.f32, d.f32 && !d.first);
+  }
+  // an fp32 gradient computed in a workspace (embedding tables): cast, or copy / add into acc
+  void grad_from_f32(const float* src, int64_t n, GradDst d) {
+    if (!d.f32)
+      cast_f32_bf16(src, d.b16, n, ctas, st);
+    else if (d.first)
+      CK(cudaMemcpyAsync(d.f32, src, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+    else
+      add_f32(d.f32, src, n, ctas, st);
+  }
   bf16* Gp(const Tensor& t) const {
     if (stage != 3) return g16 + t.off;
     if (n == 1) return r16 + t.off;
@@ -448,12 +476,23 @@ struct Runtime {
   // across CTAs (fp32 atomics into a workspace, then a cast) when the tiles cannot fill the
   // rank's SMs.
   void wgrad(int M, int N, int64_t T, const bf16* A, int64_t lda, const bf16* B, int64_t ldb,
-             bf16* dst) {
+             GradDst d) {
     const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
     const int64_t tiles = int64_t((M + 127) / 128) * ((N + bn - 1) / bn);
     const int64_t kblocks = (T + 63) / 64;
     int split = 1;
     if (tiles < ctas) split = int(std::min<int64_t>((ctas + tiles - 1) / tiles, std::max<int64_t>(1, kblocks / 16)));
+    if (d.f32) {  // straight into the fp32 accumulator
+      if (split <= 1) {
+        mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, d.f32, N, d.first ? kEpiStoreF32 : kEpiAccumF32);
+      } else {
+        if (d.first) CK(cudaMemsetAsync(d.f32, 0, size_t(M) * N * 4, st));
+        mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, d.f32, N, kEpiAtomicF32, 1.f, nullptr, nullptr, nullptr,
+           -1);
+      }
+      return;
+    }
+    bf16* dst = d.b16;
     if (split <= 1) {
       mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, dst, N, kEpiStoreBf16);
       return;
@@ -534,9 +573,10 @@ struct Runtime {
     gb_layer[0] = gb_layer[1] = nullptr;
     acc = r32 = nullptr;
     const int64_t SL = new_stage == 0 ? T : S;
+    direct = new_stage <= 1 || n == 1;  // gradients accumulate straight into the fp32 accumulator
     if (new_stage <= 2) {
       p16 = B16(T, "bf16 params");
-      g16 = B16(T, "bf16 grads");
+      if (!direct) g16 = B16(T, "bf16 grads");
     } else {
       p16s = B16(S, "bf16 param shard");
       if (n > 1) {
@@ -554,7 +594,7 @@ struct Runtime {
     if (new_stage == 1) r32 = F32(S, "rs shard");
     if (new_stage >= 2) {
       acc = F32(S, "grad accumulator shard");
-      r16 = B16(S, "rs shard");
+      if (!direct) r16 = B16(S, "rs shard");
     }
     gkeep = keep_grads ? F32(SL, "kept grads") : nullptr;
     const int64_t h = c.d_model;
@@ -734,10 +774,7 @@ struct Runtime {
   }
   // A rank with no samples in a ZeRO-3 micro-step still joins every collective, with zeros.
   void z3_idle_step() {
-    if (n == 1) {
-      CK(cudaMemsetAsync(r16, 0, size_t(shard()) * 2, st));
-      return;
-    }
+    if (n == 1) return;  // one rank: nothing to join, its gradients live in the accumulator
     const int G = int(lay.groups.size());
     CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
     for (int g = 0; g < G; ++g) z3_gather(g, kAgF);
@@ -783,8 +820,8 @@ struct Runtime {
 
   void ln_grads(const Tensor& g, const Tensor& b, int nblk) {
     const int h = c.d_model;
-    sum_partials(ln_part, nblk, h, Gp(g), st);
-    sum_partials(ln_part + int64_t(nblk) * h, nblk, h, Gp(b), st);
+    grad_partials(ln_part, nblk, h, Gd(g));
+    grad_partials(ln_part + int64_t(nblk) * h, nblk, h, Gd(b));
   }
 
   // ---------------------------------------------------------------- Llama family
@@ -824,10 +861,10 @@ struct Runtime {
     z3_clear_group(NG - 1);
     // untied LM head: dlnf = dlogits * W_head ; dW_head = dlogits^T * lnf
     mm(T, h, vocab_pad, A.logits, kKMajor, vocab_pad, Wp(lay.lm_head), kMNMajor, h, A.dln, h, kEpiStoreBf16);
-    wgrad(vocab_pad, int(h), T, A.logits, vocab_pad, A.lnf, h, Gp(lay.lm_head));
+    wgrad(vocab_pad, int(h), T, A.logits, vocab_pad, A.lnf, h, Gd(lay.lm_head));
     CK(layernorm_bwd(A.dln, A.x_final, A.muf, A.rsf, Wp(lay.lnf_g), nullptr, A.dx, ln_part, &nblk, T, int(h), ctas,
                      st, true));
-    sum_partials(ln_part, nblk, int(h), Gp(lay.lnf_g), st);
+    grad_partials(ln_part, nblk, int(h), Gd(lay.lnf_g));
     z3_reduce(NG - 1);
     for (int i = c.n_layer - 1; i >= 0; --i) {
       const LayerP& P = lay.layers[i];
@@ -835,30 +872,30 @@ struct Runtime {
       z3_gather(i + 1, kAgB);
       z3_clear_group(i + 1);
       // MLP: down projection, SwiGLU, gate/up projection
-      wgrad(int(h), int(f), T, A.dx, h, L.g, f, Gp(P.w_down));
+      wgrad(int(h), int(f), T, A.dx, h, L.g, f, Gd(P.w_down));
       mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_down), kMNMajor, f, A.dh, f, kEpiStoreBf16);
       swiglu_bwd(L.u, A.dh, A.du, T, int(f), ctas, st);
-      wgrad(int(2 * f), int(h), T, A.du, 2 * f, L.ln2, h, Gp(P.w_gu));
+      wgrad(int(2 * f), int(h), T, A.du, 2 * f, L.ln2, h, Gd(P.w_gu));
       mm(T, h, 2 * f, A.du, kKMajor, 2 * f, Wp(P.w_gu), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h), ctas, st,
                        true));
-      sum_partials(ln_part, nblk, int(h), Gp(P.ln2_g), st);
+      grad_partials(ln_part, nblk, int(h), Gd(P.ln2_g));
       // attention
-      wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gp(P.w_o));
+      wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gd(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
       CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd()));
       rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st, hd());  // back to pre-rotation Q, K
-      wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
+      wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gd(P.w_qkv));
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h), ctas, st,
                        true));
-      sum_partials(ln_part, nblk, int(h), Gp(P.ln1_g), st);
+      grad_partials(ln_part, nblk, int(h), Gd(P.ln1_g));
       z3_reduce(i + 1);
     }
     z3_clear_group(0);
     CK(cudaMemsetAsync(dwte32, 0, size_t(vocab_pad) * h * 4, st));
     embed_bwd(tok, int(s), A.dx, dwte32, nullptr, T, int(h), ctas, st);
-    cast_f32_bf16(dwte32, Gp(lay.wte), int64_t(vocab_pad) * h, ctas, st);
+    grad_from_f32(dwte32, int64_t(vocab_pad) * h, Gd(lay.wte));
     z3_reduce(0);
   }
 
@@ -885,27 +922,30 @@ struct Runtime {
       z3_gather(i + 1, kAgB);
       z3_clear_group(i + 1);
       // MLP
-      sum_partials(cs_part, ncs, int(h), Gp(P.b_proj), st);
-      wgrad(h, f, T, A.dx, h, L.g, f, Gp(P.w_proj));
+      grad_partials(cs_part, ncs, int(h), Gd(P.b_proj));
+      wgrad(h, f, T, A.dx, h, L.g, f, Gd(P.w_proj));
       // dgrad through GELU'; its epilogue also sums the columns of du (the b_fc gradient)
       CK(cudaMemsetAsync(col_work, 0, size_t(f) * 4, st));
       mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_proj), kMNMajor, f, A.du, f, kEpiGeluBwdBf16, 1.f, nullptr, L.u, nullptr,
          1, col_work);
-      sum_partials(col_work, 1, int(f), Gp(P.b_fc), st);
-      wgrad(f, h, T, A.du, f, L.ln2, h, Gp(P.w_fc));
+      grad_partials(col_work, 1, int(f), Gd(P.b_fc));
+      wgrad(f, h, T, A.du, f, L.ln2, h, Gd(P.w_fc));
       mm(T, h, f, A.du, kKMajor, f, Wp(P.w_fc), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h),
                        ctas, st, false, cs_part));
       ln_grads(P.ln2_g, P.ln2_b, nblk);
       // attention output projection
-      sum_partials(cs_part, nblk, int(h), Gp(P.b_o), st);
-      wgrad(h, h, T, A.dx2, h, L.attn, h, Gp(P.w_o));
+      grad_partials(cs_part, nblk, int(h), Gd(P.b_o));
+      wgrad(h, h, T, A.dx2, h, L.attn, h, Gd(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
       // fused attention backward (recomputes P from the saved LSE)
       CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd()));
       // QKV projection
-      colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, Gp(P.b_qkv), ctas, st);
-      wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gp(P.w_qkv));
+      {
+        const GradDst d = Gd(P.b_qkv);
+        colsum_bf16(A.dqkv, T, int(3 * h), int(3 * h), col_work, d.b16, ctas, st, d.f32, d.f32 && !d.first);
+      }
+      wgrad(3 * h, h, T, A.dqkv, 3 * h, L.ln1, h, Gd(P.w_qkv));
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h),
                        ctas, st, false, i > 0 ? cs_part : nullptr));
@@ -916,8 +956,8 @@ struct Runtime {
     CK(cudaMemsetAsync(dwpe32, 0, size_t(c.seq_len) * h * 4, st));
     z3_clear_group(0);
     embed_bwd(tok, int(s), A.dx, dwte32, dwpe32, T, int(h), ctas, st);
-    cast_f32_bf16(dwte32, Gp(lay.wte), int64_t(vocab_pad) * h, ctas, st);
-    cast_f32_bf16(dwpe32, Gp(lay.wpe), int64_t(c.seq_len) * h, ctas, st);
+    grad_from_f32(dwte32, int64_t(vocab_pad) * h, Gd(lay.wte));
+    grad_from_f32(dwpe32, int64_t(c.seq_len) * h, Gd(lay.wpe));
     z3_reduce(0);
   }
 
@@ -1091,6 +1131,7 @@ struct Runtime {
       }
       const bool last = (k + 1 == steps.size());
       z3_first = (k == 0);
+      gfirst = !any_local;
       if (b > 0) {
         const int32_t* tok = tokens + sample * (c.seq_len + 1);
         const int f0 = tm.mark(st);
@@ -1106,27 +1147,23 @@ struct Runtime {
         reduce_sum_f32(A.row_loss, b * c.seq_len, loss_steps + k, st);
         sample += b;
         ++active;
-      } else if (stage == 2) {
+      } else if (stage == 2 && !direct) {
         CK(cudaMemsetAsync(g16, 0, size_t(total) * 2, st));  // joins the collective with zeros
       } else if (stage == 3) {
         z3_idle_step();  // gathers and zero-gradient reduce-scatters, same order as a real step
       }
-      if (stage <= 1) {
-        if (b > 0) {
-          accumulate_bf16(acc, g16, total, !any_local, ctas, st);
-          any_local = true;
-        }
+      if (direct) {  // the backward wrote / added this micro-step's gradient into acc
+        if (b > 0) any_local = true;
       } else if (stage == 2 && peer) {  // Z2 over NVLink: pull-reduce into the fp32 shard
         if (!last) peer_reduce_accumulate(k == 0);
       } else if (stage == 2) {  // Z2: reduce-scatter every micro-step
-        bf16* src = (n == 1) ? g16 : r16;
         reduce_scatter_bf16(g16, r16);
-        if (!last) accumulate_bf16(acc, src, sh, k == 0, ctas, st);
-      } else if (!(peer && n > 1)) {  // Z3: the per-group reduce-scatters landed in r16 in backward
+        if (!last) accumulate_bf16(acc, r16, sh, k == 0, ctas, st);
+      } else if (!peer) {  // Z3 over NCCL: the per-group reduce-scatters landed in r16 in backward
         if (!last) accumulate_bf16(acc, r16, sh, k == 0, ctas, st);
       }
     }
-    if (stage <= 1 && !any_local) CK(cudaMemsetAsync(acc, 0, size_t(total) * 4, st));
+    if (direct && !any_local) CK(cudaMemsetAsync(acc, 0, size_t(state_len()) * 4, st));
 
     // ---- synchronisation point + optimizer
     const AdamParams ap = adam_params();
@@ -1156,9 +1193,10 @@ struct Runtime {
       tm.close(kOpt, o0, st);
       all_gather_params();
     } else {
-      const bool z3peer = stage == 3 && peer;  // every micro-step already summed into acc (fp32)
-      const bf16* g = z3peer ? nullptr : ((stage == 2 && n == 1) ? g16 : r16);
-      const float* a = (steps.size() > 1 || z3peer) ? acc : nullptr;
+      // every micro-step already summed into acc (fp32): one rank (direct) or the Z3 NVLink path
+      const bool in_acc = direct || (stage == 3 && peer);
+      const bf16* g = in_acc ? nullptr : r16;
+      const float* a = (steps.size() > 1 || in_acc) ? acc : nullptr;
       if (gkeep) {
         if (g) {
           accumulate_bf16(gkeep, g, L, true, ctas, st);
