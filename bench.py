@@ -474,7 +474,10 @@ def main():
         nvl_bytes = shard * (world - 1) * (gb + 2)
         adam_s = last_timing["sync"]
     else:
-        gbytes = 4 if stage <= 1 else (2 + (4 if steps_r > 1 else 0))
+        # gradient read: the fp32 accumulator only when it holds every micro-step (ZeRO-0/1, one
+        # rank, or ZeRO-3 over NVLink); else the last micro-step's bf16 shard (+ the accumulator)
+        in_acc = stage <= 1 or world == 1 or (stage == 3 and rt.peer_collectives())
+        gbytes = 4 if in_acc else (2 + (4 if steps_r > 1 else 0))
         adam_bytes = shard * (26 + gbytes)
         nvl_bytes = 0
         adam_s = last_timing["optimizer"]

@@ -483,12 +483,14 @@ struct Runtime {
     int split = 1;
     if (tiles < ctas) split = int(std::min<int64_t>((ctas + tiles - 1) / tiles, std::max<int64_t>(1, kblocks / 16)));
     if (d.f32) {  // straight into the fp32 accumulator
-      if (split <= 1) {
-        mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, d.f32, N, d.first ? kEpiStoreF32 : kEpiAccumF32);
+      if (d.first && split <= 1) {
+        mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, d.f32, N, kEpiStoreF32);
       } else {
+        // later micro-steps add with fire-and-forget vector reductions (the L2 does the
+        // read-modify-write; an epilogue that read C back would stall on every tile)
         if (d.first) CK(cudaMemsetAsync(d.f32, 0, size_t(M) * N * 4, st));
         mm(M, N, int(T), A, kMNMajor, lda, B, kMNMajor, ldb, d.f32, N, kEpiAtomicF32, 1.f, nullptr, nullptr, nullptr,
-           -1);
+           split > 1 ? -1 : 1);
       }
       return;
     }
