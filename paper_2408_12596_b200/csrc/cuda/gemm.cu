@@ -48,7 +48,6 @@ struct TileInfo {
 struct Sched {
   int m_tiles, n_tiles, nb1, total, split_k;
   int M, N, K, BN, causal, tile_m;  // tile_m = 128 * CTA-group size
-  int group_n;  // 1: runs of kGroupM n-tiles sweep the m-tiles (B larger than A)
   __device__ TileInfo tile(int unit) const {
     TileInfo ti;
     const int split = unit % split_k;
@@ -59,24 +58,11 @@ struct Sched {
     // grouped raster: runs of kGroupM m-tiles sweep the n-tiles together, so the tiles in flight
     // at any time share a few A row-blocks and B column-blocks (L2 reuse for large N, e.g. the
     // LM head)
-    // The operand that is swept is re-read once per run: it should be the smaller one, which stays
-    // in L2, while every tile of the larger one is read from DRAM once. With B larger (N > M, e.g.
-    // a 7B model's LM head or gate/up weights against an 8192-token micro-batch) the runs are
-    // groups of n-tiles sweeping the m-tiles instead.
-    int mb, nb;
-    if (group_n) {
-      const int first_n = (r / (kGroupM * m_tiles)) * kGroupM;
-      const int gsize = min(kGroupM, n_tiles - first_n);
-      const int rr = r - first_n * m_tiles;
-      nb = first_n + rr % gsize;
-      mb = rr / gsize;
-    } else {
-      const int first_m = (r / (kGroupM * n_tiles)) * kGroupM;
-      const int gsize = min(kGroupM, m_tiles - first_m);
-      const int rr = r - first_m * n_tiles;
-      mb = first_m + rr % gsize;
-      nb = rr / gsize;
-    }
+    const int first_m = (r / (kGroupM * n_tiles)) * kGroupM;
+    const int gsize = min(kGroupM, m_tiles - first_m);
+    const int rr = r - first_m * n_tiles;
+    const int mb = first_m + rr % gsize;
+    const int nb = rr / gsize;
     ti.z1 = z % nb1;
     ti.z2 = z / nb1;
     ti.m0 = mb * tile_m;
@@ -780,7 +766,6 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   s.m_tiles = (a.M + s.tile_m - 1) / s.tile_m;
   s.n_tiles = (a.N + BN - 1) / BN;
   s.nb1 = a.nb1;
-  s.group_n = (a.N > a.M && a.causal == kCausalNone) ? 1 : 0;
   int ctas = num_sms();
   if (a.max_ctas > 0 && a.max_ctas < ctas) ctas = a.max_ctas;
   const int workers = ctas / CG;  // persistent CTAs (pairs)
