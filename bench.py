@@ -6,7 +6,7 @@
 
 Default workload: the largest BASELINE.json configuration that fits one B200 — C5, a
 Llama-style 7B (L32 h4096 ffn11008 V32000, s=4096) at ZeRO-3 bf16, ranks cycling the SM tiers
-148 / 104 / 74 SMs and HBM caps 180 / 96 GB (rank 0: 148 SMs, full HBM), global batch 16*N
+148 / 104 / 74 SMs and HBM caps 180 / 96 GB (rank 0: 148 SMs, full HBM), global batch 32*N
 samples (weak scaling). `--config c1..c4` select the other BASELINE configs (C2 = GPT-2 small
 ZeRO-2 at 132 / 66 SMs, the round-1 headline).
 
@@ -58,7 +58,7 @@ CONFIGS = {
     "c4": dict(model="llama-1.3b", stage=3, tiers=[148, 148, 74, 148, 74, 148, 74, 148], caps=[0],
                gbs_per_gpu=128, label="C4: Llama-style 1.3B s2048, ZeRO-3 bf16, 5 fast (148 SM) + 3 slow (74 SM)"),
     "c5": dict(model="llama-7b", stage=3, tiers=[148, 104, 74, 148, 104, 74, 148, 74], caps=[0, 0, 0, 96],
-               gbs_per_gpu=16, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/96 GB"),
+               gbs_per_gpu=32, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/96 GB"),
 }
 DEFAULT_CONFIG = "c5"
 
@@ -435,12 +435,13 @@ def main():
         import torch
         s1 = model.seq_len + 1
         host = torch.randint(0, model.vocab, (max(count, 1), s1), dtype=torch.int32).pin_memory()
-        T_e2e, _ = timed(args.steps, plan, host_tokens=(host.data_ptr(), max(count, 1)))
+        ke = max(1, min(args.steps, 5))  # iterations are seconds long: five end-to-end ones suffice
+        T_e2e, _ = timed(ke, plan, host_tokens=(host.data_ptr(), max(count, 1)))
         rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
         h2d = sum(allgather(count * s1 * 4))
         d2h = 4 * sum(rank_micro_steps(plan, r, stage) for r in range(world))  # per-step loss read-back
-        e2e = {"value": args.steps * gbs / T_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        e2e = {"value": ke * gbs / T_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": ke}
 
     # Heterogeneity-blind baseline (equal split) on the same devices
     rt.load_tokens(first_sample=poplar.rank_slice(uniform, rank)[0],

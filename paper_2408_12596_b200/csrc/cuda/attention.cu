@@ -1172,7 +1172,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                          const __grid_constant__ CUtensorMap map_dq, const float* __restrict__ lse,
                          const float* __restrict__ dvec, bf16* __restrict__ dqkv, int seq, int heads, int nz,
-                         float scale) {
+                         float scale, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // the SWIZZLE_128B tiles need 1 KiB alignment
   uint8_t* sm = smem_raw;
@@ -1423,7 +1423,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_reduce_add_2d(&map_dq, box, head * kD2 + 32 * c, row);
+            if (!(dbg & 1)) ptx::tma_reduce_add_2d(&map_dq, box, head * kD2 + 32 * c, row);
             ptx::bulk_commit();
           }
         }
@@ -1655,8 +1655,10 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
   const float scale = 1.0f / std::sqrt(float(kD2));
+  static int dbg = -1;  // diagnostics (ZP_ATTN_DBG): bit 0 = skip the dQ reduce-add
+  if (dbg < 0) dbg = std::getenv("ZP_ATTN_DBG") ? std::atoi(std::getenv("ZP_ATTN_DBG")) : 0;
   attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, mdq, lse, dvec, dqkv, seq,
-                                                                                heads, nz, scale);
+                                                                                heads, nz, scale, dbg);
   note_launch();
   attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h, scale);
   note_launch();

@@ -97,6 +97,9 @@ struct Tensor {
 // rank r owns the r-th equal slice of every group.
 struct Group {
   int64_t start = 0, len = 0;
+  // [begin, end) ranges of the group (relative to start) that no tensor covers: alignment and
+  // shard padding, the only elements of a group gradient the backward never writes
+  std::vector<std::pair<int64_t, int64_t>> gaps;
 };
 struct LayerP {
   Tensor ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_fc, b_fc, w_proj, b_proj;
@@ -116,8 +119,11 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
   const int64_t unit = int64_t(world) * 256;
   auto open_group = [&]() { L.groups.push_back(Group{cur, 0}); };
   auto close_group = [&]() {
-    cur = round_up(cur, unit);
-    L.groups.back().len = cur - L.groups.back().start;
+    Group& G = L.groups.back();
+    const int64_t end = round_up(cur, unit);
+    if (end > cur) G.gaps.push_back({cur - G.start, end - G.start});
+    cur = end;
+    G.len = cur - G.start;
   };
   auto add = [&](const std::string& name, int64_t r, int64_t k, int64_t logical_rows) {
     Tensor t;
@@ -125,7 +131,9 @@ Layout make_layout(const zp_gpt_config& c, int vocab_pad, int world) {
     t.rows = r;
     t.cols = k;
     t.group = int(L.groups.size()) - 1;
-    cur = round_up(cur + r * k, 64);
+    const int64_t end = round_up(cur + r * k, 64);
+    if (end > cur + r * k) L.groups.back().gaps.push_back({cur + r * k - L.groups.back().start, end - L.groups.back().start});
+    cur = end;
     L.logical += logical_rows * k;
     L.by_name[name] = t;
     return t;
@@ -770,9 +778,11 @@ struct Runtime {
   }
   bool z3_first = true;  // ZeRO-3 peer path: the current micro-step is the iteration's first
   // Zero the reused group-gradient buffer so padding never carries another group's values.
+  // Only the group's padding: every tensor element is overwritten by its gradient producer.
   void z3_clear_group(int g) {
     if (stage != 3 || n == 1) return;
-    CK(cudaMemsetAsync(ggrp, 0, size_t(lay.groups[g].len) * 2, st));
+    for (const auto& gap : lay.groups[g].gaps)
+      CK(cudaMemsetAsync(ggrp + gap.first, 0, size_t(gap.second - gap.first) * 2, st));
   }
   // A rank with no samples in a ZeRO-3 micro-step still joins every collective, with zeros.
   void z3_idle_step() {
