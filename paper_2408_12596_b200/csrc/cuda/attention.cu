@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 // issued as soon as dV has consumed P^T (the tensor pipe executes in order), so the eight builder
 // warps compute the next tile's exponentials while dK / dQ run; dP^T(i+1) waits until the four dQ
 // warps have read dQ(i) out of TMEM. dS'^T also goes to shared memory for the dQ product (MN-major
-// A operand); the dQ warps stage dQ through the Q(i) buffer (free once tile i's products are done) and add it into fp32 dQ with TMA
+// A operand); the dQ warps stage dQ through that same region and add it into fp32 dQ with TMA
 // bulk reduce-add, then release it to the builders of the next tile.
 // Warp roles: 0-7 builders (lane quarter w % 4, query half w / 4), 8-11 dQ out + dK/dV epilogue,
 // 12 TMA producer, 13 MMA issuer. K/V single-buffered per task; Q/dO(+LSE, D) two stages.
@@ -1188,6 +1188,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
   uint64_t* ds_full = bar + 10;   // dS'^T in shared memory (builders, 256)
   uint64_t* mm_done = bar + 11;   // dQ in TMEM (MMA)
   uint64_t* dq_free = bar + 12;   // dQ read out of TMEM (dQ warps, 128)
+  uint64_t* stg_free = bar + 13;  // dQ staging drained (dQ warps, 4)
   uint64_t* acc_full = bar + 14;  // dK, dV complete (MMA)
   uint64_t* acc_free = bar + 15;  // dK, dV read out (epilogue, 128)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
@@ -1206,7 +1207,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     ptx::mbar_init(kv_empty, 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&qd_full[i], 1);
-      ptx::mbar_init(&qd_empty[i], 4);  // the dQ warps, once their staging in this Q buffer drained
+      ptx::mbar_init(&qd_empty[i], 1);
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(dp_full, 1);
@@ -1215,6 +1216,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     ptx::mbar_init(ds_full, 256);
     ptx::mbar_init(mm_done, 1);
     ptx::mbar_init(dq_free, 128);
+    ptx::mbar_init(stg_free, 4);
     ptx::mbar_init(acc_full, 1);
     ptx::mbar_init(acc_free, 128);
     ptx::fence_barrier_init();
@@ -1309,7 +1311,8 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           ptx::tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
-          ptx::umma_commit(mm_done);  // also: Q(i) / dO(i) no longer read by the tensor pipe
+          ptx::umma_commit(mm_done);
+          ptx::umma_commit(&qd_empty[it & 1]);
           if (last) {
             ptx::umma_commit(acc_full);
             ptx::umma_commit(kv_empty);
@@ -1376,8 +1379,8 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(dst_full);
-        // dS'^T into shared memory for dQ = dS' K, once dQ of the previous tile has consumed it
-        ptx::mbar_wait(mm_done, (it & 1) ^ 1);
+        // dS'^T into shared memory for dQ = dS' K, once the previous tile's dQ staging drained
+        ptx::mbar_wait(stg_free, (it & 1) ^ 1);
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           st_shared_v4(sds + p_off(r, qh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
@@ -1389,15 +1392,13 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    uint8_t* stg = sm + B2Smem::kDS + q4 * (2 * 32 * 32 * 4);  // two [32 x 32] fp32 boxes per warp
     uint32_t it = 0, item = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
       const AttnTask tk = group_task(t, nz, nt, false);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; tile i's products done with Q(i) and dO(i)
-        // stage dQ through the Q(i) buffer (free now; the producer refills it after qd_empty):
-        // two [32 x 32] fp32 boxes per warp
-        uint8_t* stg = sm + B2Smem::kQ + (it & 1) * kTile2 + q4 * (2 * 32 * 32 * 4);
+        ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; dS' shared memory consumed
         ptx::tc_fence_after();
         uint32_t v[4][32];
         ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off, v[0]);
@@ -1428,7 +1429,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         }
         if (lane == 0) {
           ptx::bulk_wait_read<0>();
-          ptx::mbar_arrive(&qd_empty[it & 1]);  // the stage (Q, dO, LSE, D) may be refilled
+          ptx::mbar_arrive(stg_free);  // the builders may write the next dS'^T over the boxes
         }
         __syncwarp();
       }
