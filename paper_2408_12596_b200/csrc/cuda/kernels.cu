@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __rest
     const bf16* da = dy + ra * h + lane * 8;
     const bf16* db = dy + rb * h + lane * 8;
     float s1a = 0.f, s2a = 0.f, s1b = 0.f, s2b = 0.f;
-#pragma unroll
+    // four column chunks per step: 16 loads in flight per lane (one 8-warp CTA per SM at wide h is
+    // otherwise latency-bound at ~0.45 of HBM)
+#pragma unroll 4
     for (int j = 0; j < nv; ++j) {
       const uint4 qxa = *reinterpret_cast<const uint4*>(xa + 256 * j);
       const uint4 qda = *reinterpret_cast<const uint4*>(da + 256 * j);
@@ -329,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __rest
     const float m2a = warp_sum(s2a) * inv_h;
     const float m1b = RMS ? 0.f : warp_sum(s1b) * inv_h;
     const float m2b = warp_sum(s2b) * inv_h;
-#pragma unroll 1
-    for (int j = 0; j < nv; ++j) {  // second pass re-reads the two rows (L1 hits)
+#pragma unroll 2
+    for (int j = 0; j < nv; ++j) {  // second pass re-reads the two rows (L1 / L2 hits)
       const int col = lane * 8 + 256 * j;
       const uint4 qxa = *reinterpret_cast<const uint4*>(xa + 256 * j);
       const uint4 qda = *reinterpret_cast<const uint4*>(da + 256 * j);
