@@ -529,7 +529,9 @@ def main():
                                   "optimizer_s": max(d["optimizer_time"] for d in profile["devices"])},
                     "measured_last_iteration": {"compute_s": m_comp, "comm_floor_s": report["comm_total"],
                                                 "optimizer_s": m_opt,
-                                                "unmodelled_s": t_last - m_comp - report["comm_total"] - m_opt}}
+                                                "unmodelled_s": t_last - m_comp - report["comm_total"] - m_opt},
+                    "per_rank_compute_s": {"predicted": [d["predicted_time"] for d in plan["devices"]],
+                                           "measured": report["compute"]}}
         try:
             ref_pred = reference_prediction(rt, profile, probes, link, gbs, stage, world)
         except Exception as e:  # the reference pipeline may reject a fitted cluster

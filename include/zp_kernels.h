@@ -62,14 +62,14 @@ int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const f
                      float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t max_ctas,
                      void* stream);
 
-/* ---- NVLink peer-memory collectives (csrc/cuda/peer.cu), drivable on ONE device for parity.
- * A peer group is n "rank arenas" given as n base pointers (any device memory the calling
- * process can address: regions of one allocation on one GPU, or peer-mapped arenas of n GPUs)
- * plus n flag blocks the group allocates (zeroed). Offsets are byte offsets from each base, the
- * same for every rank, exactly as the runtime uses them. The kernels synchronise through
- * epoch-stamped flags, so the n rank instances of one call must run CONCURRENTLY (one stream per
- * rank, `ctas` small enough that all instances are co-resident); epochs must increase by one per
- * call. Bounded spin: an instance whose peers never arrive traps after 20 s instead of hanging.
+/* ---- NVLink peer-memory collectives (csrc/cuda/peer.cu), emulated on ONE device for parity.
+ * A peer group is n "rank arenas": n equal regions of `arena_bytes` starting at `base` (device
+ * memory), plus n flag blocks the group allocates (zeroed). Every call runs ALL n rank instances
+ * of the kernel in ONE cooperative launch (blocks [r*G, (r+1)*G) are rank r), so instances that
+ * wait on one another through the epoch-stamped flags are co-resident by construction; epochs
+ * must increase by one per call. Every buffer is given as a byte offset inside the arenas, the
+ * same for every rank (rank r's lives at base + r*arena_bytes + offset), exactly as the runtime
+ * lays them out. Rank r owns shard r: elements [r*len, (r+1)*len) of the full-size buffers.
  * Reference counterpart: none (the reference models these collectives as
  * collective_time(param_count * bytes_per_param), proj/core/src/comm.cpp:88-99). */
 typedef struct zp_peer_group zp_peer_group;
@@ -77,25 +77,21 @@ typedef struct zp_adam_params {
   float lr, beta1, beta2, eps, weight_decay;
   float bc1, bc2; /* 1 - beta^t */
 } zp_adam_params;
-int zp_peer_group_create(int32_t n, void* const* bases, zp_peer_group** out);
+int zp_peer_group_create(int32_t n, void* base, int64_t arena_bytes, zp_peer_group** out);
 int zp_peer_group_destroy(zp_peer_group* g);
-/* acc[i] = (overwrite ? 0 : acc[i]) + sum_{j=0..n-1} bf16 src_j[shard_off + i] (fp32, rank order) */
-int zp_peer_rs_accumulate(zp_peer_group* g, int32_t rank, int64_t src_off, int64_t shard_off, float* acc,
-                          int64_t len, int32_t overwrite, uint32_t epoch, int32_t ctas, void* stream);
-/* g = (acc ? acc : 0) + sum_j src_j[shard_off + i] (bf16, or fp32 when src_f32); AdamW on
- * (p32, m, v); bf16(p32) pushed to element shard_off + i of every rank's p16 (byte offset p16_off);
- * gout (optional) receives g. */
-int zp_peer_rs_adam_ag(zp_peer_group* g, int32_t rank, int64_t src_off, int32_t src_f32, int64_t shard_off,
-                       const float* acc, float* p32, float* m, float* v, int64_t p16_off, float* gout,
-                       int64_t len, const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream);
-/* dst[j*len + e] = bf16 src_j[e] (byte offset shard_src_off in every arena), every rank j */
-int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_src_off, void* dst, int64_t len,
-                       uint32_t epoch, int32_t ctas, void* stream);
-
-/* Same with an explicit head_dim (64 or 128). */
-int zp_attention_bwd_hd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
-                        float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t head_dim,
-                        int32_t max_ctas, void* stream);
+/* rank r: acc_r[i] = (overwrite ? 0 : acc_r[i]) + sum_{j=0..n-1} bf16 src_j[r*len + i] (fp32, rank
+ * order); src: bf16 [n*len] at src_off; acc: fp32 [len] at acc_off */
+int zp_peer_rs_accumulate(zp_peer_group* g, int64_t src_off, int64_t len, int64_t acc_off, int32_t overwrite,
+                          uint32_t epoch, int32_t ctas, void* stream);
+/* rank r: grad[i] = (acc_off >= 0 ? acc_r[i] : 0) + sum_j src_j[r*len + i] (bf16, or fp32 when
+ * src_f32); AdamW on (p32, m, v)_r[i] (fp32 [len] each); bf16(p32_r[i]) pushed to element
+ * r*len + i of EVERY rank's p16 [n*len]; gout_r (fp32 [len], optional: gout_off >= 0) gets grad */
+int zp_peer_rs_adam_ag(zp_peer_group* g, int64_t src_off, int32_t src_f32, int64_t len, int64_t acc_off,
+                       int64_t p32_off, int64_t m_off, int64_t v_off, int64_t p16_off, int64_t gout_off,
+                       const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream);
+/* rank r: dst_r[j*len + e] = src_j[e] (bf16 [len] at shard_src_off in every arena; dst [n*len]) */
+int zp_peer_all_gather(zp_peer_group* g, int64_t shard_src_off, int64_t dst_off, int64_t len, uint32_t epoch,
+                       int32_t ctas, void* stream);
 
 /* Number of kernels launched by this library since load (all entry points). */
 int64_t zp_launch_count(void);

@@ -51,23 +51,28 @@ extern "C" int zp_attention_bwd(const void* qkv, const void* out, const void* do
   return e == cudaSuccess ? 0 : 5;
 }
 
-// ---- peer-memory collectives on caller-given arenas (include/zp_kernels.h)
+// ---- peer-memory collectives, all ranks of a group emulated on one device (include/zp_kernels.h)
 struct zp_peer_group {
-  zp::PeerView pv;  // rank is set per call
+  zp::PeerView pv;  // rank 0's view; the emulated launch derives every rank's
   zp::PeerFlags* flags = nullptr;
+  char* base = nullptr;
+  int64_t arena = 0;
 };
 
-extern "C" int zp_peer_group_create(int32_t n, void* const* bases, zp_peer_group** out) {
-  if (!out || !bases || n < 1 || n > zp::kMaxPeers) return 1;
+extern "C" int zp_peer_group_create(int32_t n, void* base, int64_t arena_bytes, zp_peer_group** out) {
+  if (!out || !base || n < 1 || n > zp::kMaxPeers || arena_bytes <= 0) return 1;
   auto* g = new zp_peer_group();
   if (cudaMalloc(&g->flags, sizeof(zp::PeerFlags) * n) != cudaSuccess ||
       cudaMemset(g->flags, 0, sizeof(zp::PeerFlags) * n) != cudaSuccess) {
     delete g;
     return 5;
   }
+  g->base = static_cast<char*>(base);
+  g->arena = arena_bytes;
   g->pv.n = n;
+  g->pv.rank = 0;
   for (int j = 0; j < n; ++j) {
-    g->pv.base[j] = static_cast<char*>(bases[j]);
+    g->pv.base[j] = g->base + arena_bytes * j;
     g->pv.flags[j] = g->flags + j;
   }
   *out = g;
@@ -81,38 +86,48 @@ extern "C" int zp_peer_group_destroy(zp_peer_group* g) {
   return 0;
 }
 
-static zp::PeerView view_of(const zp_peer_group* g, int rank) {
-  zp::PeerView v = g->pv;
-  v.rank = rank;
-  return v;
+static int peer_rc(cudaError_t e) { return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5); }
+
+template <class T>
+static T* at(const zp_peer_group* g, int64_t off) {  // rank 0's buffer at `off` (nullptr if off < 0)
+  return off < 0 ? nullptr : reinterpret_cast<T*>(g->base + off);
 }
 
-extern "C" int zp_peer_rs_accumulate(zp_peer_group* g, int32_t rank, int64_t src_off, int64_t shard_off, float* acc,
-                                     int64_t len, int32_t overwrite, uint32_t epoch, int32_t ctas, void* stream) {
-  if (!g || rank < 0 || rank >= g->pv.n) return 1;
-  const cudaError_t e = zp::peer_rs_accumulate(view_of(g, rank), src_off, shard_off, acc, len, overwrite != 0, epoch,
-                                               ctas, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+extern "C" int zp_peer_rs_accumulate(zp_peer_group* g, int64_t src_off, int64_t len, int64_t acc_off,
+                                     int32_t overwrite, uint32_t epoch, int32_t ctas, void* stream) {
+  if (!g || acc_off < 0) return 1;
+  zp::PeerEmu emu;
+  emu.g = 1;  // set to the per-rank grid by the launcher
+  emu.stride = g->arena;
+  emu.shard = len;
+  return peer_rc(zp::peer_rs_accumulate(g->pv, src_off, 0, at<float>(g, acc_off), len, overwrite != 0, epoch, ctas,
+                                        static_cast<cudaStream_t>(stream), emu));
 }
 
-extern "C" int zp_peer_rs_adam_ag(zp_peer_group* g, int32_t rank, int64_t src_off, int32_t src_f32, int64_t shard_off,
-                                  const float* acc, float* p32, float* m, float* v, int64_t p16_off, float* gout,
-                                  int64_t len, const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream) {
-  if (!g || !ap || rank < 0 || rank >= g->pv.n) return 1;
+extern "C" int zp_peer_rs_adam_ag(zp_peer_group* g, int64_t src_off, int32_t src_f32, int64_t len, int64_t acc_off,
+                                  int64_t p32_off, int64_t m_off, int64_t v_off, int64_t p16_off, int64_t gout_off,
+                                  const zp_adam_params* ap, uint32_t epoch, int32_t ctas, void* stream) {
+  if (!g || !ap || p32_off < 0 || m_off < 0 || v_off < 0) return 1;
   zp::AdamParams a;
   a.lr = ap->lr; a.beta1 = ap->beta1; a.beta2 = ap->beta2; a.eps = ap->eps; a.weight_decay = ap->weight_decay;
   a.bc1 = ap->bc1; a.bc2 = ap->bc2;
-  const cudaError_t e = zp::peer_rs_adam_ag(view_of(g, rank), src_off, src_f32 != 0, shard_off, acc, p32, m, v,
-                                            p16_off, gout, len, a, epoch, ctas, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+  zp::PeerEmu emu;
+  emu.g = 1;
+  emu.stride = g->arena;
+  emu.shard = len;
+  return peer_rc(zp::peer_rs_adam_ag(g->pv, src_off, src_f32 != 0, 0, at<float>(g, acc_off), at<float>(g, p32_off),
+                                     at<float>(g, m_off), at<float>(g, v_off), p16_off, at<float>(g, gout_off), len, a,
+                                     epoch, ctas, static_cast<cudaStream_t>(stream), emu));
 }
 
-extern "C" int zp_peer_all_gather(zp_peer_group* g, int32_t rank, int64_t shard_src_off, void* dst, int64_t len,
+extern "C" int zp_peer_all_gather(zp_peer_group* g, int64_t shard_src_off, int64_t dst_off, int64_t len,
                                   uint32_t epoch, int32_t ctas, void* stream) {
-  if (!g || rank < 0 || rank >= g->pv.n) return 1;
-  const cudaError_t e = zp::peer_all_gather(view_of(g, rank), shard_src_off, static_cast<zp::bf16*>(dst), len, epoch,
-                                            ctas, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+  if (!g || dst_off < 0) return 1;
+  zp::PeerEmu emu;
+  emu.g = 1;
+  emu.stride = g->arena;
+  return peer_rc(zp::peer_all_gather(g->pv, shard_src_off, at<zp::bf16>(g, dst_off), len, epoch, ctas,
+                                     static_cast<cudaStream_t>(stream), emu));
 }
 
 extern "C" int zp_attention_bwd_hd(const void* qkv, const void* out, const void* dout, const float* lse,

@@ -35,9 +35,9 @@ __device__ void wait_all(const uint32_t* flags, int n, uint32_t epoch) {
 }
 
 // Entry: CTA 0 announces "my inputs are final" to every rank; every CTA waits for all ranks.
-__device__ void entry_barrier(const PeerView& pv, uint32_t epoch) {
+__device__ void entry_barrier(const PeerView& pv, uint32_t epoch, int blk) {
   if (threadIdx.x == 0) {
-    if (blockIdx.x == 0)
+    if (blk == 0)
       for (int j = 0; j < pv.n; ++j) st_release_sys(&pv.flags[j]->ready[pv.rank], epoch);
     wait_all(pv.flags[pv.rank]->ready, pv.n, epoch);
   }
@@ -46,17 +46,31 @@ __device__ void entry_barrier(const PeerView& pv, uint32_t epoch) {
 
 // Exit: the last CTA of this rank to finish tells every rank "done with your buffers" and waits
 // until every rank said the same, so the kernel completes only when all peers finished.
-__device__ void exit_barrier(const PeerView& pv, uint32_t epoch) {
+__device__ void exit_barrier(const PeerView& pv, uint32_t epoch, int nblk) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    const uint32_t old = atomicInc(&pv.flags[pv.rank]->ctr, gridDim.x - 1);
-    if (old == gridDim.x - 1) {
+    const uint32_t old = atomicInc(&pv.flags[pv.rank]->ctr, nblk - 1);
+    if (old == nblk - 1) {
       __threadfence_system();
       for (int j = 0; j < pv.n; ++j) st_release_sys(&pv.flags[j]->done[pv.rank], epoch);
       wait_all(pv.flags[pv.rank]->done, pv.n, epoch);
     }
   }
+}
+
+// This block's rank instance: (block index, block count) within the rank's grid; in an emulated
+// launch also the rank itself and its pointer / shard offsets.
+struct Blk {
+  int blk, nblk, rank;
+};
+__device__ __forceinline__ Blk resolve(const PeerEmu& emu, int rank) {
+  if (emu.g == 0) return {int(blockIdx.x), int(gridDim.x), rank};
+  return {int(blockIdx.x) % emu.g, emu.g, int(blockIdx.x) / emu.g};
+}
+template <class T>
+__device__ __forceinline__ T* rank_ptr(T* p, const PeerEmu& emu, int rank) {
+  return (emu.g == 0 || p == nullptr) ? p : reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(p) + emu.stride * rank);
 }
 
 __device__ __forceinline__ void add_bf16x8(float (&a)[8], const uint4& u) {
@@ -89,11 +103,15 @@ __device__ __forceinline__ void pull_sum8(const PeerView& pv, int64_t src_off, i
 
 __global__ void __launch_bounds__(kThreads) peer_rs_acc_k(PeerView pv, int64_t src_off, int64_t shard_off,
                                                           float* __restrict__ acc, int64_t len, int overwrite,
-                                                          uint32_t epoch) {
-  entry_barrier(pv, epoch);
+                                                          uint32_t epoch, PeerEmu emu) {
+  const Blk B = resolve(emu, pv.rank);
+  pv.rank = B.rank;
+  acc = rank_ptr(acc, emu, B.rank);
+  shard_off += emu.shard * B.rank;
+  entry_barrier(pv, epoch, B.blk);
   const int64_t n8 = len / 8;
-  const int64_t step = int64_t(gridDim.x) * kThreads;
-  int64_t i0 = blockIdx.x * int64_t(kThreads) + threadIdx.x;
+  const int64_t step = int64_t(B.nblk) * kThreads;
+  int64_t i0 = B.blk * int64_t(kThreads) + threadIdx.x;
   // two items per thread: 2n remote loads in flight before the sums (same per-element order)
   for (; i0 + step < n8; i0 += 2 * step) {
     float g[2][8];
@@ -132,7 +150,7 @@ __global__ void __launch_bounds__(kThreads) peer_rs_acc_k(PeerView pv, int64_t s
     a[0] = make_float4(g[0], g[1], g[2], g[3]);
     a[1] = make_float4(g[4], g[5], g[6], g[7]);
   }
-  exit_barrier(pv, epoch);
+  exit_barrier(pv, epoch, B.nblk);
 }
 
 template <bool F32>
@@ -141,12 +159,20 @@ __global__ void __launch_bounds__(kThreads) peer_rs_adam_ag_k(PeerView pv, int64
                                                               float* __restrict__ p32, float* __restrict__ m,
                                                               float* __restrict__ v, int64_t p16_off,
                                                               float* __restrict__ gout, int64_t len,
-                                                              AdamParams ap, uint32_t epoch) {
-  entry_barrier(pv, epoch);
+                                                              AdamParams ap, uint32_t epoch, PeerEmu emu) {
+  const Blk B = resolve(emu, pv.rank);
+  pv.rank = B.rank;
+  acc = rank_ptr(acc, emu, B.rank);
+  p32 = rank_ptr(p32, emu, B.rank);
+  m = rank_ptr(m, emu, B.rank);
+  v = rank_ptr(v, emu, B.rank);
+  gout = rank_ptr(gout, emu, B.rank);
+  shard_off += emu.shard * B.rank;
+  entry_barrier(pv, epoch, B.blk);
   const float inv_bc1 = 1.0f / ap.bc1;
   const float inv_sqrt_bc2 = rsqrtf(ap.bc2);
   const int64_t n8 = len / 8;
-  for (int64_t i = blockIdx.x * int64_t(kThreads) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * kThreads) {
+  for (int64_t i = B.blk * int64_t(kThreads) + threadIdx.x; i < n8; i += int64_t(B.nblk) * kThreads) {
     float g[8];
     pull_sum8<F32>(pv, src_off, shard_off + i * 8, g);
     if (acc) {
@@ -185,15 +211,18 @@ __global__ void __launch_bounds__(kThreads) peer_rs_adam_ag_k(PeerView pv, int64
     for (int j = 0; j < pv.n; ++j)  // push the new parameters to every rank (the all-gather)
       *(reinterpret_cast<uint4*>(pv.base[j] + p16_off) + (shard_off / 8 + i)) = o;
   }
-  exit_barrier(pv, epoch);
+  exit_barrier(pv, epoch, B.nblk);
 }
 
 __global__ void __launch_bounds__(kThreads) peer_ag_k(PeerView pv, int64_t src_off, bf16* __restrict__ dst,
-                                                      int64_t len, uint32_t epoch) {
-  entry_barrier(pv, epoch);
+                                                      int64_t len, uint32_t epoch, PeerEmu emu) {
+  const Blk B = resolve(emu, pv.rank);
+  pv.rank = B.rank;
+  dst = rank_ptr(dst, emu, B.rank);
+  entry_barrier(pv, epoch, B.blk);
   const int64_t n8 = len / 8, total8 = n8 * pv.n;
-  const int64_t step = int64_t(gridDim.x) * kThreads;
-  int64_t i = blockIdx.x * int64_t(kThreads) + threadIdx.x;
+  const int64_t step = int64_t(B.nblk) * kThreads;
+  int64_t i = B.blk * int64_t(kThreads) + threadIdx.x;
   // Item i is element e of the c-th shard in this rank's visiting order, which starts at the next
   // rank: at any moment every GPU is read by one peer instead of all ranks reading rank 0 first.
   // Four remote 16-byte loads in flight per thread before their stores (NVLink latency).
@@ -218,7 +247,7 @@ __global__ void __launch_bounds__(kThreads) peer_ag_k(PeerView pv, int64_t src_o
     const int j = (c + pv.rank + 1) % pv.n;
     reinterpret_cast<uint4*>(dst)[int64_t(j) * n8 + e] = *(reinterpret_cast<const uint4*>(pv.base[j] + src_off) + e);
   }
-  exit_barrier(pv, epoch);
+  exit_barrier(pv, epoch, B.nblk);
 }
 
 int grid(int64_t items, int ctas) {
@@ -227,37 +256,49 @@ int grid(int64_t items, int ctas) {
   return int(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
+// One launch per rank, or (emu.g > 0) one cooperative launch of every rank's instance.
+template <class K, class... Args>
+cudaError_t launch(K kernel, int g, const PeerView& pv, const PeerEmu& emu, cudaStream_t s, Args... args) {
+  if (emu.g == 0) {
+    kernel<<<g, kThreads, 0, s>>>(args..., emu);
+    note_launch();
+    return cudaGetLastError();
+  }
+  PeerEmu e = emu;
+  e.g = g;
+  void* params[] = {&args..., &e};
+  const cudaError_t r = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(g * pv.n),
+                                                    dim3(kThreads), params, 0, s);
+  note_launch();
+  return r;
+}
+
 }  // namespace
 
 cudaError_t peer_rs_accumulate(const PeerView& pv, int64_t src_off, int64_t shard_off, float* acc,
-                               int64_t len, bool overwrite, uint32_t epoch, int ctas, cudaStream_t s) {
-  if (len % 8 || shard_off % 8) return cudaErrorInvalidValue;
-  peer_rs_acc_k<<<grid(len / 8, ctas), kThreads, 0, s>>>(pv, src_off, shard_off, acc, len, overwrite ? 1 : 0, epoch);
-  note_launch();
-  return cudaGetLastError();
+                               int64_t len, bool overwrite, uint32_t epoch, int ctas, cudaStream_t s,
+                               const PeerEmu& emu) {
+  if (len % 8 || shard_off % 8 || emu.shard % 8) return cudaErrorInvalidValue;
+  return launch(peer_rs_acc_k, grid(len / 8, ctas), pv, emu, s, pv, src_off, shard_off, acc, len,
+                overwrite ? 1 : 0, epoch);
 }
 
 cudaError_t peer_rs_adam_ag(const PeerView& pv, int64_t src_off, bool src_f32, int64_t shard_off,
                             const float* acc, float* p32, float* m, float* v, int64_t p16_off,
                             float* gout, int64_t len, const AdamParams& ap, uint32_t epoch, int ctas,
-                            cudaStream_t s) {
-  if (len % 8 || shard_off % 8) return cudaErrorInvalidValue;
+                            cudaStream_t s, const PeerEmu& emu) {
+  if (len % 8 || shard_off % 8 || emu.shard % 8) return cudaErrorInvalidValue;
   if (src_f32)
-    peer_rs_adam_ag_k<true><<<grid(len / 8, ctas), kThreads, 0, s>>>(pv, src_off, shard_off, acc, p32, m, v,
-                                                                   p16_off, gout, len, ap, epoch);
-  else
-    peer_rs_adam_ag_k<false><<<grid(len / 8, ctas), kThreads, 0, s>>>(pv, src_off, shard_off, acc, p32, m, v,
-                                                                    p16_off, gout, len, ap, epoch);
-  note_launch();
-  return cudaGetLastError();
+    return launch(peer_rs_adam_ag_k<true>, grid(len / 8, ctas), pv, emu, s, pv, src_off, shard_off, acc, p32, m,
+                  v, p16_off, gout, len, ap, epoch);
+  return launch(peer_rs_adam_ag_k<false>, grid(len / 8, ctas), pv, emu, s, pv, src_off, shard_off, acc, p32, m, v,
+                p16_off, gout, len, ap, epoch);
 }
 
 cudaError_t peer_all_gather(const PeerView& pv, int64_t shard_src_off, bf16* dst, int64_t len,
-                            uint32_t epoch, int ctas, cudaStream_t s) {
+                            uint32_t epoch, int ctas, cudaStream_t s, const PeerEmu& emu) {
   if (len % 8) return cudaErrorInvalidValue;
-  peer_ag_k<<<grid(len / 8 * pv.n, ctas), kThreads, 0, s>>>(pv, shard_src_off, dst, len, epoch);
-  note_launch();
-  return cudaGetLastError();
+  return launch(peer_ag_k, grid(len / 8 * pv.n, ctas), pv, emu, s, pv, shard_src_off, dst, len, epoch);
 }
 
 }  // namespace zp

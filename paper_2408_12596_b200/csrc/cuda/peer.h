@@ -34,10 +34,20 @@ struct PeerView {
   PeerFlags* flags[kMaxPeers] = {};  // every rank's flag block
 };
 
+// Single-device emulation of all n ranks in ONE cooperative launch (test harness, include/
+// zp_kernels.h): blocks [r*g, (r+1)*g) run rank r's instance, so instances that wait on one
+// another are co-resident by construction. Rank r's per-rank pointers are the given (rank 0)
+// pointers + r*stride bytes, its shard offset + r*shard elements. g == 0: a normal per-rank launch.
+struct PeerEmu {
+  int g = 0;
+  int64_t stride = 0, shard = 0;
+};
+
 // acc[i] = (overwrite ? 0 : acc[i]) + sum_j src_j[shard_off + i], i < len. src_off = byte offset
 // of src (bf16 [total]) inside every rank's arena.
 cudaError_t peer_rs_accumulate(const PeerView& pv, int64_t src_off, int64_t shard_off, float* acc,
-                               int64_t len, bool overwrite, uint32_t epoch, int ctas, cudaStream_t s);
+                               int64_t len, bool overwrite, uint32_t epoch, int ctas, cudaStream_t s,
+                               const PeerEmu& emu = PeerEmu());
 
 // g[i] = (acc ? acc[i] : 0) + sum_j src_j[shard_off + i] (src bf16, or fp32 when src_f32);
 // AdamW on (p32, m, v)[i]; bf16(p32[i]) stored to every rank's p16 at element shard_off + i
@@ -45,11 +55,11 @@ cudaError_t peer_rs_accumulate(const PeerView& pv, int64_t src_off, int64_t shar
 cudaError_t peer_rs_adam_ag(const PeerView& pv, int64_t src_off, bool src_f32, int64_t shard_off,
                             const float* acc, float* p32, float* m, float* v, int64_t p16_off,
                             float* gout, int64_t len, const AdamParams& ap, uint32_t epoch, int ctas,
-                            cudaStream_t s);
+                            cudaStream_t s, const PeerEmu& emu = PeerEmu());
 
 // dst[i] = src_j[...] gather: every rank's shard j (len elements of bf16 at byte offset
 // src_off + j*len*2 ... ) is pulled into dst at element j*len. Used by ZeRO-3 group gathers.
 cudaError_t peer_all_gather(const PeerView& pv, int64_t shard_src_off, bf16* dst, int64_t len,
-                            uint32_t epoch, int ctas, cudaStream_t s);
+                            uint32_t epoch, int ctas, cudaStream_t s, const PeerEmu& emu = PeerEmu());
 
 }  // namespace zp
