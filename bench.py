@@ -376,6 +376,7 @@ def main():
     # rank launches no collectives: latency 0 and infinite bandwidth make collective_time 0 in the
     # reference's own formula (validate() only requires bandwidth > 0).
     link = rt.link_model(stage) if world > 1 else (float("inf"), 0.0)
+    link_measured = link
 
     # Poplar: Alg. 1 on the devices, Alg. 2 on the host (bit-exact planner)
     t0 = time.perf_counter()
@@ -394,9 +395,19 @@ def main():
         # correction is corrected too; the compute of two iterations is averaged)
         for _ in range(max(1, args.recalibrate_passes)):
             rt.execute_iteration(plan, stage)
-            t_cal = [rt.execute_iteration(plan, stage)["compute"] for _ in range(2)]
+            t_cal = [rt.execute_iteration(plan, stage) for _ in range(2)]
+            all_cal = allgather([{"compute": t["compute"], "coll_times": t["coll_times"], "wall": t["wall"],
+                                  "optimizer": t["optimizer"]} for t in t_cal])
             profile = poplar.recalibrate(profile, plan,
-                                         allgather({"compute": sum(t_cal) / len(t_cal)}))
+                                         [{"compute": sum(c["compute"] for c in r) / len(r)} for r in all_cal])
+            # the link model likewise: fitted to the comm the iteration exposed (mean of the two)
+            floors = [poplar.iteration_report([r[k] for r in all_cal], gbs)["comm_total"] for k in range(2)]
+            floor = sum(floors) / 2
+            if stage in (1, 2) and rt.peer_collectives():
+                # the fused sync kernel's span holds the AdamW pass too; the planner adds that as its
+                # optimizer tail, so it leaves the comm floor
+                floor -= max(d["optimizer_time"] for d in profile["devices"])
+            link = poplar.recalibrate_link(link, stage, plan["gas"], floor, rt.param_count)
             plan = poplar.poplar_plan(rt, profile, gbs, stage, world, link=link)
             first, count = poplar.rank_slice(plan, rank)
             rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
@@ -556,8 +567,12 @@ def main():
                        "recalibrated": plan is not plan_initial,
                        "recalibrate_passes": 0 if plan is plan_initial else max(1, args.recalibrate_passes),
                        "mbs": [d["mbs"] for d in profile["devices"]],
-                       "link_model": ({"bandwidth_GBps": link[0] / 1e9, "latency_us": link[1] * 1e6,
-                                       "source": "measured (zp_runtime_link_model, max over ranks)"}
+                       "link_model": ({"bandwidth_GBps": link_measured[0] / 1e9, "latency_us": link_measured[1] * 1e6,
+                                       "source": "measured (zp_runtime_link_model, max over ranks)",
+                                       "recalibrated_bandwidth_GBps": (link[0] / 1e9 if link is not link_measured
+                                                                       else None),
+                                       "recalibrated_note": "bandwidth solved from the measured exposed comm "
+                                                            "(poplar.recalibrate_link); used by the final plan"}
                                       if world > 1 else "one rank: no collectives (latency 0, bandwidth inf)"),
                        "profile_seconds": t_profile, "parallelism": f"zero{stage}-dp{world}",
                        "collectives": (("nvlink-peer (pull RS/AG; fused RS+AdamW+AG at sync)" if stage in (1, 2) else "nvlink-peer (pull RS, copy-engine AG prefetch)" if stage == 3 else "nccl (all-reduce)") if rt.peer_collectives() else "nccl") if world > 1 else "none",

@@ -64,6 +64,28 @@ def recalibrate(profile: dict, plan: dict, timings: Sequence[dict]) -> dict:
     return out
 
 
+def recalibrate_link(link, stage: int, gas: int, comm_floor: float, param_count: float,
+                     bytes_per_param: float = 2.0):
+    """Link model (bandwidth, latency) fitted to the collective time an executed iteration actually
+    exposed. The reference's cost model charges every collective in full, additively
+    (comm.cpp:101-120): per iteration `gas` micro-step launches (ZeRO-2: one reduce-scatter; ZeRO-3:
+    two gathers + one reduce-scatter) plus the synchronisation collective (ZeRO-0/1: an all-reduce
+    of twice the model; ZeRO-2: a gather). On B200 the ZeRO-3 gathers are prefetched behind
+    compute, so the additive model over-charges them. Keeping the measured latency, the bandwidth
+    is solved from the measured comm floor (poplar.iteration_report) so that the planner's comm
+    term equals what the iteration exposed; the unchanged planner then re-plans with it."""
+    bw, alpha = link
+    vol = param_count * bytes_per_param
+    if stage <= 1:
+        launches, volume = 1, 2.0 * vol
+    elif stage == 2:
+        launches, volume = gas + 1, (gas + 1) * vol
+    else:
+        launches, volume = 3 * gas, 3 * gas * vol
+    t = comm_floor - launches * alpha
+    return (volume / t if t > 0 else 1e15, alpha)
+
+
 def rank_slice(plan: dict, rank: int):
     """First global sample index and sample count of `rank` (ranks take contiguous ranges in
     device order, so global sample j is the same sample for every allocation)."""

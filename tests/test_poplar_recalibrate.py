@@ -46,3 +46,18 @@ def test_recalibrate_passes_compose():
     third = poplar.recalibrate(once, plan2, [{"compute": 0.1155}, {"compute": 0.190}])
     for (b, t0), (_, t2) in zip(prof["devices"][0]["samples"], third["devices"][0]["samples"]):
         assert t2 == pytest.approx(t0 * 1.05 * 1.1)
+
+
+@pytest.mark.parametrize("stage,gas", [(1, 3), (2, 4), (3, 6)])
+def test_recalibrated_link_reproduces_the_measured_comm(stage, gas):
+    """With the fitted link model the reference's additive comm cost (comm.cpp:101-120) of one
+    iteration equals the measured exposed comm it was fitted to."""
+    from paper_2408_12596_b200 import host, poplar
+    from paper_2408_12596_b200.host import ClusterSpec, Device, ModelSpec
+    psi = 6.738e9
+    link = poplar.recalibrate_link((845e9, 26e-6), stage, gas, 0.108, psi)
+    model = ModelSpec(psi, 4096, 32, 2.0, 16.0)
+    cl = ClusterSpec([Device(1.0, 1.0, 0.0, 1.0)] * 4, [link[0]] * 4, link[1])
+    cp = host.product().make_comm_profile(model, stage, cl)
+    charged = (gas * cp.time_per_step if stage >= 2 else 0.0) + cp.sync_time
+    assert charged == pytest.approx(0.108, rel=1e-12)
