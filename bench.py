@@ -245,16 +245,17 @@ def plans_equal(a: dict, b: dict) -> list:
 
 
 def plan_parity(rt, profiles, gbs, stage, world, link):
-    """Re-plan each measured profile with the reference planner compiled from its own sources
-    (oracle/_ref, the checker) and compare with the product plan bit for bit."""
+    """Re-plan each measured profile (with the link model its plan used) with the reference planner
+    compiled from its own sources (oracle/_ref, the checker) and compare with the product plan bit
+    for bit."""
     import oracle
     from paper_2408_12596_b200 import poplar
     if not oracle.available():
         return {"checked": 0, "note": "oracle/_ref not built"}
     ref = oracle.reference()
     out = {"checked": 0, "identical": True, "diffs": []}
-    for name, prof, plan in profiles:
-        theirs = poplar.poplar_plan(rt, prof, gbs, stage, world, link=link, api=ref)
+    for name, prof, plan, lk in profiles:
+        theirs = poplar.poplar_plan(rt, prof, gbs, stage, world, link=lk, api=ref)
         d = plans_equal(plan, theirs)
         out["checked"] += 1
         if d:
@@ -518,8 +519,8 @@ def main():
         peak_sust = peaks["bf16_tflops_sustained"] * tr / 148.0
         traffic = gemm_traffic(args.config)
         # checks against the reference (the oracle as checker; not timed, not on the product path)
-        parity = plan_parity(rt, [("alg1", profile_initial, plan_initial)] +
-                             ([("recalibrated", profile, plan)] if plan is not plan_initial else []),
+        parity = plan_parity(rt, [("alg1", profile_initial, plan_initial, link_measured)] +
+                             ([("recalibrated", profile, plan, link)] if plan is not plan_initial else []),
                              gbs, stage, world, link)
         measured_iter = T / args.steps
         # where the prediction and the measurement differ: the planner's wall time is
