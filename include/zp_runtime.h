@@ -28,7 +28,8 @@ extern "C" {
 
 /* Decoder config. arch 0: GPT-2 family (pre-LN LayerNorm with bias, learned positions, tied LM
  * head, GELU-tanh MLP, biases). arch 1: Llama family (RMSNorm, rotary positions theta 1e4,
- * SwiGLU MLP with d_ff hidden units, no biases, untied LM head). head_dim is 64 in both. */
+ * SwiGLU MLP with d_ff hidden units, no biases, untied LM head). head_dim = d_model / n_head must be
+ * 64 or 128. */
 typedef struct zp_gpt_config {
   int32_t n_layer, d_model, n_head, d_ff, vocab, seq_len;
   int32_t arch;

@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(kThreads) adam_k(float* __restrict__ p32, floa
 
 }  // namespace
 
-// ------------------------------------------------------------------ RoPE (rotate-half, head_dim 64)
+// ------------------------------------------------------------------ RoPE (rotate-half, any head_dim)
 
 // cos / sin of pos * theta^(-2j/64) for pos < seq, j < 32 (computed once per (seq, theta) in
 // double precision, kept in a small per-process table).

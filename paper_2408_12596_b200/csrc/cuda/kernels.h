@@ -49,7 +49,8 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
                           int64_t rows, int h, int ctas, cudaStream_t s, bool rms = false,
                           float* cs = nullptr);
-// Rotary embedding (rotate-half, head_dim 64) on the Q and K blocks of qkv [T, 3h], in place.
+// Rotary embedding (rotate-half pairs (i, i + dh/2), any head_dim dh multiple of 16) on the Q and K
+// blocks of qkv [T, 3h], in place.
 void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s,
           int dh = 64);
 // SwiGLU with gate/up interleaved in 32-column blocks of gu [T, 2f]: out [T, f].
