@@ -6,7 +6,7 @@
 
 Default workload: the largest BASELINE.json configuration that fits one B200 — C5, a
 Llama-style 7B (L32 h4096 ffn11008 V32000, s=4096) at ZeRO-3 bf16, ranks cycling the SM tiers
-148 / 104 / 74 SMs and HBM caps 180 / 96 GB (rank 0: 148 SMs, full HBM), global batch 32*N
+148 / 104 / 74 SMs and HBM caps 180 / 128 GB (rank 0: 148 SMs, full HBM), global batch 32*N
 samples (weak scaling). `--config c1..c4` select the other BASELINE configs (C2 = GPT-2 small
 ZeRO-2 at 132 / 66 SMs, the round-1 headline).
 
@@ -57,8 +57,12 @@ CONFIGS = {
     # 5 fast + 3 slow ranks at N=8 (tier list indexed by rank)
     "c4": dict(model="llama-1.3b", stage=3, tiers=[148, 148, 74, 148, 74, 148, 74, 148], caps=[0],
                gbs_per_gpu=128, label="C4: Llama-style 1.3B s2048, ZeRO-3 bf16, 5 fast (148 SM) + 3 slow (74 SM)"),
-    "c5": dict(model="llama-7b", stage=3, tiers=[148, 104, 74, 148, 104, 74, 148, 74], caps=[0, 0, 0, 96],
-               gbs_per_gpu=32, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/96 GB"),
+    # the memory tier (every 4th rank) holds 128 GB: 6 samples per micro-step instead of 8. A 96 GB
+    # tier (3 samples) pinned every lockstep ZeRO-3 micro-step to 3 samples on the fast ranks, so
+    # the 104-SM tier could only take 2 and idled 24 % by the planner's own prediction
+    # (profiles/r2_bench_lines/g15_c5_n4.json, g20_c5_n4.json)
+    "c5": dict(model="llama-7b", stage=3, tiers=[148, 104, 74, 148, 104, 74, 148, 74], caps=[0, 0, 0, 128],
+               gbs_per_gpu=32, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/128 GB"),
 }
 DEFAULT_CONFIG = "c5"
 
