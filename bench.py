@@ -602,7 +602,13 @@ def main():
                          "launches": nl},
             "roofline_hbm": {"kernel": ("peer_rs_adam_ag_k (fused NVLink RS + AdamW + push AG), last-arriving rank" if fused else
                                         "adam_k (fused accumulate + AdamW + bf16 cast), rank 0"),
-                             "bound": "hbm",
+                             "bound": "nvlink" if fused else "hbm",
+                             "nvlink": ({"achieved_GBps": a_nvl / a_s / 1e9, "peak_GBps": 770.0,
+                                         "frac": a_nvl / a_s / 1e9 / 770.0,
+                                         "peak_note": "measured peer copy per direction per GPU on this pool "
+                                                      "(B200_PROFILING.md; 900 nominal); bytes = the peers' "
+                                                      "gradient shards pulled + the new bf16 shard pushed"}
+                                        if (fused and a_s) else None),
                              "achieved": a_bytes / a_s / 1e9 if a_s else None,
                              "peak": peaks["hbm_gbs"], "unit": "GB/s",
                              "frac": (a_bytes / a_s / 1e9 / peaks["hbm_gbs"]) if a_s else None,
