@@ -547,7 +547,11 @@ def main():
                                                 "optimizer_s": m_opt,
                                                 "unmodelled_s": t_last - m_comp - report["comm_total"] - m_opt},
                     "per_rank_compute_s": {"predicted": [d["predicted_time"] for d in plan["devices"]],
-                                           "measured": report["compute"]}}
+                                           "measured": report["compute"]},
+                    "per_rank_collectives_s": {"gather": [t["ag_fwd"] + t["ag_bwd"] for t in timings],
+                                               "reduce_scatter": [t["rs"] for t in timings],
+                                               "sync": [t["sync"] for t in timings],
+                                               "wall": [t["wall"] for t in timings]}}
         try:
             ref_pred = reference_prediction(rt, profile, probes, link, gbs, stage, world)
         except Exception as e:  # the reference pipeline may reject a fitted cluster
