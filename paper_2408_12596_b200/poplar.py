@@ -46,20 +46,29 @@ def poplar_plan(rt, profile: dict, gbs: int, stage: int, n: int, uniform: bool =
     return api.make_uniform_plan(gbs, profile, stage, comm, tail)
 
 
-def recalibrate(profile: dict, plan: dict, timings: Sequence[dict]) -> dict:
+def recalibrate(profile: dict, plan: dict, timings: Sequence[dict], slow_only: bool = True) -> dict:
     """Profile with every rank's step-time samples rescaled by the ratio of its measured compute
     in a planned iteration to the compute the plan predicted for it.
 
     Alg. 1's probes are short; a long iteration settles at lower power-capped clocks, and not by
     the same factor on every tier (a rank with more SMs draws more power). One measured iteration
     corrects the curves; the planner (Alg. 2) is then re-run unchanged on the corrected profile.
-    Ranks that did no work keep their samples."""
+    Ranks that did no work keep their samples.
+
+    slow_only: a rank is only ever slowed, never sped up. Under the board power cap a GPU that
+    idles part of the iteration (waiting in lockstep collectives) computes at higher clocks than
+    one that never idles, so its faster measurement is an artefact of the plan: crediting it made
+    the next plan give that rank the bigger batch, it became the bottleneck and slowed down, and
+    the passes oscillated between two plans (C5 on 4 GPUs: ±10 % per rank). The full-load speed is
+    what the bottleneck rank runs at, and that is what slowing-only converges to."""
     out = {**profile, "devices": []}
     for d, dp, t in zip(profile["devices"], plan["devices"], timings):
         # predicted_time = sum of the curve's step times over the rank's micro-steps
         # (reference planner.cpp:40-58, 318-326): compute only, like the measured spans
         predicted, measured = dp["predicted_time"], t["compute"]
         ratio = measured / predicted if predicted > 0 and measured > 0 else 1.0
+        if slow_only:
+            ratio = max(ratio, 1.0)
         out["devices"].append({**d, "samples": [(b, tt * ratio) for b, tt in d["samples"]]})
     return out
 

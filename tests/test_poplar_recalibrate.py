@@ -61,3 +61,15 @@ def test_recalibrated_link_reproduces_the_measured_comm(stage, gas):
     cp = host.product().make_comm_profile(model, stage, cl)
     charged = (gas * cp.time_per_step if stage >= 2 else 0.0) + cp.sync_time
     assert charged == pytest.approx(0.108, rel=1e-12)
+
+
+def test_recalibrate_only_slows():
+    """A rank measured faster than predicted keeps its curve (its speed-up came from idling under
+    the power cap); with slow_only=False it is credited."""
+    prof = _profile()
+    plan = {"stage": 3, "gas": 2, "devices": [{"predicted_time": 0.100}, {"predicted_time": 0.200}]}
+    out = poplar.recalibrate(prof, plan, [{"compute": 0.090}, {"compute": 0.220}])
+    assert out["devices"][0]["samples"] == prof["devices"][0]["samples"]
+    assert out["devices"][1]["samples"][0][1] == pytest.approx(0.020 * 1.1)
+    both = poplar.recalibrate(prof, plan, [{"compute": 0.090}, {"compute": 0.220}], slow_only=False)
+    assert both["devices"][0]["samples"][0][1] == pytest.approx(0.010 * 0.9)
