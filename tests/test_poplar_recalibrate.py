@@ -28,7 +28,7 @@ def test_recalibrate_scales_each_rank():
 def test_recalibrate_keeps_idle_rank():
     prof = _profile()
     plan = {"stage": 2, "gas": 1, "devices": [{"predicted_time": 0.0}, {"predicted_time": 0.2}]}
-    out = poplar.recalibrate(prof, plan, [{"compute": 0.0}, {"compute": 0.1}])
+    out = poplar.recalibrate(prof, plan, [{"compute": 0.0}, {"compute": 0.1}], slow_only=False)
     assert out["devices"][0]["samples"] == prof["devices"][0]["samples"]
     assert out["devices"][1]["samples"][3][1] == pytest.approx(0.066)
 
