@@ -1154,6 +1154,20 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 // Warp roles: 0-7 builders (lane quarter w % 4, query half w / 4), 8-11 dQ out + dK/dV epilogue,
 // 12 TMA producer, 13 MMA issuer. K/V single-buffered per task; Q/dO(+LSE, D) two stages.
 constexpr int kB2Threads = 14 * 32;
+
+// Timeline diagnostics (tools/microbench/attn_trace.cu builds this file with ZP_ATTN_TRACE): CTA 0
+// stamps clock64 at each pipeline event of its first tiles.
+#ifdef ZP_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[16][64];
+#define ATR(ev, i)                                                           \
+  do {                                                                       \
+    if (blockIdx.x == 0 && (i) < 64) g_attn_trace[ev][i] = clock64();       \
+  } while (0)
+#else
+#define ATR(ev, i) \
+  do {             \
+  } while (0)
+#endif
 constexpr int kB2TS = 0, kB2TDP = 128, kB2TDV = 256, kB2TDK = 384;
 
 struct B2Smem {
@@ -1275,6 +1289,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       auto issue_st = [&](uint32_t i) {  // S^T(i) = K Q(i)^T
         ptx::mbar_wait(&qd_full[i & 1], (i >> 1) & 1);
         ptx::tc_fence_after();
+        ATR(2, i);
 #pragma unroll
         for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TS, kdesc128(sk, k), kdesc128(sq(i), k), id_ss, k > 0);
         ptx::umma_commit(s_full);
@@ -1282,6 +1297,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       auto issue_dpt = [&](uint32_t i) {  // dP^T(i) = V dO(i)^T, once dQ(i-1) has left the columns
         ptx::mbar_wait(dq_free, (i & 1) ^ 1);
         ptx::tc_fence_after();
+        ATR(0, i);
 #pragma unroll
         for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, kdesc128(sv, k), kdesc128(sdo(i), k), id_ss, k > 0);
         ptx::umma_commit(dp_full);
@@ -1298,17 +1314,20 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           if (first) ptx::mbar_wait(acc_free, (item & 1) ^ 1);  // previous task's dK/dV read out
           ptx::mbar_wait(pt_full, it & 1);
           ptx::tc_fence_after();
+          ATR(1, it);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             ptx::umma_bf16_ts(tmem + kB2TDV, tmem + kB2TS + tcol(k), mndesc(sdo(it), k), id_t, !first || k > 0);
           if (!last) issue_st(it + 1);  // overwrites P^T only after dV (in-order tensor pipe)
           ptx::mbar_wait(dst_full, it & 1);
           ptx::tc_fence_after();
+          ATR(3, it);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             ptx::umma_bf16_ts(tmem + kB2TDK, tmem + kB2TDP + tcol(k), mndesc(sq(it), k), id_t, !first || k > 0);
           ptx::mbar_wait(ds_full, it & 1);
           ptx::tc_fence_after();
+          ATR(4, it);
 #pragma unroll
           for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
           ptx::umma_commit(mm_done);
@@ -1335,6 +1354,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         const float* ld = reinterpret_cast<const float*>(sm + B2Smem::kLD + (it & 1) * 1024);
         ptx::mbar_wait(s_full, it & 1);  // S^T(i) landed; Q(i) / LSE(i) are in this stage
         ptx::tc_fence_after();
+        if (warp == 0 && lane == 0) ATR(5, it);
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1356,10 +1376,12 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tmem_st_32x32b_x32(tmem + kB2TS + lane_off + qh * 64, pk);  // P^T over this half's S^T
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
+        if (warp == 0 && lane == 0) ATR(6, it);
         ptx::mbar_arrive(pt_full);
         // dS'^T = P^T (dP^T - D), from the bf16 P (the value the dV product also uses)
         ptx::mbar_wait(dp_full, it & 1);
         ptx::tc_fence_after();
+        if (warp == 0 && lane == 0) ATR(7, it);
         uint32_t dk[32];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1378,13 +1400,16 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tmem_st_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64, dk);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
+        if (warp == 0 && lane == 0) ATR(8, it);
         ptx::mbar_arrive(dst_full);
         // dS'^T into shared memory for dQ = dS' K, once the previous tile's dQ staging drained
         ptx::mbar_wait(stg_free, (it & 1) ^ 1);
+        if (warp == 0 && lane == 0) ATR(9, it);
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           st_shared_v4(sds + p_off(r, qh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
         fence_proxy_async();
+        if (warp == 0 && lane == 0) ATR(10, it);
         ptx::mbar_arrive(ds_full);
       }
     }
@@ -1400,6 +1425,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       for (int i = tk.tile; i < nt; ++i, ++it) {
         ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; dS' shared memory consumed
         ptx::tc_fence_after();
+        if (warp == 8 && lane == 0) ATR(11, it);
         uint32_t v[4][32];
         ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off, v[0]);
         ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + 32, v[1]);
@@ -1407,6 +1433,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + 96, v[3]);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
+        if (warp == 8 && lane == 0) ATR(12, it);
         ptx::mbar_arrive(dq_free);  // the MMA warp may put dP^T(i+1) into these columns
         const int row = smp * seq + i * kT + q4 * 32;
 #pragma unroll
@@ -1429,6 +1456,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         }
         if (lane == 0) {
           ptx::bulk_wait_read<0>();
+          if (warp == 8) ATR(13, it);
           ptx::mbar_arrive(stg_free);  // the builders may write the next dS'^T over the boxes
         }
         __syncwarp();
