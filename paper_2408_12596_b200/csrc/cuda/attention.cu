@@ -12,7 +12,8 @@
 // head_dim 128 forward  (attn_fwd_d128_kernel): two query tiles per CTA share every K/V tile and
 //              ping-pong their softmax warp groups with one MMA warp; P overwrites S in TMEM.
 // head_dim 128 backward (attn_bwd_d128_kernel): the transposed scheme with every TMEM region
-//              reused in place (S^T -> P^T, dP^T -> dS'^T -> dQ), see the kernel's comment.
+//              reused in place (S^T -> P^T, dP^T -> dS'^T -> dQ^T), dQ added with fp32 reductions
+//              straight from registers, see the kernel's comment.
 // Plus D = rowsum(dO * O) (attn_dvec_kernel) and the fp32 dQ -> bf16 cast (attn_dq_cast_kernel).
 #include <cmath>
 #include <cstdlib>
@@ -79,13 +80,14 @@ struct AttnTask {
 constexpr int kGroupZ = 16;
 __device__ unsigned int g_sched[4];  // [fwd counter, fwd done, bwd counter, bwd done]
 
-__device__ __forceinline__ AttnTask group_task(int t, int nz, int nt, bool longest_is_last_tile) {
-  const int per = kGroupZ * nt;
+__device__ __forceinline__ AttnTask group_task(int t, int nz, int nt, bool longest_is_last_tile,
+                                              int group = kGroupZ) {
+  const int per = group * nt;
   const int g = t / per;
   const int rem = t - g * per;
-  const int gz = min(kGroupZ, nz - g * kGroupZ);
+  const int gz = min(group, nz - g * group);
   const int rank = rem / gz;  // 0 = longest
-  return {longest_is_last_tile ? nt - 1 - rank : rank, g * kGroupZ + rem % gz};
+  return {longest_is_last_tile ? nt - 1 - rank : rank, g * group + rem % gz};
 }
 __device__ __forceinline__ AttnTask fwd_task(int t, int nz, int nt) { return group_task(t, nz, nt, true); }
 // Backward: static round-robin, tile-major (longest key tiles first) over all (sample, head)
@@ -102,6 +104,16 @@ __device__ __forceinline__ float lds_f32(const float* p) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(ptx::smem_u32(p)) : "memory");
   return v;
+}
+// Four consecutive floats; one wavefront when the whole warp reads the same address (broadcast).
+__device__ __forceinline__ float4 lds_v4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ptx::smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 __device__ __forceinline__ void sts_f32(float* p, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(ptx::smem_u32(p)), "f"(v) : "memory");
@@ -1148,9 +1160,12 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 // MMA issue order per tile: dV(i) | S^T(i+1) | dK(i) | dQ(i) | dP^T(i+1): S^T of the next tile is
 // issued as soon as dV has consumed P^T (the tensor pipe executes in order), so the eight builder
 // warps compute the next tile's exponentials while dK / dQ run; dP^T(i+1) waits until the four dQ
-// warps have read dQ(i) out of TMEM. dS'^T also goes to shared memory for the dQ product (MN-major
-// A operand); the dQ warps stage dQ through that same region and add it into fp32 dQ with TMA
-// bulk reduce-add, then release it to the builders of the next tile.
+// warps have read dQ(i) out of TMEM. dS'^T also goes to shared memory as the MN-major B operand of
+// dQ^T = K^T dS'^T: with the head dims on the TMEM lanes, every fp32 reduction instruction of the dQ
+// warps adds 128 contiguous bytes of one query row (red.global.add, no shared-memory staging that
+// the next tile would wait on; the fp32 reductions run at the L2's ~20 B/clk/SM, measured by
+// tools/microbench/red_bench.cu). Q(i) / dO(i) are released after dK(i), so the next loads start
+// before the dQ product.
 // Warp roles: 0-7 builders (lane quarter w % 4, query half w / 4), 8-11 dQ out + dK/dV epilogue,
 // 12 TMA producer, 13 MMA issuer. K/V single-buffered per task; Q/dO(+LSE, D) two stages.
 constexpr int kB2Threads = 14 * 32;
@@ -1184,9 +1199,8 @@ static_assert(B2Smem::kBytes <= 232448, "backward d128 shared memory");
 
 __global__ void __launch_bounds__(kB2Threads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
-                         const __grid_constant__ CUtensorMap map_dq, const float* __restrict__ lse,
-                         const float* __restrict__ dvec, bf16* __restrict__ dqkv, int seq, int heads, int nz,
-                         float scale, int dbg) {
+                         const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
+                         bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // the SWIZZLE_128B tiles need 1 KiB alignment
   uint8_t* sm = smem_raw;
@@ -1202,7 +1216,6 @@ __global__ void __launch_bounds__(kB2Threads, 1)
   uint64_t* ds_full = bar + 10;   // dS'^T in shared memory (builders, 256)
   uint64_t* mm_done = bar + 11;   // dQ in TMEM (MMA)
   uint64_t* dq_free = bar + 12;   // dQ read out of TMEM (dQ warps, 128)
-  uint64_t* stg_free = bar + 13;  // dQ staging drained (dQ warps, 4)
   uint64_t* acc_full = bar + 14;  // dK, dV complete (MMA)
   uint64_t* acc_free = bar + 15;  // dK, dV read out (epilogue, 128)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
@@ -1216,7 +1229,6 @@ __global__ void __launch_bounds__(kB2Threads, 1)
   if (warp == 12 && lane == 0) {
     ptx::tma_prefetch_desc(&map_qkv);
     ptx::tma_prefetch_desc(&map_do);
-    ptx::tma_prefetch_desc(&map_dq);
     ptx::mbar_init(kv_full, 1);
     ptx::mbar_init(kv_empty, 1);
     for (int i = 0; i < 2; ++i) {
@@ -1230,7 +1242,6 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     ptx::mbar_init(ds_full, 256);
     ptx::mbar_init(mm_done, 1);
     ptx::mbar_init(dq_free, 128);
-    ptx::mbar_init(stg_free, 4);
     ptx::mbar_init(acc_full, 1);
     ptx::mbar_init(acc_free, 128);
     ptx::fence_barrier_init();
@@ -1325,13 +1336,14 @@ __global__ void __launch_bounds__(kB2Threads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             ptx::umma_bf16_ts(tmem + kB2TDK, tmem + kB2TDP + tcol(k), mndesc(sq(it), k), id_t, !first || k > 0);
+          ptx::umma_commit(&qd_empty[it & 1]);  // Q(i), dO(i) are not dQ operands: release the stage now
           ptx::mbar_wait(ds_full, it & 1);
           ptx::tc_fence_after();
           ATR(4, it);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) ptx::umma_bf16(tmem + kB2TDP, mndesc(sds, k), mndesc(sk, k), id_q, k > 0);
+          for (int k = 0; k < 8; ++k)  // dQ^T = K^T dS'^T (head dims on the lanes)
+            ptx::umma_bf16(tmem + kB2TDP, mndesc(sk, k), mndesc(sds, k), id_q, k > 0);
           ptx::umma_commit(mm_done);
-          ptx::umma_commit(&qd_empty[it & 1]);
           if (last) {
             ptx::umma_commit(acc_full);
             ptx::umma_commit(kv_empty);
@@ -1362,15 +1374,20 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           ptx::tmem_ld_32x32b_x32(tmem + kB2TS + lane_off + qh * 64 + c * 32, vs);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
+          for (int e = 0; e < 32; e += 4) {
             const int q = qh * 64 + c * 32 + e;
-            float p0 = ex2(fmaf(__uint_as_float(vs[e]), sl2, -lds_f32(ld + q) * kLog2e));
-            float p1 = ex2(fmaf(__uint_as_float(vs[e + 1]), sl2, -lds_f32(ld + q + 1) * kLog2e));
+            const float4 l4 = lds_v4(ld + q);  // LSE of queries q..q+3 (broadcast)
+            float p[4] = {ex2(fmaf(__uint_as_float(vs[e]), sl2, -l4.x * kLog2e)),
+                          ex2(fmaf(__uint_as_float(vs[e + 1]), sl2, -l4.y * kLog2e)),
+                          ex2(fmaf(__uint_as_float(vs[e + 2]), sl2, -l4.z * kLog2e)),
+                          ex2(fmaf(__uint_as_float(vs[e + 3]), sl2, -l4.w * kLog2e))};
             if (i == tk.tile) {  // diagonal tile: key r > query q gives P = 0
-              if (r > q) p0 = 0.f;
-              if (r > q + 1) p1 = 0.f;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (r > q + u) p[u] = 0.f;
             }
-            pk[c * 16 + e / 2] = pack_bf16(p0, p1);
+            pk[c * 16 + e / 2] = pack_bf16(p[0], p[1]);
+            pk[c * 16 + e / 2 + 1] = pack_bf16(p[2], p[3]);
           }
         }
         ptx::tmem_st_32x32b_x32(tmem + kB2TS + lane_off + qh * 64, pk);  // P^T over this half's S^T
@@ -1389,12 +1406,14 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           ptx::tmem_ld_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64 + c * 32, vp);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
+          for (int e = 0; e < 32; e += 4) {
             const int q = qh * 64 + c * 32 + e;
-            const uint32_t pp = pk[c * 16 + e / 2];
-            const float p0 = __uint_as_float(pp << 16), p1 = __uint_as_float(pp & 0xffff0000u);
-            dk[c * 16 + e / 2] = pack_bf16(p0 * (__uint_as_float(vp[e]) - lds_f32(ld + 128 + q)),
-                                           p1 * (__uint_as_float(vp[e + 1]) - lds_f32(ld + 128 + q + 1)));
+            const float4 d4 = lds_v4(ld + 128 + q);  // D of queries q..q+3 (broadcast)
+            const uint32_t pa = pk[c * 16 + e / 2], pb = pk[c * 16 + e / 2 + 1];
+            dk[c * 16 + e / 2] = pack_bf16(__uint_as_float(pa << 16) * (__uint_as_float(vp[e]) - d4.x),
+                                           __uint_as_float(pa & 0xffff0000u) * (__uint_as_float(vp[e + 1]) - d4.y));
+            dk[c * 16 + e / 2 + 1] = pack_bf16(__uint_as_float(pb << 16) * (__uint_as_float(vp[e + 2]) - d4.z),
+                                               __uint_as_float(pb & 0xffff0000u) * (__uint_as_float(vp[e + 3]) - d4.w));
           }
         }
         ptx::tmem_st_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64, dk);
@@ -1402,9 +1421,8 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tc_fence_before();
         if (warp == 0 && lane == 0) ATR(8, it);
         ptx::mbar_arrive(dst_full);
-        // dS'^T into shared memory for dQ = dS' K, once the previous tile's dQ staging drained
-        ptx::mbar_wait(stg_free, (it & 1) ^ 1);
-        if (warp == 0 && lane == 0) ATR(9, it);
+        // dS'^T into shared memory: the B operand of dQ^T = K^T dS'^T. dQ^T(i-1) has finished reading
+        // it: it precedes dP^T(i) in the in-order tensor pipe.
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           st_shared_v4(sds + p_off(r, qh * 64 + g * 8), dk[4 * g], dk[4 * g + 1], dk[4 * g + 2], dk[4 * g + 3]);
@@ -1415,15 +1433,14 @@ __global__ void __launch_bounds__(kB2Threads, 1)
     }
   } else if (warp < 12) {  // ------------------------------------------ warps 8-11: dQ + dK/dV out
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;
+    const int r = q4 * 32 + lane;  // TMEM lane: head dim of dQ^T, key row of dK / dV
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
-    uint8_t* stg = sm + B2Smem::kDS + q4 * (2 * 32 * 32 * 4);  // two [32 x 32] fp32 boxes per warp
     uint32_t it = 0, item = 0;
     for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++item) {
       const AttnTask tk = group_task(t, nz, nt, false);
       const int smp = tk.z / heads, head = tk.z % heads;
       for (int i = tk.tile; i < nt; ++i, ++it) {
-        ptx::mbar_wait(mm_done, it & 1);  // dQ(i) in TMEM; dS' shared memory consumed
+        ptx::mbar_wait(mm_done, it & 1);  // dQ^T(i) in TMEM
         ptx::tc_fence_after();
         if (warp == 8 && lane == 0) ATR(11, it);
         uint32_t v[4][32];
@@ -1435,31 +1452,17 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tc_fence_before();
         if (warp == 8 && lane == 0) ATR(12, it);
         ptx::mbar_arrive(dq_free);  // the MMA warp may put dP^T(i+1) into these columns
-        const int row = smp * seq + i * kT + q4 * 32;
+        // dQ^T: lane = head dim r, column = query; each reduction instruction adds one query row's
+        // 32 consecutive head dims (128 B, coalesced) into fp32 dQ. The reductions need no shared
+        // memory, so nothing waits for them to drain.
+        float* dst = dq32 + (int64_t(smp) * seq + int64_t(i) * kT) * h + head * kD2 + r;
+        if (!(dbg & 1)) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint8_t* box = stg + (c & 1) * (32 * 32 * 4);
-          if (lane == 0 && c >= 2) ptx::bulk_wait_read<1>();  // this box's previous reduce read it
-          __syncwarp();
-          const uint32_t rowa = ptx::smem_u32(box) + lane * 128;
+          for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + ((j ^ (lane & 7)) << 4)),
-                         "r"(v[c][4 * j]), "r"(v[c][4 * j + 1]), "r"(v[c][4 * j + 2]), "r"(v[c][4 * j + 3])
-                         : "memory");
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            if (!(dbg & 1)) ptx::tma_reduce_add_2d(&map_dq, box, head * kD2 + 32 * c, row);
-            ptx::bulk_commit();
-          }
+            for (int j = 0; j < 32; ++j) red_add_f32(dst + int64_t(c * 32 + j) * h, __uint_as_float(v[c][j]));
         }
-        if (lane == 0) {
-          ptx::bulk_wait_read<0>();
-          if (warp == 8) ATR(13, it);
-          ptx::mbar_arrive(stg_free);  // the builders may write the next dS'^T over the boxes
-        }
-        __syncwarp();
+        if (warp == 8 && lane == 0) ATR(13, it);
       }
       // epilogue: dK (scaled), dV rows of this key tile -> bf16 into dqkv
       ptx::mbar_wait(acc_full, item & 1);
@@ -1489,7 +1492,6 @@ __global__ void __launch_bounds__(kB2Threads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(acc_free);
     }
-    if (lane == 0) ptx::bulk_wait<0>();  // dQ reductions complete before the kernel ends
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1672,9 +1674,8 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
   }
   const int h = heads * kD2;
   const int64_t T = batch * seq;
-  CUtensorMap mq, md, mdq;
-  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h) || !map_f32_rows(&mdq, dq32, T, h))
-    return cudaErrorInvalidValue;
+  CUtensorMap mq, md;
+  if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
   attn_dvec_kernel<128><<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
   note_launch();
@@ -1683,9 +1684,9 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
   const float scale = 1.0f / std::sqrt(float(kD2));
-  static int dbg = -1;  // diagnostics (ZP_ATTN_DBG): bit 0 = skip the dQ reduce-add
+  static int dbg = -1;  // diagnostics (ZP_ATTN_DBG): bit 0 = skip the dQ reductions (wrong dQ)
   if (dbg < 0) dbg = std::getenv("ZP_ATTN_DBG") ? std::atoi(std::getenv("ZP_ATTN_DBG")) : 0;
-  attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, mdq, lse, dvec, dqkv, seq,
+  attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
                                                                                 heads, nz, scale, dbg);
   note_launch();
   attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h, scale);

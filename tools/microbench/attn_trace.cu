@@ -66,7 +66,7 @@ int main(int argc, char** argv) {
   unsigned long long tr[16][64];
   cudaMemcpyFromSymbol(tr, zp::g_attn_trace, sizeof(tr));
   const char* names[14] = {"dP_iss", "dV_iss", "S_iss", "dK_iss", "dQ_iss", "P_beg", "P_end",
-                           "dS_beg", "dS_end", "stg_ok", "dSsm_end", "dQ_rd", "dQ_free", "stg_free"};
+                           "dS_beg", "dS_end", "unused", "dSsm_end", "dQ_rd", "dQ_free", "red_end"};
   const unsigned long long t0 = tr[0][0];
   printf("tile");
   for (int e = 0; e < 14; ++e) printf(" %9s", names[e]);
