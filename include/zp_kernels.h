@@ -61,6 +61,22 @@ int zp_attention_fwd_hd(const void* qkv, void* out, float* lse, int64_t batch, i
 int zp_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
                      float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t max_ctas,
                      void* stream);
+/* Same with an explicit head_dim (64 or 128; dq32 [batch*seq, heads*head_dim]). */
+int zp_attention_bwd_hd(const void* qkv, const void* out, const void* dout, const float* lse, float* dvec,
+                        float* dq32, void* dqkv, int64_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                        int32_t max_ctas, void* stream);
+
+/* LayerNorm (rms = 0) / RMSNorm (rms = 1) backward over `rows` rows of h (a multiple of 256)
+ * columns, bf16 in / out, given the forward's per-row mean and rstd (fp32; RMS: mean = 0):
+ * dx = dres + rstd * (gamma * dy - mean(gamma * dy) - xhat * mean(gamma * dy * xhat)), the
+ * mean(gamma * dy) term only for LayerNorm; dres optional (NULL = 0). Column partials (fp32,
+ * summed over the row chunk of each of *nparts CTAs): part[k*h + c] = dgamma, part[(*nparts + k)*h
+ * + c] = dbeta (LayerNorm), colsum_part[k*h + c] (optional) = sum of dx. Capacities in floats:
+ * part >= 2 * 592 * h, colsum_part >= 592 * h (592 = 4 x 148 CTAs, the largest split). */
+int zp_norm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
+                const void* dres, void* dx, float* part, int64_t part_capacity, float* colsum_part,
+                int64_t colsum_capacity, int32_t* nparts, int64_t rows, int32_t h, int32_t rms, int32_t max_ctas,
+                void* stream);
 
 /* ---- NVLink peer-memory collectives (csrc/cuda/peer.cu), emulated on ONE device for parity.
  * A peer group is n "rank arenas": n equal regions of `arena_bytes` starting at `base` (device

@@ -51,6 +51,27 @@ extern "C" int zp_attention_bwd(const void* qkv, const void* out, const void* do
   return e == cudaSuccess ? 0 : 5;
 }
 
+extern "C" int zp_norm_bwd(const void* dy, const void* x, const float* mean, const float* rstd, const void* gamma,
+                           const void* dres, void* dx, float* part, int64_t part_capacity, float* colsum_part,
+                           int64_t colsum_capacity, int32_t* nparts, int64_t rows, int32_t h, int32_t rms,
+                           int32_t max_ctas, void* stream) {
+  if (!dy || !x || !mean || !rstd || !gamma || !dx || !part || !nparts || rows < 1 || h < 256 || h % 256 ||
+      part_capacity < int64_t(2) * 592 * h || (colsum_part && colsum_capacity < int64_t(592) * h))
+    return 1;
+  int dev = 0, ctas = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&ctas, cudaDevAttrMultiProcessorCount, dev);
+  if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
+  int nb = 0;
+  const cudaError_t e =
+      zp::layernorm_bwd(static_cast<const zp::bf16*>(dy), static_cast<const zp::bf16*>(x), mean, rstd,
+                        static_cast<const zp::bf16*>(gamma), static_cast<const zp::bf16*>(dres),
+                        static_cast<zp::bf16*>(dx), part, &nb, rows, h, ctas, static_cast<cudaStream_t>(stream),
+                        rms != 0, colsum_part);
+  *nparts = nb;
+  return e == cudaSuccess ? 0 : (e == cudaErrorInvalidValue ? 1 : 5);
+}
+
 // ---- peer-memory collectives, all ranks of a group emulated on one device (include/zp_kernels.h)
 struct zp_peer_group {
   zp::PeerView pv;  // rank 0's view; the emulated launch derives every rank's

@@ -395,6 +395,120 @@ __global__ void __launch_bounds__(kThreads, 2) ln_bwd_fused_k(const bf16* __rest
   }
 }
 
+// The same backward for wide rows (h = 2048 V): the whole CTA takes one row at a time, thread t
+// owning columns 8t + 2048v (v < V), so the row sits in registers for both passes (the warp-per-row
+// kernel above re-reads each row from L2 and, at one 128 KB-smem CTA per SM, stays latency-bound
+// at ~0.5 of HBM for h = 4096). The row statistics are one block reduction per row through a
+// double-buffered shared array (one barrier per row); the next row's loads are issued before it.
+// dgamma / dbeta / dx column partials accumulate in registers: no shared-memory slices. Output
+// layout as ln_bwd_fused_k: part[blk][h] (dgamma), part[grid + blk][h] (dbeta), cs[blk][h].
+template <bool RMS, bool CS, int V>
+__global__ void __launch_bounds__(kThreads, 2) ln_bwd_rows_k(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd,
+                                                          const bf16* __restrict__ g, const bf16* dres, bf16* dx,
+                                                          int64_t rows, int64_t chunk, float* __restrict__ part,
+                                                          float* __restrict__ cs) {
+  constexpr int h = 2048 * V;
+  __shared__ float2 red[2][kThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int col0 = threadIdx.x * 8;
+  float gg[V][8], ag[V][8], ab[V][8], ac[V][8];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    unpack8(*reinterpret_cast<const uint4*>(g + col0 + 2048 * v), gg[v]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ag[v][k] = ab[v][k] = ac[v][k] = 0.f;
+  }
+  const int64_t r0 = blockIdx.x * chunk;
+  const int64_t r1 = min(rows, r0 + chunk);
+  uint4 qx[V], qd[V], qr[V];
+  auto load = [&](int64_t r, uint4 (&ox)[V], uint4 (&od)[V], uint4 (&orr)[V]) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t o = r * h + col0 + 2048 * v;
+      ox[v] = *reinterpret_cast<const uint4*>(x + o);
+      od[v] = *reinterpret_cast<const uint4*>(dy + o);
+      orr[v] = dres ? *reinterpret_cast<const uint4*>(dres + o) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (r0 < r1) load(r0, qx, qd, qr);
+  for (int64_t r = r0; r < r1; ++r) {
+    uint4 nx[V], nd[V], nr[V];
+    if (r + 1 < r1) load(r + 1, nx, nd, nr);  // in flight during this row's reduction
+    if (r + 2 < r1) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int64_t o = (r + 2) * h + col0 + 2048 * v;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + o));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(dy + o));
+      }
+    }
+    const float mu = RMS ? 0.f : mean[r], rs = rstd[r];
+    float xv[V][8], dv[V][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      unpack8(qx[v], xv[v]);
+      unpack8(qd[v], dv[v]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        xv[v][k] = (xv[v][k] - mu) * rs;  // x-hat
+        const float gd = gg[v][k] * dv[v][k];
+        s1 += gd;
+        s2 += gd * xv[v][k];
+      }
+    }
+    s2 = warp_sum(s2);
+    if (!RMS) s1 = warp_sum(s1);
+    if (lane == 0) red[r & 1][w] = make_float2(s1, s2);
+    __syncthreads();
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) {
+      const float2 p = red[r & 1][i];
+      t1 += p.x;
+      t2 += p.y;
+    }
+    const float m1 = RMS ? 0.f : t1 * (1.0f / h), m2 = t2 * (1.0f / h);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float o[8];
+      unpack8(qr[v], o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        o[k] += rs * (gg[v][k] * dv[v][k] - m1 - xv[v][k] * m2);
+        ag[v][k] += xv[v][k] * dv[v][k];
+        if (!RMS) ab[v][k] += dv[v][k];
+        if (CS) ac[v][k] += o[k];
+      }
+      *reinterpret_cast<uint4*>(dx + r * h + col0 + 2048 * v) = pack8(o);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      qx[v] = nx[v];
+      qd[v] = nd[v];
+      qr[v] = nr[v];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    float* pg = part + int64_t(blockIdx.x) * h + col0 + 2048 * v;
+    *reinterpret_cast<float4*>(pg) = make_float4(ag[v][0], ag[v][1], ag[v][2], ag[v][3]);
+    *reinterpret_cast<float4*>(pg + 4) = make_float4(ag[v][4], ag[v][5], ag[v][6], ag[v][7]);
+    if (!RMS) {
+      float* pb = part + int64_t(gridDim.x + blockIdx.x) * h + col0 + 2048 * v;
+      *reinterpret_cast<float4*>(pb) = make_float4(ab[v][0], ab[v][1], ab[v][2], ab[v][3]);
+      *reinterpret_cast<float4*>(pb + 4) = make_float4(ab[v][4], ab[v][5], ab[v][6], ab[v][7]);
+    }
+    if (CS) {
+      float* pc = cs + int64_t(blockIdx.x) * h + col0 + 2048 * v;
+      *reinterpret_cast<float4*>(pc) = make_float4(ac[v][0], ac[v][1], ac[v][2], ac[v][3]);
+      *reinterpret_cast<float4*>(pc + 4) = make_float4(ac[v][4], ac[v][5], ac[v][6], ac[v][7]);
+    }
+  }
+}
+
 // dgamma / dbeta partial column sums over a chunk of rows: block (32, 8) covers 256 columns.
 // part[chunk][h] holds dgamma partials, part[nchunks + chunk][h] dbeta partials.
 template <bool RMS>
@@ -1131,6 +1245,21 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
                           const bf16* g, const bf16* dres, bf16* dx, float* part, int* nblk,
                           int64_t rows, int h, int ctas, cudaStream_t s, bool rms, float* cs) {
   if (h % 256) return cudaErrorInvalidValue;
+  static const bool rows_kernel = !std::getenv("ZP_LN_ROWS") || std::atoi(std::getenv("ZP_LN_ROWS")) != 0;
+  if (rows_kernel && (h == 2048 || (h == 4096 && rms && !cs))) {  // wide rows: one row per CTA step
+    int grid = int(std::min<int64_t>(int64_t(ctas) * 2, rows));
+    if (grid < 1) grid = 1;
+    const int64_t chunk = (rows + grid - 1) / grid;
+    grid = int((rows + chunk - 1) / chunk);
+    *nblk = grid;
+    // (h = 4096 only for RMSNorm without the dx column sums: more accumulators would spill)
+    const auto kern = h == 4096 ? ln_bwd_rows_k<true, false, 2>
+                      : rms     ? (cs ? ln_bwd_rows_k<true, true, 1> : ln_bwd_rows_k<true, false, 1>)
+                                : (cs ? ln_bwd_rows_k<false, true, 1> : ln_bwd_rows_k<false, false, 1>);
+    kern<<<grid, kThreads, 0, s>>>(dy, x, mean, rstd, g, dres, dx, rows, chunk, part, cs);
+    note_launch();
+    return cudaGetLastError();
+  }
   const int Q = (rms ? 1 : 2) + (cs ? 1 : 0);
   const size_t smem = size_t(kThreads / 32) * Q * h * sizeof(float);
   if (smem <= 200 * 1024) {
