@@ -1200,7 +1200,8 @@ static_assert(B2Smem::kBytes <= 232448, "backward d128 shared memory");
 __global__ void __launch_bounds__(kB2Threads, 1)
     attn_bwd_d128_kernel(const __grid_constant__ CUtensorMap map_qkv, const __grid_constant__ CUtensorMap map_do,
                          const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq32,
-                         bf16* __restrict__ dqkv, int seq, int heads, int nz, float scale, int dbg) {
+                         bf16* __restrict__ dqkv, const float2* __restrict__ rope_tab, int seq, int heads, int nz,
+                         float scale, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   if (ptx::smem_u32(smem_raw) & 1023) __trap();  // the SWIZZLE_128B tiles need 1 KiB alignment
   uint8_t* sm = smem_raw;
@@ -1464,12 +1465,48 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         }
         if (warp == 8 && lane == 0) ATR(13, it);
       }
-      // epilogue: dK (scaled), dV rows of this key tile -> bf16 into dqkv
+      // epilogue: dK (scaled), dV rows of this key tile -> bf16 into dqkv. With rope_tab, dK leaves
+      // through the inverse rotary embedding (the forward rotated K in the QKV GEMM epilogue):
+      // column pairs (j, j + 64) are chunks c and c + 2 of the same thread's row.
       ptx::mbar_wait(acc_full, item & 1);
       ptx::tc_fence_after();
       const int64_t krow = int64_t(smp) * seq + int64_t(tk.tile) * kT + r;
+      auto store32 = [&](bf16* dst, const uint32_t (&w)[32], float f) {  // bf16(f * w) (w: fp32 bits)
 #pragma unroll
-      for (int which = 0; which < 2; ++which) {
+        for (int e = 0; e < 32; e += 8) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(w[e]) * f, __uint_as_float(w[e + 1]) * f);
+          u.y = pack_bf16(__uint_as_float(w[e + 2]) * f, __uint_as_float(w[e + 3]) * f);
+          u.z = pack_bf16(__uint_as_float(w[e + 4]) * f, __uint_as_float(w[e + 5]) * f);
+          u.w = pack_bf16(__uint_as_float(w[e + 6]) * f, __uint_as_float(w[e + 7]) * f);
+          *reinterpret_cast<uint4*>(dst + e) = u;
+        }
+      };
+      if (rope_tab) {
+        bf16* dst = dqkv + krow * 3 * h + h + head * kD2;
+        const float4* cs4 = reinterpret_cast<const float4*>(rope_tab + int64_t(tk.tile * kT + r) * (kD2 / 2));
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t ua[32], ub[32];
+          ptx::tmem_ld_32x32b_x32(tmem + kB2TDK + lane_off + c * 32, ua);
+          ptx::tmem_ld_32x32b_x32(tmem + kB2TDK + lane_off + 64 + c * 32, ub);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {  // in place; the softmax scale is applied by store32
+            const float4 w = cs4[(c * 32 + e) >> 1];  // (cos, sin) of frequencies 32c + e, +1
+            const float a0 = __uint_as_float(ua[e]), b0 = __uint_as_float(ub[e]);
+            const float a1 = __uint_as_float(ua[e + 1]), b1 = __uint_as_float(ub[e + 1]);
+            ua[e] = __float_as_uint(fmaf(a0, w.x, b0 * w.y));  // inverse rotation: a cos + b sin,
+            ub[e] = __float_as_uint(fmaf(b0, w.x, -a0 * w.y));  //                   b cos - a sin
+            ua[e + 1] = __float_as_uint(fmaf(a1, w.z, b1 * w.w));
+            ub[e + 1] = __float_as_uint(fmaf(b1, w.z, -a1 * w.w));
+          }
+          store32(dst + c * 32, ua, scale);
+          store32(dst + 64 + c * 32, ub, scale);
+        }
+      }
+#pragma unroll 1
+      for (int which = rope_tab ? 1 : 0; which < 2; ++which) {
         bf16* dst = dqkv + krow * 3 * h + (which == 0 ? h : 2 * h) + head * kD2;
         const uint32_t src = tmem + (which == 0 ? kB2TDK : kB2TDV) + lane_off;
         const float f = which == 0 ? scale : 1.f;  // dK = scale * dS'^T Q
@@ -1478,15 +1515,7 @@ __global__ void __launch_bounds__(kB2Threads, 1)
           uint32_t w[32];
           ptx::tmem_ld_32x32b_x32(src + c * 32, w);
           ptx::tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 u;
-            u.x = pack_bf16(__uint_as_float(w[e]) * f, __uint_as_float(w[e + 1]) * f);
-            u.y = pack_bf16(__uint_as_float(w[e + 2]) * f, __uint_as_float(w[e + 3]) * f);
-            u.z = pack_bf16(__uint_as_float(w[e + 4]) * f, __uint_as_float(w[e + 5]) * f);
-            u.w = pack_bf16(__uint_as_float(w[e + 6]) * f, __uint_as_float(w[e + 7]) * f);
-            *reinterpret_cast<uint4*>(dst + c * 32 + e) = u;
-          }
+          store32(dst + c * 32, w, f);
         }
       }
       ptx::tc_fence_before();
@@ -1556,6 +1585,43 @@ __global__ void attn_dq_cast_kernel(const float* __restrict__ dq32, bf16* __rest
     o.z = pack_bf16(b.x * scale, b.y * scale);
     o.w = pack_bf16(b.z * scale, b.w * scale);
     *reinterpret_cast<uint4*>(dqkv + tok * 3 * h + col) = o;
+  }
+}
+
+// The same cast through the inverse rotary embedding (head_dim D): one item = 8 rotation pairs
+// (j, j + D/2) of one (token, head), read from fp32 dQ, rotated back by the token's position.
+template <int D>
+__global__ void attn_dq_cast_rope_kernel(const float* __restrict__ dq32, bf16* __restrict__ dqkv,
+                                         const float2* __restrict__ tab, int64_t tokens, int seq, int h,
+                                         float scale) {
+  constexpr int half = D / 2, groups = half / 8;
+  const int per_row = (h / D) * groups;
+  const int64_t n = tokens * per_row;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t tok = i / per_row;
+    const int r = int(i - tok * per_row);
+    const int col = (r / groups) * D + (r % groups) * 8;  // head start + first pair's column
+    const int j0 = (r % groups) * 8;
+    const float4* pa = reinterpret_cast<const float4*>(dq32 + tok * h + col);
+    const float4* pb = reinterpret_cast<const float4*>(dq32 + tok * h + col + half);
+    const float4 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
+    const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    const float4* cs = reinterpret_cast<const float4*>(tab + int64_t(tok % seq) * half + j0);
+    float oa[8], ob[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 w = cs[k];  // (cos, sin) of pairs 2k, 2k + 1
+      oa[2 * k] = scale * fmaf(a[2 * k], w.x, b[2 * k] * w.y);  // a cos + b sin
+      ob[2 * k] = scale * fmaf(b[2 * k], w.x, -a[2 * k] * w.y);  // b cos - a sin
+      oa[2 * k + 1] = scale * fmaf(a[2 * k + 1], w.z, b[2 * k + 1] * w.w);
+      ob[2 * k + 1] = scale * fmaf(b[2 * k + 1], w.z, -a[2 * k + 1] * w.w);
+    }
+    bf16* d = dqkv + tok * 3 * h + col;
+    *reinterpret_cast<uint4*>(d) = make_uint4(pack_bf16(oa[0], oa[1]), pack_bf16(oa[2], oa[3]),
+                                              pack_bf16(oa[4], oa[5]), pack_bf16(oa[6], oa[7]));
+    *reinterpret_cast<uint4*>(d + half) = make_uint4(pack_bf16(ob[0], ob[1]), pack_bf16(ob[2], ob[3]),
+                                                     pack_bf16(ob[4], ob[5]), pack_bf16(ob[6], ob[7]));
   }
 }
 
@@ -1665,7 +1731,8 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
 }
 
 cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
-                               float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s) {
+                               float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
+                               const float2* rope_tab) {
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1686,19 +1753,25 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
   const float scale = 1.0f / std::sqrt(float(kD2));
   static int dbg = -1;  // diagnostics (ZP_ATTN_DBG): bit 0 = skip the dQ reductions (wrong dQ)
   if (dbg < 0) dbg = std::getenv("ZP_ATTN_DBG") ? std::atoi(std::getenv("ZP_ATTN_DBG")) : 0;
-  attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv, seq,
-                                                                                heads, nz, scale, dbg);
+  attn_bwd_d128_kernel<<<std::min(ntasks, cap), kB2Threads, B2Smem::kBytes, s>>>(mq, md, lse, dvec, dq32, dqkv,
+                                                                                rope_tab, seq, heads, nz, scale, dbg);
   note_launch();
-  attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h, scale);
+  if (rope_tab)
+    attn_dq_cast_rope_kernel<kD2><<<std::min<int64_t>(cap * 4, (T * h / 16 + 255) / 256), 256, 0, s>>>(
+        dq32, dqkv, rope_tab, T, seq, h, scale);
+  else
+    attn_dq_cast_kernel<<<std::min<int64_t>(cap * 4, (T * h / 8 + 255) / 256), 256, 0, s>>>(dq32, dqkv, T, h, scale);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
                           float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
-                          int head_dim) {
+                          int head_dim, const float2* rope_tab) {
   if (seq % kT || batch < 1 || (head_dim != 64 && head_dim != 128)) return cudaErrorInvalidValue;
-  if (head_dim == 128) return attention_bwd_d128(qkv, out, dout, lse, dvec, dq32, dqkv, batch, seq, heads, ctas, s);
+  if (head_dim == 128)
+    return attention_bwd_d128(qkv, out, dout, lse, dvec, dq32, dqkv, batch, seq, heads, ctas, s, rope_tab);
+  if (rope_tab) return cudaErrorInvalidValue;  // head_dim 64: the caller applies the inverse rotation
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

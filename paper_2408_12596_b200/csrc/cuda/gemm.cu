@@ -102,6 +102,8 @@ struct EpiParams {
   int aux_tma;      // residual / GELU-input rows loaded by TMA into the staging boxes
   int aux_out_tma;  // GELU pre-activation written by TMA stores
   float* colsum;    // += column sums of the bf16-path output over the rows (fp32 [N]); may be null
+  const float2* rope_tab;  // kEpiRopeBf16: (cos, sin) [rope_seq][rope_dh / 2]
+  int rope_seq, rope_dh, rope_cols;
 };
 
 // Column sums of one warp's 32 rows x 64 columns (v[g][i]: row = lane, column = 32g + i) added
@@ -608,6 +610,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 *reinterpret_cast<uint4*>(hrow + i) = make_uint4(p[0], p[1], p[2], p[3]);
               }
             }
+          } else if (ep.epilogue == kEpiRopeBf16) {
+            // rotary embedding of the Q / K columns on the fp32 accumulators (one bf16 rounding):
+            // the partner column j +- dh/2 of the same head is re-read from TMEM (the tile is
+            // aligned to heads). Warp-uniform branches only: tcgen05.ld is warp-collective.
+            const int halfd = ep.rope_dh >> 1;
+            const int pos = row % ep.rope_seq;
+#pragma unroll 1
+            for (int g = 0; g < 2; ++g) {
+              const int n = n0 + 32 * g;
+              if (n >= ep.rope_cols) continue;
+              const int j = n % ep.rope_dh;
+              const bool lo = j < halfd;
+              uint32_t pr[32];
+              ptx::tmem_ld_32x32b_x32(tbase + c + 32 * g + (lo ? halfd : -halfd), pr);
+              ptx::tmem_ld_wait();
+              const float4* cs = reinterpret_cast<const float4*>(ep.rope_tab + int64_t(pos) * halfd + (j % halfd));
+              const float sg = lo ? -1.f : 1.f;  // lo: a cos - b sin ; hi: b cos + a sin
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const float4 w = cs[i >> 1];  // (cos, sin) of frequencies f + i, f + i + 1
+                v[g][i] = fmaf(sg * w.y, __uint_as_float(pr[i]), v[g][i] * w.x);
+                v[g][i + 1] = fmaf(sg * w.w, __uint_as_float(pr[i + 1]), v[g][i + 1] * w.z);
+              }
+            }
           } else {
 #pragma unroll
             for (int g = 0; g < 2; ++g) epi_bf16_math(ep, v[g], row_off + n0 + 32 * g, n0 + 32 * g, sched.N, valid);
@@ -745,12 +771,16 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   // bf16 outputs of plain (unbatched) GEMMs go through TMA stores.
   const bool bf16_out = a.epilogue == kEpiStoreBf16 || a.epilogue == kEpiBiasBf16 ||
                         a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiBiasGeluBf16 ||
-                        a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiSwiGluBf16;
+                        a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiSwiGluBf16 || a.epilogue == kEpiRopeBf16;
   if (a.epilogue == kEpiSwiGluBf16 && (a.N % 64 || !a.aux_out || a.nb1 != 1 || a.nb2 != 1))
     return cudaErrorInvalidValue;
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
   if (a.epilogue == kEpiSwiGluBf16 && !tma_store) return cudaErrorInvalidValue;
+  if (a.epilogue == kEpiRopeBf16 &&
+      (!tma_store || !a.rope_tab || a.rope_seq < 1 || (a.rope_dh != 64 && a.rope_dh != 128) || BN % a.rope_dh ||
+       a.rope_cols % a.rope_dh || a.alpha != 1.0f || (reinterpret_cast<uintptr_t>(a.rope_tab) % 16)))
+    return cudaErrorInvalidValue;
   if (a.colsum && !tma_store) return cudaErrorInvalidValue;
   if (!tma_store) mc = ma;  // unused placeholder
   // aux tiles share C's layout (ldc): residual / GELU input loaded, pre-activation stored by TMA
@@ -809,6 +839,10 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.aux_tma = aux_tma ? 1 : 0;
   ep.aux_out_tma = aux_out_tma ? 1 : 0;
   ep.colsum = a.colsum;
+  ep.rope_tab = static_cast<const float2*>(a.rope_tab);
+  ep.rope_seq = a.rope_seq;
+  ep.rope_dh = a.rope_dh;
+  ep.rope_cols = a.rope_cols;
   int units = workers;
   if (s.total < units) units = s.total;
   if (units < 1) return cudaSuccess;

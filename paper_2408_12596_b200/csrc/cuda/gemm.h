@@ -28,6 +28,8 @@ enum GemmEpilogue : int {
   kEpiAtomicF32 = 7,      // C(f32) += alpha*acc with fp32 vector atomics (split-K partials)
   kEpiSwiGluBf16 = 8,     // C(bf16) = acc (gate/up interleaved in 32-column blocks);
                           // aux_out[m, j] (bf16, ld = ldc / 2) = silu(gate_j) * up_j
+  kEpiRopeBf16 = 9,       // C(bf16) = acc, columns [0, rope_cols) rotated (rotate-half pairs
+                          // (j, j + dh/2) of every head of rope_dh) by position m % rope_seq
 };
 
 enum GemmCausal : int {
@@ -59,6 +61,9 @@ struct GemmArgs {
   int max_ctas = 0;            // SM budget cap (0 = all SMs)
   int split_k = 1;             // >1: K range split across CTAs; -1: auto; requires kEpiAtomicF32
   float* colsum = nullptr;     // bf16 epilogues: += column sums of the output (fp32 [N]; bias grad)
+  // kEpiRopeBf16: (cos, sin) table float2 [rope_seq][rope_dh / 2] (kernels.h rope_table)
+  const void* rope_tab = nullptr;
+  int rope_seq = 0, rope_dh = 0, rope_cols = 0;
 };
 
 // Returns cudaSuccess or the launch/encode error.

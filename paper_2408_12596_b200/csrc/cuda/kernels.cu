@@ -1174,7 +1174,7 @@ void embed_fwd(const int32_t* tokens, int seq, const bf16* wte, const bf16* wpe,
   embed_fwd_k<<<grid_for(rows * h / 8, kThreads, ctas), kThreads, 0, s>>>(tokens, seq, wte, wpe, x,
                                                                           rows, h); note_launch();
 }
-void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s, int dh) {
+const float2* rope_table(int seq, int dh, float theta, cudaStream_t s) {
   // per-device cos/sin table for the largest sequence seen on that device (a process may drive
   // several GPUs, one host thread each)
   struct Table {
@@ -1186,24 +1186,26 @@ void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, 
   static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
-  float2* tab = nullptr;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    Table& t = tables[dev & 63];
-    if (seq > t.seq || theta != t.theta || dh / 2 != t.half) {
-      if (t.tab) cudaFree(t.tab);
-      t.tab = nullptr;
-      t.seq = 0;
-      if (cudaMalloc(&t.tab, size_t(seq) * (dh / 2) * sizeof(float2)) != cudaSuccess) return;
-      rope_table_k<<<(seq * (dh / 2) + kThreads - 1) / kThreads, kThreads, 0, s>>>(t.tab, seq, dh / 2,
-                                                                                 std::log(double(theta)));
-      note_launch();
-      t.seq = seq;
-      t.half = dh / 2;
-      t.theta = theta;
-    }
-    tab = t.tab;
+  std::lock_guard<std::mutex> lock(mu);
+  Table& t = tables[dev & 63];
+  if (seq > t.seq || theta != t.theta || dh / 2 != t.half) {
+    if (t.tab) cudaFree(t.tab);
+    t.tab = nullptr;
+    t.seq = 0;
+    if (cudaMalloc(&t.tab, size_t(seq) * (dh / 2) * sizeof(float2)) != cudaSuccess) return nullptr;
+    rope_table_k<<<(seq * (dh / 2) + kThreads - 1) / kThreads, kThreads, 0, s>>>(t.tab, seq, dh / 2,
+                                                                               std::log(double(theta)));
+    note_launch();
+    t.seq = seq;
+    t.half = dh / 2;
+    t.theta = theta;
   }
+  return t.tab;
+}
+
+void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s, int dh) {
+  const float2* tab = rope_table(seq, dh, theta, s);
+  if (!tab) return;
   rope_k<<<grid_for(tokens * 2 * (h / dh) * (dh / 16), kThreads, ctas), kThreads, 0, s>>>(qkv, tab, tokens, seq, h,
                                                                                         dh, inverse ? -1.f : 1.f);
   note_launch();

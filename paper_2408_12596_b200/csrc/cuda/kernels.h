@@ -53,6 +53,9 @@ cudaError_t layernorm_bwd(const bf16* dy, const bf16* x, const float* mean, cons
 // blocks of qkv [T, 3h], in place.
 void rope(bf16* qkv, int64_t tokens, int seq, int h, float theta, bool inverse, int ctas, cudaStream_t s,
           int dh = 64);
+// The (cos, sin) table it uses: float2 [seq][dh / 2], per device, built on first use (nullptr on
+// allocation failure). The QKV GEMM's kEpiRopeBf16 epilogue reads the same table.
+const float2* rope_table(int seq, int dh, float theta, cudaStream_t s);
 // SwiGLU with gate/up interleaved in 32-column blocks of gu [T, 2f]: out [T, f].
 void swiglu_fwd(const bf16* gu, bf16* out, int64_t tokens, int f, int ctas, cudaStream_t s);
 void swiglu_bwd(const bf16* gu, const bf16* dh, bf16* dgu, int64_t tokens, int f, int ctas, cudaStream_t s);

@@ -480,6 +480,31 @@ struct Runtime {
     g.colsum = colsum;
     launch_gemm(g, 2.0 * M * double(N) * K);
   }
+  // Llama QKV projection with the rotary embedding of Q and K applied in the GEMM epilogue on the
+  // fp32 accumulators (kEpiRopeBf16); the inverse rotation of dQ / dK happens in the head_dim-128
+  // attention backward. ZP_ROPE_EPI=0 keeps the separate in-place rope kernels.
+  static bool rope_epi() {
+    static const bool on = !std::getenv("ZP_ROPE_EPI") || std::atoi(std::getenv("ZP_ROPE_EPI")) != 0;
+    return on;
+  }
+  void qkv_rope(int64_t T, const bf16* x, const bf16* w, bf16* qkv) {
+    const int h = int(c.d_model);
+    const float2* tab = rope_epi() ? rope_table(int(c.seq_len), hd(), 10000.f, st) : nullptr;
+    if (!tab) {
+      mm(int(T), 3 * h, h, x, kKMajor, h, w, kKMajor, h, qkv, 3 * h, kEpiStoreBf16);
+      rope(qkv, T, int(c.seq_len), h, 10000.f, false, ctas, st, hd());
+      return;
+    }
+    GemmArgs g;
+    g.M = int(T); g.N = 3 * h; g.K = h;
+    g.a.ptr = x; g.a.major = kKMajor; g.a.ld = h;
+    g.b.ptr = w; g.b.major = kKMajor; g.b.ld = h;
+    g.c = qkv; g.ldc = 3 * h;
+    g.epilogue = kEpiRopeBf16;
+    g.rope_tab = tab; g.rope_seq = int(c.seq_len); g.rope_dh = hd(); g.rope_cols = 2 * h;
+    g.max_ctas = ctas;
+    launch_gemm(g, 2.0 * double(T) * 3 * h * h);
+  }
   // Weight gradient dW[M, N] = sum over the T tokens: few output tiles, very long K. Split K
   // across CTAs (fp32 atomics into a workspace, then a cast) when the tiles cannot fill the
   // rank's SMs.
@@ -849,8 +874,7 @@ struct Runtime {
       z3_gather(i + 1, kAgF);
       bf16* x_out = (i + 1 < c.n_layer) ? A.l[i + 1].x_in : A.x_final;
       CK(layernorm_fwd(L.x_in, Wp(P.ln1_g), nullptr, L.ln1, L.mu1, L.rs1, T, int(h), ctas, st));
-      mm(T, 3 * h, h, L.ln1, kKMajor, h, Wp(P.w_qkv), kKMajor, h, L.qkv, 3 * h, kEpiStoreBf16);
-      rope(L.qkv, T, int(s), int(h), 10000.f, false, ctas, st, hd());
+      qkv_rope(T, L.ln1, Wp(P.w_qkv), L.qkv);
       CK(attention_fwd(L.qkv, L.attn, L.lse, b, int(s), int(H), ctas, st, hd()));
       mm(T, h, h, L.attn, kKMajor, h, Wp(P.w_o), kKMajor, h, L.x_mid, h, kEpiBiasResidBf16, 1.f, nullptr, L.x_in);
       CK(layernorm_fwd(L.x_mid, Wp(P.ln2_g), nullptr, L.ln2, L.mu2, L.rs2, T, int(h), ctas, st));
@@ -895,8 +919,11 @@ struct Runtime {
       // attention
       wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gd(P.w_o));
       mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
-      CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd()));
-      rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st, hd());  // back to pre-rotation Q, K
+      {  // dQ, dK back to pre-rotation Q, K: inside the attention backward at head_dim 128
+        const float2* tab = hd() == 128 && rope_epi() ? rope_table(int(s), hd(), 10000.f, st) : nullptr;
+        CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd(), tab));
+        if (!tab) rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st, hd());
+      }
       wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gd(P.w_qkv));
       mm(T, h, 3 * h, A.dqkv, kKMajor, 3 * h, Wp(P.w_qkv), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_in, L.mu1, L.rs1, Wp(P.ln1_g), A.dx2, A.dx, ln_part, &nblk, T, int(h), ctas, st,
