@@ -859,6 +859,28 @@ static_assert(F2Smem::kBytes <= 232448, "forward d128 shared memory");
 
 __device__ unsigned int g_sched2[4];  // [fwd counter, fwd done, bwd counter, bwd done] (head_dim 128)
 
+// Timeline diagnostics (tools/microbench/attn_trace.cu builds this file with ZP_ATTN_TRACE): CTA 0
+// stamps clock64 at the pipeline events of its first tiles (ATR: backward, ATRF: forward).
+#ifdef ZP_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[16][64];
+__device__ unsigned long long g_attn_trace_f[16][64];
+#define ATR(ev, i)                                                           \
+  do {                                                                       \
+    if (blockIdx.x == 0 && (i) < 64) g_attn_trace[ev][i] = clock64();       \
+  } while (0)
+#define ATRF(ev, i, first)                                                             \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && (first) && (i) < 64) g_attn_trace_f[ev][i] = clock64();    \
+  } while (0)
+#else
+#define ATR(ev, i) \
+  do {             \
+  } while (0)
+#define ATRF(ev, i, first) \
+  do {                     \
+  } while (0)
+#endif
+
 // K-major [128, 128] tile stored as two 64-wide SWIZZLE_128B blocks, k16 step 0..7.
 __device__ __forceinline__ uint64_t kdesc128(uint32_t base, int k16) {
   return ptx::smem_desc_sw128(base + (k16 >> 2) * kBlk + (k16 & 3) * 32, 16, 1024);
@@ -966,7 +988,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           ++kw;
         }
       };
+      uint32_t titem = 0;  // trace: the first task only
       auto issue_s = [&](int g, int kvi) {
+        ATRF(1 + 2 * g, kvi, titem == 0);
         const uint32_t sq = ptx::smem_u32(sm + F2Smem::kQ + g * kTile2);
         const uint32_t sk = ptx::smem_u32(sm + F2Smem::kK + (kvi & 1) * kTile2);
         ptx::tc_fence_after();
@@ -978,6 +1002,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         ptx::mbar_wait(&p_full[g], gp[g] & 1);
         ++gp[g];
         ptx::tc_fence_after();
+        ATRF(2 * g, kvi, titem == 0);
         const uint32_t sv = ptx::smem_u32(sm + F2Smem::kV + (kvi & 1) * kTile2);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -989,6 +1014,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       for (uint32_t item = 0;; ++item) {
         const int t = ring.consume1(item);
         if (t >= ntasks) break;
+        titem = item;
         const AttnTask tk = group_task(t, nz, nb, true);
         const bool has1 = 2 * tk.tile + 1 < nt;
         const int nj0 = 2 * tk.tile + 1, nj1 = has1 ? 2 * tk.tile + 2 : 0;
@@ -1046,9 +1072,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const int qt = 2 * tk.tile + g;  // this group's query tile
       const int nj = qt + 1;           // key tiles 0..qt, qt diagonal
       float m = -INFINITY, l = 0.f;
+      const bool tr = item == 0 && lane == 0 && (warp == 0 || warp == 8);
       for (int j = 0; j < nj; ++j, ++cnt) {
         ptx::mbar_wait(&s_full[g], cnt & 1);
         ptx::tc_fence_after();
+        ATRF(4 + 4 * g, j, tr);
         float sv[64];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1076,6 +1104,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
         const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
         asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
+        ATRF(5 + 4 * g, j, tr);
         const bool raise = mx > m + kRescaleLog2;
         const float alpha = raise ? ex2(m - mx) : 1.f;
         if (raise) m = mx;
@@ -1089,6 +1118,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           ps[(i >> 1) & 7] += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
+        ATRF(6 + 4 * g, j, tr);
         // O += P.V of the previous tile is complete (it precedes this tile's S in the tensor pipe)
         if (j > 0 && __any_sync(0xffffffffu, raise)) {
 #pragma unroll
@@ -1105,6 +1135,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         ptx::tmem_st_32x32b_x32(t_p, pk);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
+        ATRF(7 + 4 * g, j, tr);
         ptx::mbar_arrive(&p_full[g]);
       }
       // epilogue: the last P.V, the halves' row sums, O / l -> bf16, LSE
@@ -1170,19 +1201,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 // 12 TMA producer, 13 MMA issuer. K/V single-buffered per task; Q/dO(+LSE, D) two stages.
 constexpr int kB2Threads = 14 * 32;
 
-// Timeline diagnostics (tools/microbench/attn_trace.cu builds this file with ZP_ATTN_TRACE): CTA 0
-// stamps clock64 at each pipeline event of its first tiles.
-#ifdef ZP_ATTN_TRACE
-__device__ unsigned long long g_attn_trace[16][64];
-#define ATR(ev, i)                                                           \
-  do {                                                                       \
-    if (blockIdx.x == 0 && (i) < 64) g_attn_trace[ev][i] = clock64();       \
-  } while (0)
-#else
-#define ATR(ev, i) \
-  do {             \
-  } while (0)
-#endif
 constexpr int kB2TS = 0, kB2TDP = 128, kB2TDV = 256, kB2TDK = 384;
 
 struct B2Smem {

@@ -3,9 +3,11 @@
 // prints per-query-tile event times relative to the first dP^T issue.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -DZP_ATTN_TRACE -lineinfo \
 //     tools/microbench/attn_trace.cu paper_2408_12596_b200/csrc/cuda/kernels.cu -lcuda -o /tmp/attn_trace
-// Usage: attn_trace [batch 2] [seq 4096] [heads 32] [dbg 0]   (dbg: ZP_ATTN_DBG bits)
+// Usage: attn_trace [batch 2] [seq 4096] [heads 32] [dbg 0] [fwd]   (dbg: ZP_ATTN_DBG bits; "fwd":
+// time and trace the forward instead)
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "../../paper_2408_12596_b200/csrc/cuda/attention.cu"
@@ -44,6 +46,35 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  if (argc > 5 && std::string(argv[5]) == "fwd") {
+    float bestf = 1e30f;
+    for (int r = 0; r < 6; ++r) {
+      cudaEventRecord(e0);
+      if (zp::attention_fwd(qkv, out, lse, batch, seq, heads, 0, nullptr, 128) != cudaSuccess) return 2;
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r > 0 && ms < bestf) bestf = ms;
+    }
+    const double ff = 4.0 * batch * heads * double(seq) * seq * 128 / 2;
+    printf("attention fwd d128 b%lld s%d h%d: %.3f ms, %.0f TFLOP/s causal\n", (long long)batch, seq, heads, bestf,
+           ff / (bestf * 1e-3) / 1e12);
+    unsigned long long tf[16][64];
+    cudaMemcpyFromSymbol(tf, zp::g_attn_trace_f, sizeof(tf));
+    const char* fn[12] = {"PV0_iss", "S0_iss", "PV1_iss", "S1_iss", "g0_sfull", "g0_max", "g0_exp", "g0_pfull",
+                          "g1_sfull", "g1_max", "g1_exp", "g1_pfull"};
+    const unsigned long long f0 = tf[1][0];
+    printf("tile");
+    for (int e = 0; e < 12; ++e) printf(" %9s", fn[e]);
+    printf("   period\n");
+    for (int i = 0; i < seq / 128 && i < 64; ++i) {
+      printf("%4d", i);
+      for (int e = 0; e < 12; ++e) printf(" %9lld", (long long)(tf[e][i] - f0));
+      printf("   %6lld\n", i ? (long long)(tf[1][i] - tf[1][i - 1]) : 0LL);
+    }
+    return 0;
+  }
   float best = 1e30f;
   for (int r = 0; r < 6; ++r) {
     cudaEventRecord(e0);
