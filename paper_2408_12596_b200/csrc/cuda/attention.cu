@@ -851,8 +851,8 @@ struct F2Smem {
   static constexpr int kQ = 0;                     // Q0, Q1
   static constexpr int kK = kQ + 2 * kTile2;       // 2 stages
   static constexpr int kV = kK + 2 * kTile2;       // 2 stages
-  static constexpr int kRed = kV + 2 * kTile2;     // [2 groups][2 halves][128 rows] fp32
-  static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
+  static constexpr int kRed = kV + 2 * kTile2;     // [2 groups][3 buffers][2 halves][128 rows] fp32
+  static constexpr int kBar = kRed + 2 * 3 * 2 * 128 * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 static_assert(F2Smem::kBytes <= 232448, "forward d128 shared memory");
@@ -1057,7 +1057,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
     const int nbar = 1 + g * 4 + q4;         // named barrier of the row quarter's two halves
     const int r = q4 * 32 + lane;            // query row within the tile == TMEM lane
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
-    float* red = reinterpret_cast<float*>(sm + F2Smem::kRed) + g * 256;  // [2 halves][128]
+    // row-statistics exchange between the two halves of a row: [3 buffers][2 halves][128]; the
+    // per-tile max alternates between buffers 0 and 1 (one barrier per tile: a half rewrites a
+    // buffer only after the barrier of the next tile, which its partner passes after reading it),
+    // buffer 2 carries the final row sum
+    float* red0 = reinterpret_cast<float*>(sm + F2Smem::kRed) + g * 768;
     const uint32_t t_s = tmem + 128 * g + lane_off + kh * 64;
     const uint32_t t_p = tmem + 128 * g + lane_off + kh * 64;  // packed P over this half's S columns
     const uint32_t t_o = tmem + 256 + 128 * g + lane_off + kh * 64;
@@ -1078,13 +1082,16 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         ptx::tc_fence_after();
         ATRF(4 + 4 * g, j, tr);
         float sv[64];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t v[32];
-          ptx::tmem_ld_32x32b_x32(t_s + c * 32, v);
+        {
+          uint32_t v0[32], v1[32];
+          ptx::tmem_ld_32x32b_x32(t_s, v0);
+          ptx::tmem_ld_32x32b_x32(t_s + 32, v1);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(v[i]);
+          for (int i = 0; i < 32; ++i) {
+            sv[i] = __uint_as_float(v0[i]);
+            sv[32 + i] = __uint_as_float(v1[i]);
+          }
         }
         if (j == qt) {  // diagonal tile: key > query is masked
 #pragma unroll
@@ -1099,11 +1106,11 @@ __global__ void __launch_bounds__(kF2Threads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) pm[k] = fmaxf(pm[k], sv[i + k]);
         }
+        float* red = red0 + (cnt & 1) * 256;
         sts_f32(&red[kh * 128 + r], fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                           fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))));
         asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
         const float mx = fmaxf(lds_f32(&red[r]), lds_f32(&red[128 + r])) * scale_log2;
-        asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
         ATRF(5 + 4 * g, j, tr);
         const bool raise = mx > m + kRescaleLog2;
         const float alpha = raise ? ex2(m - mx) : 1.f;
@@ -1112,8 +1119,8 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 64; i += 2) {
-          const bool poly = ((i >> 1) & 3) < POLY;
           const float x0 = fmaf(sv[i], scale_log2, -m), x1 = fmaf(sv[i + 1], scale_log2, -m);
+          const bool poly = ((i >> 1) & 3) < POLY;
           const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
           ps[(i >> 1) & 7] += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
@@ -1148,10 +1155,10 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&o_free[g]);
       ++ntk;
+      float* red = red0 + 512;  // buffer 2: rewritten only after the next task's tile barriers
       sts_f32(&red[kh * 128 + r], l);
       asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
       const float lt = lds_f32(&red[r]) + lds_f32(&red[128 + r]);
-      asm volatile("bar.sync %0, 64;" ::"r"(nbar) : "memory");
       const float inv = 1.f / lt;
       const int64_t row = int64_t(smp) * seq + int64_t(qt) * kT + r;
       bf16* dst = out + row * h + head * kD2 + kh * 64;

@@ -25,6 +25,12 @@ __global__ void k(float* out, int iters) {
       asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h3) : "f"(x3), "f"(x0));
       x0 = __uint_as_float(h0 ^ 0x3f800000u); x1 = __uint_as_float(h1 ^ 0x3f800000u);
       x2 = __uint_as_float(h2 ^ 0x3f800000u); x3 = __uint_as_float(h3 ^ 0x3f800000u);
+    } else if (MODE == 5) {
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h0)); asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h1));
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h2)); asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h3));
+    } else if (MODE == 6) {
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h0)); asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h1));
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h2)); asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(h3));
     } else {
       asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x0)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x1));
       asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x2)); asm volatile("rcp.approx.ftz.f32 %0, %0;" : "+f"(x3));
@@ -35,16 +41,19 @@ __global__ void k(float* out, int iters) {
   if (x0 + x1 + x2 + x3 == 12345.f || (h0 ^ h1 ^ h2 ^ h3) == 1u) out[8] = 1;
 }
 int main() {
-  float* d; cudaMalloc(&d, 64);
+  float* d; cudaMalloc(&d, 64);  // out[0..6] cycles, out[8] sink
   const int iters = 4096, threads = 1024;
-  const char* n[5] = {"tanh.f32", "ex2.f32", "tanh.bf16x2", "rcp.f32", "cvt.bf16x2 (+4 LOP)"};
-  for (int m = 0; m < 5; ++m) {
+  const char* n[7] = {"tanh.f32", "ex2.f32", "tanh.bf16x2", "rcp.f32", "cvt.bf16x2 (+4 LOP)", "ex2.f16x2",
+                      "ex2.bf16x2"};
+  for (int m = 0; m < 7; ++m) {
     for (int r = 0; r < 2; ++r) {
       if (m == 0) k<0><<<148, threads>>>(d, iters);
       if (m == 1) k<1><<<148, threads>>>(d, iters);
       if (m == 2) k<2><<<148, threads>>>(d, iters);
       if (m == 3) k<3><<<148, threads>>>(d, iters);
       if (m == 4) k<4><<<148, threads>>>(d, iters);
+      if (m == 5) k<5><<<148, threads>>>(d, iters);
+      if (m == 6) k<6><<<148, threads>>>(d, iters);
     }
     cudaDeviceSynchronize();
     float c; cudaMemcpy(&c, d + m, 4, cudaMemcpyDeviceToHost);
