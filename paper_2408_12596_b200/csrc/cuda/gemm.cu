@@ -343,6 +343,69 @@ __device__ __forceinline__ void epilogue_row32(const EpiParams& ep, const uint32
   }
 }
 
+// kEpiSwiGluBwdBf16, one 64-column chunk of dh = features [n0, n0 + 64) of this warp's 32 rows:
+// u columns [2 n0, 2 n0 + 128) arrive by TMA as two [32 x 64] boxes (box j: gate | up of features
+// n0 + 32j .. +31), (dgate, dup) overwrite them in place and leave by TMA store into C. Same math as
+// kernels.cu swiglu_bwd_k, from the fp32 dh instead of its bf16 copy.
+__device__ __forceinline__ void swiglu_bwd_chunk(uint32_t tcol, int n0, int r0, int lane, uint8_t* stage_buf,
+                                                 uint64_t* ab, uint32_t (&ph)[2], const CUtensorMap* map_u,
+                                                 const CUtensorMap* map_c) {
+  if (lane == 0) {
+    ptx::bulk_wait_read<0>();  // the previous chunk's stores have read the boxes
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      ptx::mbar_arrive_expect_tx(&ab[j], kStageBufBytes);
+      ptx::tma_load_2d(stage_buf + j * kStageBufBytes, map_u, &ab[j], 2 * n0 + 64 * j, r0);
+    }
+  }
+  float d[2][32];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    uint32_t r[32];
+    ptx::tmem_ld_32x32b_x32(tcol + 32 * g, r);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) d[g][i] = __uint_as_float(r[i]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    ptx::mbar_wait(&ab[j], ph[j]);
+    ph[j] ^= 1;
+    const uint32_t srow = ptx::smem_u32(stage_buf + j * kStageBufBytes) + lane * 128;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // 16-byte chunk k: gate features 8k..8k+7, chunk k + 4: their up
+      const uint32_t ag = srow + ((k ^ (lane & 7)) << 4), au = srow + (((k + 4) ^ (lane & 7)) << 4);
+      uint32_t gq[4], uq[4];
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(gq[0]), "=r"(gq[1]), "=r"(gq[2]), "=r"(gq[3]) : "r"(ag));
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(uq[0]), "=r"(uq[1]), "=r"(uq[2]), "=r"(uq[3]) : "r"(au));
+      uint32_t dg[4], du[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float a2[2] = {__uint_as_float(gq[e] << 16), __uint_as_float(gq[e] & 0xffff0000u)};
+        float b2[2] = {__uint_as_float(uq[e] << 16), __uint_as_float(uq[e] & 0xffff0000u)};
+        float oa[2], ob[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float dv = d[j][8 * k + 2 * e + t];
+          const float sg = 1.0f / (1.0f + __expf(-a2[t]));
+          ob[t] = dv * (a2[t] * sg);
+          oa[t] = dv * b2[t] * sg * (1.0f + a2[t] * (1.0f - sg));
+        }
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(dg[e]) : "f"(oa[1]), "f"(oa[0]));
+        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(du[e]) : "f"(ob[1]), "f"(ob[0]));
+      }
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ag), "r"(dg[0]), "r"(dg[1]), "r"(dg[2]), "r"(dg[3]) : "memory");
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(au), "r"(du[0]), "r"(du[1]), "r"(du[2]), "r"(du[3]) : "memory");
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(map_c, stage_buf + j * kStageBufBytes, 2 * n0 + 64 * j, r0);
+      ptx::bulk_commit();
+    }
+  }
+}
+
 template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -527,6 +590,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(q * 32) << 16);
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + cols && ti.n0 + c < sched.N; c += 64) {
+        if (ep.epilogue == kEpiSwiGluBwdBf16) {
+          swiglu_bwd_chunk(tbase + c, ti.n0 + c, mrow0 + q * 32, lane, stage_buf, &auxbar[(warp - 4) * 2], aux_ph,
+                           &map_x, &map_c);
+          continue;
+        }
         if (ep.tma_store) {
           float v[2][32];
 #pragma unroll
@@ -777,6 +845,14 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
   if (tma_store) tma_store = make_store_map(&mc, a.c, a.M, a.N, a.ldc);
   if (a.epilogue == kEpiSwiGluBf16 && !tma_store) return cudaErrorInvalidValue;
+  if (a.epilogue == kEpiSwiGluBwdBf16) {
+    // C and aux are [M, 2N] (row stride ldc); the accumulator (dh) itself is never stored
+    if (a.N % 64 || !a.aux || a.nb1 != 1 || a.nb2 != 1 || a.alpha != 1.0f || a.colsum ||
+        (reinterpret_cast<uintptr_t>(a.c) % 16) || (reinterpret_cast<uintptr_t>(a.aux) % 16) ||
+        !make_store_map(&mc, a.c, a.M, 2 * int64_t(a.N), a.ldc))
+      return cudaErrorInvalidValue;
+    tma_store = true;
+  }
   if (a.epilogue == kEpiRopeBf16 &&
       (!tma_store || !a.rope_tab || a.rope_seq < 1 || (a.rope_dh != 64 && a.rope_dh != 128) || BN % a.rope_dh ||
        a.rope_cols % a.rope_dh || a.alpha != 1.0f || (reinterpret_cast<uintptr_t>(a.rope_tab) % 16)))
@@ -786,6 +862,8 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   // aux tiles share C's layout (ldc): residual / GELU input loaded, pre-activation stored by TMA
   CUtensorMap mx = mc;
   bool aux_tma = false, aux_out_tma = false;
+  if (a.epilogue == kEpiSwiGluBwdBf16 && !make_store_map(&mx, const_cast<void*>(a.aux), a.M, 2 * int64_t(a.N), a.ldc))
+    return cudaErrorInvalidValue;  // u: loaded box by box inside the epilogue (no prefetch)
   if (tma_store && (a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiGeluBwdBf16) && a.aux &&
       (reinterpret_cast<uintptr_t>(a.aux) % 16) == 0)
     aux_tma = make_store_map(&mx, const_cast<void*>(a.aux), a.M, a.N, a.ldc);

@@ -30,6 +30,9 @@ enum GemmEpilogue : int {
                           // aux_out[m, j] (bf16, ld = ldc / 2) = silu(gate_j) * up_j
   kEpiRopeBf16 = 9,       // C(bf16) = acc, columns [0, rope_cols) rotated (rotate-half pairs
                           // (j, j + dh/2) of every head of rope_dh) by position m % rope_seq
+  kEpiSwiGluBwdBf16 = 10, // acc = dh [M, N] (never stored): with aux = u [M, 2N] (gate/up
+                          // interleaved in 32-column blocks, as kEpiSwiGluBf16 wrote it), C [M, 2N]
+                          // (same layout, row stride ldc) = (dgate, dup) of h = silu(gate) * up
 };
 
 enum GemmCausal : int {

@@ -483,6 +483,10 @@ struct Runtime {
   // Llama QKV projection with the rotary embedding of Q and K applied in the GEMM epilogue on the
   // fp32 accumulators (kEpiRopeBf16); the inverse rotation of dQ / dK happens in the head_dim-128
   // attention backward. ZP_ROPE_EPI=0 keeps the separate in-place rope kernels.
+  static bool swiglu_epi() {  // ZP_SWIGLU_EPI=0: separate SwiGLU backward kernel
+    static const bool on = !std::getenv("ZP_SWIGLU_EPI") || std::atoi(std::getenv("ZP_SWIGLU_EPI")) != 0;
+    return on;
+  }
   static bool rope_epi() {
     static const bool on = !std::getenv("ZP_ROPE_EPI") || std::atoi(std::getenv("ZP_ROPE_EPI")) != 0;
     return on;
@@ -909,8 +913,12 @@ struct Runtime {
       z3_clear_group(i + 1);
       // MLP: down projection, SwiGLU, gate/up projection
       wgrad(int(h), int(f), T, A.dx, h, L.g, f, Gd(P.w_down));
-      mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_down), kMNMajor, f, A.dh, f, kEpiStoreBf16);
-      swiglu_bwd(L.u, A.dh, A.du, T, int(f), ctas, st);
+      if (swiglu_epi()) {  // dh = dx W_down never leaves the GEMM: its epilogue writes (dgate, dup)
+        mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_down), kMNMajor, f, A.du, 2 * f, kEpiSwiGluBwdBf16, 1.f, nullptr, L.u);
+      } else {
+        mm(T, f, h, A.dx, kKMajor, h, Wp(P.w_down), kMNMajor, f, A.dh, f, kEpiStoreBf16);
+        swiglu_bwd(L.u, A.dh, A.du, T, int(f), ctas, st);
+      }
       wgrad(int(2 * f), int(h), T, A.du, 2 * f, L.ln2, h, Gd(P.w_gu));
       mm(T, h, 2 * f, A.du, kKMajor, 2 * f, Wp(P.w_gu), kMNMajor, h, A.dln, h, kEpiStoreBf16);
       CK(layernorm_bwd(A.dln, L.x_mid, L.mu2, L.rs2, Wp(P.ln2_g), A.dx, A.dx2, ln_part, &nblk, T, int(h), ctas, st,

@@ -144,6 +144,24 @@ def test_gemm_swiglu_epilogue(cuda, M, f, K):
     assert relerr(H, torch.nn.functional.silu(gate) * up) < 1e-2
 
 
+@pytest.mark.parametrize("M,f,K", [(256, 256, 128), (200, 320, 96), (640, 5504, 512)])
+def test_gemm_swiglu_backward_epilogue(cuda, M, f, K):
+    # dh = A B^T [M, f] stays in the GEMM; with u [M, 2f] (gate/up interleaved in 32-column
+    # blocks) the epilogue writes du [M, 2f] = (dgate, dup) of h = silu(gate) * up
+    A = torch.randn(M, K, device=cuda).to(torch.bfloat16)
+    B = (0.1 * torch.randn(f, K, device=cuda)).to(torch.bfloat16)
+    U = torch.randn(M, 2 * f, device=cuda).to(torch.bfloat16)
+    dU = torch.full((M, 2 * f), float("nan"), device=cuda, dtype=torch.bfloat16)
+    run_gemm(A, 0, B, 0, M, f, K, epilogue=10, c=dU, ldc=2 * f, aux=U)
+    dh = A.float() @ B.float().t()
+    cols = torch.arange(2 * f, device=cuda)
+    gm, um = (cols % 64) < 32, (cols % 64) >= 32
+    g, u = U.float()[:, gm], U.float()[:, um]
+    sg = torch.sigmoid(g)
+    assert relerr(dU[:, um], dh * g * sg) < 1e-2
+    assert relerr(dU[:, gm], dh * u * sg * (1 + g * (1 - sg))) < 1e-2
+
+
 def test_gemm_attention_batched_heads(cuda):
     # S[z=(head, sample)] = Q_h K_h^T read in place from a fused [b*s, 3h] QKV activation.
     b, s, H, d = 2, 256, 4, 64
