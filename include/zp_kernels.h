@@ -109,6 +109,13 @@ int zp_peer_rs_adam_ag(zp_peer_group* g, int64_t src_off, int32_t src_f32, int64
 int zp_peer_all_gather(zp_peer_group* g, int64_t shard_src_off, int64_t dst_off, int64_t len, uint32_t epoch,
                        int32_t ctas, void* stream);
 
+/* On-device synthetic token rows (the loader's synthetic data, zp_runtime_load_tokens with
+ * from_host = 0): out[i * seq_plus1 + t] for samples j = first + i, i < count, is a fixed function
+ * of (seed, iteration, j, t): splitmix64 finaliser chain, modulo vocab. A sample's row does not
+ * depend on which rank or slice loads it. out: device int32 [count * seq_plus1]. */
+int zp_synth_tokens(int32_t* out, int64_t first, int64_t count, int32_t seq_plus1, int32_t vocab, uint64_t seed,
+                    uint64_t iteration, void* stream);
+
 /* Number of kernels launched by this library since load (all entry points). */
 int64_t zp_launch_count(void);
 

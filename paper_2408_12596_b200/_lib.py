@@ -67,3 +67,6 @@ lib.zp_attention_bwd_hd.restype = C.c_int
 lib.zp_norm_bwd.argtypes = [C.c_void_p] * 8 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                             C.c_int32, C.c_int32, C.c_void_p]
 lib.zp_norm_bwd.restype = C.c_int
+lib.zp_synth_tokens.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_uint64, C.c_uint64,
+                                C.c_void_p]
+lib.zp_synth_tokens.restype = C.c_int

@@ -27,6 +27,16 @@ extern "C" int zp_gemm(const zp_gemm_desc* d, void* stream) {
 
 extern "C" int64_t zp_launch_count(void) { return zp::launch_count(); }
 
+extern "C" int zp_synth_tokens(int32_t* out, int64_t first, int64_t count, int32_t seq_plus1, int32_t vocab,
+                               uint64_t seed, uint64_t iteration, void* stream) {
+  if (!out || first < 0 || count < 1 || seq_plus1 < 2 || vocab < 1) return 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  zp::synth_tokens(out, first, count, seq_plus1, vocab, seed, iteration, sms, static_cast<cudaStream_t>(stream));
+  return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
 extern "C" int zp_attention_fwd(const void* qkv, void* out, float* lse, int64_t batch, int32_t seq,
                                 int32_t heads, int32_t max_ctas, void* stream) {
   const cudaError_t e = zp::attention_fwd(static_cast<const zp::bf16*>(qkv), static_cast<zp::bf16*>(out), lse,
