@@ -1757,7 +1757,7 @@ cudaError_t attention_fwd(const bf16* qkv, bf16* out, float* lse, int64_t batch,
 
 cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
                                float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
-                               const float2* rope_tab) {
+                               const float2* rope_tab, bool dvec_ready) {
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_d128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1769,10 +1769,12 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
   CUtensorMap mq, md;
   if (!map_rows(&mq, qkv, T, 3 * h) || !map_rows(&md, dout, T, h)) return cudaErrorInvalidValue;
   const int cap = ctas > 0 ? std::min(ctas, device_sms()) : device_sms();
-  attn_dvec_kernel<128><<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
-  note_launch();
-  cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
-  if (e != cudaSuccess) return e;
+  if (!dvec_ready) {  // else the producer of dout (its GEMM epilogue) wrote D and cleared dq32
+    attn_dvec_kernel<128><<<std::min<int64_t>(cap * 8, (T + 7) / 8), 256, 0, s>>>(dout, out, dvec, T, seq, heads);
+    note_launch();
+    cudaError_t e = cudaMemsetAsync(dq32, 0, size_t(T) * h * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   const int nz = int(batch) * heads;
   const int ntasks = (seq / kT) * nz;
   const float scale = 1.0f / std::sqrt(float(kD2));
@@ -1792,11 +1794,12 @@ cudaError_t attention_bwd_d128(const bf16* qkv, const bf16* out, const bf16* dou
 
 cudaError_t attention_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse, float* dvec,
                           float* dq32, bf16* dqkv, int64_t batch, int seq, int heads, int ctas, cudaStream_t s,
-                          int head_dim, const float2* rope_tab) {
+                          int head_dim, const float2* rope_tab, bool dvec_ready) {
   if (seq % kT || batch < 1 || (head_dim != 64 && head_dim != 128)) return cudaErrorInvalidValue;
   if (head_dim == 128)
-    return attention_bwd_d128(qkv, out, dout, lse, dvec, dq32, dqkv, batch, seq, heads, ctas, s, rope_tab);
-  if (rope_tab) return cudaErrorInvalidValue;  // head_dim 64: the caller applies the inverse rotation
+    return attention_bwd_d128(qkv, out, dout, lse, dvec, dq32, dqkv, batch, seq, heads, ctas, s, rope_tab,
+                              dvec_ready);
+  if (rope_tab || dvec_ready) return cudaErrorInvalidValue;  // head_dim 64: caller-side rotation and D
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -104,6 +104,9 @@ struct EpiParams {
   float* colsum;    // += column sums of the bf16-path output over the rows (fp32 [N]); may be null
   const float2* rope_tab;  // kEpiRopeBf16: (cos, sin) [rope_seq][rope_dh / 2]
   int rope_seq, rope_dh, rope_cols;
+  float* dvec;             // kEpiDvecBf16
+  float* zero32;
+  int dvec_seq;
 };
 
 // Column sums of one warp's 32 rows x 64 columns (v[g][i]: row = lane, column = 32g + i) added
@@ -563,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stage_buf = smem_epi + (warp - 4) * 2 * kStageBufBytes;
     int buf = 0;
     uint32_t aux_ph[2] = {0, 0};  // phases of this warp's two aux-load barriers
+    float dacc = 0.f;             // kEpiDvecBf16: this row's dO . O over the current head
     int local = 0;
     const uint32_t tempty_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0;
     for (int t = unit0; t < sched.total; t += units) {
@@ -629,6 +633,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (ep.epilogue == kEpiGeluBwdBf16) {  // aux = gelu'(u)
                   w[2 * k] *= a0;
                   w[2 * k + 1] *= a1;
+                } else if (ep.epilogue == kEpiDvecBf16) {  // aux = O: D += bf16(dO) * O
+                  uint32_t pk;
+                  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(w[2 * k + 1]), "f"(w[2 * k]));
+                  dacc = fmaf(__uint_as_float(pk << 16), a0, dacc);
+                  dacc = fmaf(__uint_as_float(pk & 0xffff0000u), a1, dacc);
                 } else {  // residual
                   w[2 * k] += a0;
                   w[2 * k + 1] += a1;
@@ -636,6 +645,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             __syncwarp();  // every lane has read the aux box before it is overwritten
+            if (ep.epilogue == kEpiDvecBf16) {
+              // this warp's column half is one head (128 columns): D after its second chunk; the
+              // chunk's fp32 dQ workspace is cleared for the attention backward's reductions
+              if (valid) {
+                float4* zr = reinterpret_cast<float4*>(ep.zero32 + int64_t(row) * ep.ldc + n0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) zr[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+              if (c == c_begin + 64) {
+                if (valid) {
+                  const int heads = sched.N >> 7, head = n0 >> 7;
+                  const int smp = row / ep.dvec_seq, qi = row - smp * ep.dvec_seq;
+                  ep.dvec[(int64_t(smp) * heads + head) * ep.dvec_seq + qi] = dacc;
+                }
+                dacc = 0.f;
+              }
+            }
             if (ep.epilogue == kEpiBiasResidBf16 && ep.bias) {
 #pragma unroll
               for (int g = 0; g < 2; ++g) epi_bias(ep, v[g], n0 + 32 * g, sched.N, valid);
@@ -839,7 +865,8 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   // bf16 outputs of plain (unbatched) GEMMs go through TMA stores.
   const bool bf16_out = a.epilogue == kEpiStoreBf16 || a.epilogue == kEpiBiasBf16 ||
                         a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiBiasGeluBf16 ||
-                        a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiSwiGluBf16 || a.epilogue == kEpiRopeBf16;
+                        a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiSwiGluBf16 || a.epilogue == kEpiRopeBf16 ||
+                        a.epilogue == kEpiDvecBf16;
   if (a.epilogue == kEpiSwiGluBf16 && (a.N % 64 || !a.aux_out || a.nb1 != 1 || a.nb2 != 1))
     return cudaErrorInvalidValue;
   bool tma_store = bf16_out && a.nb1 == 1 && a.nb2 == 1 && (reinterpret_cast<uintptr_t>(a.c) % 16) == 0;
@@ -864,9 +891,13 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   bool aux_tma = false, aux_out_tma = false;
   if (a.epilogue == kEpiSwiGluBwdBf16 && !make_store_map(&mx, const_cast<void*>(a.aux), a.M, 2 * int64_t(a.N), a.ldc))
     return cudaErrorInvalidValue;  // u: loaded box by box inside the epilogue (no prefetch)
-  if (tma_store && (a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiGeluBwdBf16) && a.aux &&
-      (reinterpret_cast<uintptr_t>(a.aux) % 16) == 0)
+  if (tma_store && (a.epilogue == kEpiBiasResidBf16 || a.epilogue == kEpiGeluBwdBf16 || a.epilogue == kEpiDvecBf16) &&
+      a.aux && (reinterpret_cast<uintptr_t>(a.aux) % 16) == 0)
     aux_tma = make_store_map(&mx, const_cast<void*>(a.aux), a.M, a.N, a.ldc);
+  if (a.epilogue == kEpiDvecBf16 &&
+      (!aux_tma || BN != 256 || a.N % 256 || !a.dvec || !a.zero32 || a.dvec_seq < 1 || a.alpha != 1.0f ||
+       a.colsum || (reinterpret_cast<uintptr_t>(a.zero32) % 16)))
+    return cudaErrorInvalidValue;
   if (tma_store && a.epilogue == kEpiBiasGeluBf16 && a.aux_out && (reinterpret_cast<uintptr_t>(a.aux_out) % 16) == 0)
     aux_out_tma = make_store_map(&mx, a.aux_out, a.M, a.N, a.ldc);
   Sched s;
@@ -921,6 +952,9 @@ cudaError_t launch(const GemmArgs& a, cudaStream_t stream) {
   ep.rope_seq = a.rope_seq;
   ep.rope_dh = a.rope_dh;
   ep.rope_cols = a.rope_cols;
+  ep.dvec = a.dvec;
+  ep.zero32 = a.zero32;
+  ep.dvec_seq = a.dvec_seq;
   int units = workers;
   if (s.total < units) units = s.total;
   if (units < 1) return cudaSuccess;

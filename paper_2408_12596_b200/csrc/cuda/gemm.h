@@ -33,6 +33,9 @@ enum GemmEpilogue : int {
   kEpiSwiGluBwdBf16 = 10, // acc = dh [M, N] (never stored): with aux = u [M, 2N] (gate/up
                           // interleaved in 32-column blocks, as kEpiSwiGluBf16 wrote it), C [M, 2N]
                           // (same layout, row stride ldc) = (dgate, dup) of h = silu(gate) * up
+  kEpiDvecBf16 = 11,      // C(bf16) = acc (dO of attention); with aux = O (same layout, heads of
+                          // 128 columns): dvec[(m / dvec_seq * heads + head) * dvec_seq + m % dvec_seq]
+                          // = sum over the head of bf16(C) * O; zero32 (fp32, [M, N], ld ldc) zeroed
 };
 
 enum GemmCausal : int {
@@ -67,6 +70,10 @@ struct GemmArgs {
   // kEpiRopeBf16: (cos, sin) table float2 [rope_seq][rope_dh / 2] (kernels.h rope_table)
   const void* rope_tab = nullptr;
   int rope_seq = 0, rope_dh = 0, rope_cols = 0;
+  // kEpiDvecBf16: the attention backward's D vector and its fp32 dQ workspace to clear
+  float* dvec = nullptr;
+  float* zero32 = nullptr;
+  int dvec_seq = 0;
 };
 
 // Returns cudaSuccess or the launch/encode error.

@@ -483,6 +483,10 @@ struct Runtime {
   // Llama QKV projection with the rotary embedding of Q and K applied in the GEMM epilogue on the
   // fp32 accumulators (kEpiRopeBf16); the inverse rotation of dQ / dK happens in the head_dim-128
   // attention backward. ZP_ROPE_EPI=0 keeps the separate in-place rope kernels.
+  static bool dvec_epi_on() {  // ZP_DVEC_EPI=0: separate D-vector kernel + dQ workspace memset
+    static const bool on = !std::getenv("ZP_DVEC_EPI") || std::atoi(std::getenv("ZP_DVEC_EPI")) != 0;
+    return on;
+  }
   static bool swiglu_epi() {  // ZP_SWIGLU_EPI=0: separate SwiGLU backward kernel
     static const bool on = !std::getenv("ZP_SWIGLU_EPI") || std::atoi(std::getenv("ZP_SWIGLU_EPI")) != 0;
     return on;
@@ -926,10 +930,27 @@ struct Runtime {
       grad_partials(ln_part, nblk, int(h), Gd(P.ln2_g));
       // attention
       wgrad(int(h), int(h), T, A.dx2, h, L.attn, h, Gd(P.w_o));
-      mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
+      // dO = dx2 W_o; at head_dim 128 its epilogue also forms the attention backward's D vector
+      // (rowsum(dO * O) per head) and clears the fp32 dQ workspace
+      const bool dvec_epi = hd() == 128 && dvec_epi_on() && (h % 256) == 0;
+      if (dvec_epi) {
+        GemmArgs g;
+        g.M = int(T); g.N = int(h); g.K = int(h);
+        g.a.ptr = A.dx2; g.a.major = kKMajor; g.a.ld = h;
+        g.b.ptr = Wp(P.w_o); g.b.major = kMNMajor; g.b.ld = h;
+        g.c = A.dO; g.ldc = h;
+        g.epilogue = kEpiDvecBf16;
+        g.aux = L.attn;
+        g.dvec = A.dvec; g.zero32 = A.dq32; g.dvec_seq = int(s);
+        g.max_ctas = ctas;
+        launch_gemm(g, 2.0 * double(T) * h * h);
+      } else {
+        mm(T, h, h, A.dx2, kKMajor, h, Wp(P.w_o), kMNMajor, h, A.dO, h, kEpiStoreBf16);
+      }
       {  // dQ, dK back to pre-rotation Q, K: inside the attention backward at head_dim 128
         const float2* tab = hd() == 128 && rope_epi() ? rope_table(int(s), hd(), 10000.f, st) : nullptr;
-        CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd(), tab));
+        CK(attention_bwd(L.qkv, L.attn, A.dO, L.lse, A.dvec, A.dq32, A.dqkv, b, int(s), int(H), ctas, st, hd(), tab,
+                         dvec_epi));
         if (!tab) rope(A.dqkv, T, int(s), int(h), 10000.f, true, ctas, st, hd());
       }
       wgrad(int(3 * h), int(h), T, A.dqkv, 3 * h, L.ln1, h, Gd(P.w_qkv));
