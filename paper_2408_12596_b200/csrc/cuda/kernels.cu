@@ -986,6 +986,33 @@ __global__ void add_f32_k(float* dst, const float* src, int64_t n) {
     dst[i] += src[i];
 }
 
+// acc[i] = (first ? 0 : acc[i]) + sum over j = 0..n-1, in rank order, of bf16 src_j[i]: the local
+// half of the copy-engine ZeRO-3 reduce-scatter (the same fixed-order fp32 sum as peer_rs_acc_k).
+struct SliceSrcs {
+  const bf16* p[8];
+};
+__global__ void reduce_slices_k(float* __restrict__ acc, SliceSrcs src, int n, int64_t len, bool first) {
+  const int64_t n8 = len / 8;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    float a[8];
+    if (first) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = 0.f;
+    } else {
+      const float4 x = reinterpret_cast<const float4*>(acc)[2 * i], y = reinterpret_cast<const float4*>(acc)[2 * i + 1];
+      a[0] = x.x; a[1] = x.y; a[2] = x.z; a[3] = x.w; a[4] = y.x; a[5] = y.y; a[6] = y.z; a[7] = y.w;
+    }
+    for (int j = 0; j < n; ++j) {
+      float v[8];
+      unpack8(reinterpret_cast<const uint4*>(src.p[j])[i], v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += v[k];
+    }
+    reinterpret_cast<float4*>(acc)[2 * i] = make_float4(a[0], a[1], a[2], a[3]);
+    reinterpret_cast<float4*>(acc)[2 * i + 1] = make_float4(a[4], a[5], a[6], a[7]);
+  }
+}
+
 __global__ void accumulate_k(float* acc, const bf16* src, int64_t n, bool overwrite) {
   const int64_t n4 = n / 4;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4;
@@ -1371,6 +1398,11 @@ void cast_f32_bf16(const float* in, bf16* out, int64_t n, int ctas, cudaStream_t
 }
 void reduce_sum_f32(const float* x, int64_t n, float* out, cudaStream_t s) {
   reduce_sum_k<<<1, kThreads, 0, s>>>(x, n, out); note_launch();
+}
+void reduce_slices(float* acc, const bf16* const* srcs, int n, int64_t len, bool first, int ctas, cudaStream_t s) {
+  SliceSrcs ss{};
+  for (int j = 0; j < n && j < 8; ++j) ss.p[j] = srcs[j];
+  reduce_slices_k<<<grid_for(len / 8, kThreads, ctas), kThreads, 0, s>>>(acc, ss, n, len, first); note_launch();
 }
 void add_f32(float* dst, const float* src, int64_t n, int ctas, cudaStream_t s) {
   add_f32_k<<<grid_for(n, kThreads, ctas), kThreads, 0, s>>>(dst, src, n); note_launch();

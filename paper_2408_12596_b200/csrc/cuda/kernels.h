@@ -83,5 +83,7 @@ void adam_update(float* p32, float* m, float* v, bf16* p16, const float* acc, co
 void reduce_sum_f32(const float* x, int64_t n, float* out, cudaStream_t s);
 // dst += src (fp32)
 void add_f32(float* dst, const float* src, int64_t n, int ctas, cudaStream_t s);
+// acc = (first ? 0 : acc) + sum_j srcs[j] (bf16, j in order, n <= 8; len a multiple of 8)
+void reduce_slices(float* acc, const bf16* const* srcs, int n, int64_t len, bool first, int ctas, cudaStream_t s);
 
 }  // namespace zp

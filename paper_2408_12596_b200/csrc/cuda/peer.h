@@ -26,6 +26,10 @@ struct PeerFlags {       // one per rank, IPC-mapped by every peer
   uint32_t done[kMaxPeers];
   uint32_t ctr;          // local CTA arrival counter of the exit barrier (wraps per launch)
   uint32_t pad[15];
+  // ZeRO-3 copy-engine reduce-scatter (runtime.cu z3_reduce_async), written by stream memory
+  // operations of the peers into this rank's block, waited on locally:
+  uint32_t rs_ready[kMaxPeers][2];   // [peer][buffer]: peer's group gradient in that buffer is final
+  uint32_t rs_pulled[kMaxPeers][2];  // [peer][buffer]: peer has copied its slice out of ours
 };
 
 struct PeerView {

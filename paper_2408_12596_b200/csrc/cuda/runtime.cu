@@ -628,6 +628,16 @@ struct Runtime {
         gb_layer[0] = B16(lay.max_layer_group, "layer gather buffer 0");
         gb_layer[1] = B16(lay.max_layer_group, "layer gather buffer 1");
         ggrp = B16(lay.max_group, "group gradient");
+        ggrp_buf[0] = ggrp;
+        ggrp_buf[1] = rs_stage[0] = rs_stage[1] = nullptr;
+        z3_async = z3_async_ok();
+        if (z3_async) {
+          ggrp_buf[1] = B16(lay.max_group, "group gradient 1");
+          rs_stage[0] = B16(lay.max_group, "reduce-scatter staging 0");
+          rs_stage[1] = B16(lay.max_group, "reduce-scatter staging 1");
+        }
+        z3_cur = 0;
+        pend_g = -1;
       }
     }
     p32 = F32(SL, "master params");
@@ -654,6 +664,7 @@ struct Runtime {
     resident_mark = arena.used;
     if (g16) CK(cudaMemsetAsync(g16, 0, size_t(T) * 2, st));
     if (ggrp) CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
+    if (ggrp_buf[1]) CK(cudaMemsetAsync(ggrp_buf[1], 0, size_t(lay.max_group) * 2, st));
     if (r16) CK(cudaMemsetAsync(r16, 0, size_t(S) * 2, st));
     CK(cudaMemsetAsync(m32, 0, size_t(SL) * 4, st));
     CK(cudaMemsetAsync(v32, 0, size_t(SL) * 4, st));
@@ -798,10 +809,106 @@ struct Runtime {
       buf_pending[nb] = true;
     }
   }
+  // ---- ZeRO-3 reduce-scatter on the copy engines (ZP_Z3_ASYNC_RS=1, NVLink ranks in separate
+  // processes). The group gradient alternates between two buffers. When a group's gradient is
+  // final, stream memory operations tell every peer so (rs_ready). Each rank's side stream `rst`
+  // waits for those flags and pulls its slice of every peer's buffer with cudaMemcpyAsync, which
+  // needs no SMs and overlaps the next layer's backward. It then tells the peers it is done
+  // (rs_pulled). One group later, a short HBM-bound kernel adds the pulled slices and the rank's
+  // own slice into the fp32 shard accumulator, in rank order. A buffer is rewritten only after
+  // every peer has pulled from it.
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  WaitFn mem_wait = nullptr;
+  WriteFn mem_write = nullptr;
+  bool z3_async = false;
+  bf16* ggrp_buf[2] = {};
+  bf16* rs_stage[2] = {};
+  int z3_cur = 0;                  // buffer the gradient producers write into (ggrp)
+  uint32_t rs_ep = 0;              // reduce-scatters issued (same sequence on every rank)
+  uint32_t last_ep[2] = {0, 0};    // rs_ep of each buffer's latest use
+  int pend_g = -1, pend_b = 0;     // group whose local sum is still to be added
+  bool pend_first = false;
+  bool z3_idle = false;            // inside z3_idle_step: fresh buffers must be zero
+  cudaStream_t rst = nullptr;
+  cudaEvent_t ev_pull[2] = {};
+  bool z3_async_ok() {
+    const char* e = std::getenv("ZP_Z3_ASYNC_RS");
+    if (!e || e[0] != '1' || !peer || kernel_gathers || n > 8) return false;
+    if (!mem_wait) {
+      mem_wait = driver_fn<WaitFn>("cuStreamWaitValue32");
+      mem_write = driver_fn<WriteFn>("cuStreamWriteValue32");
+    }
+    if (!mem_wait || !mem_write) return false;
+    if (!rst) {
+      CK(cudaStreamCreateWithFlags(&rst, cudaStreamNonBlocking));
+      for (auto& ev : ev_pull) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    return true;
+  }
+  void mem_op(bool wait, cudaStream_t s, const uint32_t* addr, uint32_t v) {
+    const CUresult r = wait ? mem_wait(s, CUdeviceptr(addr), v, 0 /*CU_STREAM_WAIT_VALUE_GEQ*/)
+                            : mem_write(s, CUdeviceptr(addr), v, 0 /*CU_STREAM_WRITE_VALUE_DEFAULT*/);
+    if (r != CUDA_SUCCESS) fail(ZP_ECUDA, "stream memory operation failed");
+  }
+  void z3_local_sum() {  // the pending group's fp32 shard += its n slices, rank order
+    if (pend_g < 0) return;
+    const Group& G = lay.groups[pend_g];
+    const int64_t part = G.len / n;
+    CK(cudaStreamWaitEvent(st, ev_pull[pend_b], 0));
+    const bf16* srcs[8];
+    for (int j = 0; j < n; ++j)
+      srcs[j] = j == rank ? ggrp_buf[pend_b] + part * rank : rs_stage[pend_b] + part * j;
+    reduce_slices(acc + shoff[pend_g], srcs, n, part, pend_first, ctas, st);
+    pend_g = -1;
+  }
+  void z3_flush() {
+    if (z3_async) z3_local_sum();
+  }
+  void z3_reduce_async(int g) {
+    const Group& G = lay.groups[g];
+    const int64_t part = G.len / n;
+    const int b = z3_cur;
+    z3_local_sum();  // the previous group's pulls ran during this group's backward
+    const uint32_t ep = ++rs_ep;
+    for (int k = 1; k < n; ++k) {  // this buffer's gradient is final: tell every peer
+      const int j = (rank + k) % n;
+      mem_op(false, st, &pv.flags[j]->rs_ready[rank][b], ep);
+    }
+    for (int k = 1; k < n; ++k) {  // pull my slice of every peer's buffer (copy engines)
+      const int j = (rank + k) % n;
+      mem_op(true, rst, &pv.flags[rank]->rs_ready[j][b], ep);
+      CK(cudaMemcpyAsync(rs_stage[b] + part * j, pv.base[j] + off(ggrp_buf[b] + part * rank), size_t(part) * 2,
+                         cudaMemcpyDeviceToDevice, rst));
+    }
+    for (int k = 1; k < n; ++k) {
+      const int j = (rank + k) % n;
+      mem_op(false, rst, &pv.flags[j]->rs_pulled[rank][b], ep);
+    }
+    CK(cudaEventRecord(ev_pull[b], rst));
+    last_ep[b] = ep;
+    pend_g = g;
+    pend_b = b;
+    pend_first = z3_first;
+    // switch buffers; the other one is rewritten only after every peer has pulled its last use
+    z3_cur ^= 1;
+    ggrp = ggrp_buf[z3_cur];
+    if (last_ep[z3_cur]) {
+      // my own slice of that buffer feeds the local sum: it was added above (z3_local_sum ran
+      // before this group's flags), so only the peers' pulls gate the rewrite
+      for (int k = 1; k < n; ++k) mem_op(true, st, &pv.flags[rank]->rs_pulled[(rank + k) % n][z3_cur], last_ep[z3_cur]);
+    }
+    if (z3_idle) CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
+  }
   void z3_reduce(int g) {
     if (stage != 3 || n == 1) return;
     const Group& G = lay.groups[g];
     const int s0 = tm.mark(st);
+    if (z3_async) {
+      z3_reduce_async(g);
+      tm.close(kRs, s0, st);
+      return;
+    }
     if (peer)  // pull-reduce straight into the fp32 shard accumulator (no bf16 round trip)
       CK(peer_rs_accumulate(pv, off(ggrp), (G.len / n) * rank, acc + shoff[g], G.len / n, z3_first, ++epoch,
                             ctas, st));
@@ -822,6 +929,7 @@ struct Runtime {
     if (n == 1) return;  // one rank: nothing to join, its gradients live in the accumulator
     const int G = int(lay.groups.size());
     CK(cudaMemsetAsync(ggrp, 0, size_t(lay.max_group) * 2, st));
+    z3_idle = true;
     for (int g = 0; g < G; ++g) z3_gather(g, kAgF);
     z3_reduce(G - 1);
     for (int g = G - 2; g >= 1; --g) {
@@ -829,6 +937,8 @@ struct Runtime {
       z3_reduce(g);
     }
     z3_reduce(0);
+    z3_idle = false;
+    z3_flush();
   }
 
   // ---------------------------------------------------------------- forward / backward
@@ -965,6 +1075,7 @@ struct Runtime {
     embed_bwd(tok, int(s), A.dx, dwte32, nullptr, T, int(h), ctas, st);
     grad_from_f32(dwte32, int64_t(vocab_pad) * h, Gd(lay.wte));
     z3_reduce(0);
+    z3_flush();
   }
 
   void backward(Acts& A, const int32_t* tok) {
@@ -1027,6 +1138,7 @@ struct Runtime {
     grad_from_f32(dwte32, int64_t(vocab_pad) * h, Gd(lay.wte));
     grad_from_f32(dwpe32, int64_t(c.seq_len) * h, Gd(lay.wpe));
     z3_reduce(0);
+    z3_flush();
   }
 
   // ---------------------------------------------------------------- collectives
