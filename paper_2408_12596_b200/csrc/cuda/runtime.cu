@@ -1770,6 +1770,12 @@ int zp_runtime_destroy(zp_runtime* h) {
   for (auto& e : R.marks)
     if (e) cudaEventDestroy(e);
   if (R.cst) cudaStreamSynchronize(R.cst);
+  if (R.rst) {
+    cudaStreamSynchronize(R.rst);
+    cudaStreamDestroy(R.rst);
+  }
+  for (auto e : R.ev_pull)
+    if (e) cudaEventDestroy(e);
   if (R.arena.base) cudaFree(R.arena.base);
   if (R.st) cudaStreamDestroy(R.st);
   zp::destroy_green(&R.green);
