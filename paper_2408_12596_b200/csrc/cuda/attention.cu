@@ -1117,13 +1117,20 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         if (raise) m = mx;
         uint32_t pk[32];
         float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // two halves: the first half's P store (S columns already in registers; P.V(j-1) is complete)
+        // overlaps the second half's exponentials
 #pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          const float x0 = fmaf(sv[i], scale_log2, -m), x1 = fmaf(sv[i + 1], scale_log2, -m);
-          const bool poly = ((i >> 1) & 3) < POLY;
-          const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
-          ps[(i >> 1) & 7] += p0 + p1;
-          pk[i >> 1] = pack_bf16(p0, p1);
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int i = 32 * hh; i < 32 * hh + 32; i += 2) {
+            const float x0 = fmaf(sv[i], scale_log2, -m), x1 = fmaf(sv[i + 1], scale_log2, -m);
+            const bool poly = ((i >> 1) & 3) < POLY;
+            const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
+            ps[(i >> 1) & 7] += p0 + p1;
+            pk[i >> 1] = pack_bf16(p0, p1);
+          }
+          uint32_t (&half)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pk[16 * hh]);
+          ptx::tmem_st_32x32b_x16(t_p + 16 * hh, half);
         }
         ATRF(6 + 4 * g, j, tr);
         // O += P.V of the previous tile is complete (it precedes this tile's S in the tensor pipe)
@@ -1139,7 +1146,6 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           }
         }
         l = l * alpha + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
-        ptx::tmem_st_32x32b_x32(t_p, pk);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ATRF(7 + 4 * g, j, tr);
