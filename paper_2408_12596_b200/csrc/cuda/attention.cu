@@ -1421,8 +1421,11 @@ __global__ void __launch_bounds__(kB2Threads, 1)
             pk[c * 16 + e / 2] = pack_bf16(p[0], p[1]);
             pk[c * 16 + e / 2 + 1] = pack_bf16(p[2], p[3]);
           }
+          // P^T over this half's S^T, chunk by chunk: chunk c's 16 packed columns land on S^T columns
+          // already read (chunk 1's scores sit in columns 32..63), so the store overlaps the next load
+          ptx::tmem_st_32x32b_x16(tmem + kB2TS + lane_off + qh * 64 + c * 16,
+                                  *reinterpret_cast<const uint32_t(*)[16]>(&pk[c * 16]));
         }
-        ptx::tmem_st_32x32b_x32(tmem + kB2TS + lane_off + qh * 64, pk);  // P^T over this half's S^T
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         if (warp == 0 && lane == 0) ATR(6, it);
@@ -1447,8 +1450,9 @@ __global__ void __launch_bounds__(kB2Threads, 1)
             dk[c * 16 + e / 2 + 1] = pack_bf16(__uint_as_float(pb << 16) * (__uint_as_float(vp[e + 2]) - d4.z),
                                                __uint_as_float(pb & 0xffff0000u) * (__uint_as_float(vp[e + 3]) - d4.w));
           }
+          ptx::tmem_st_32x32b_x16(tmem + kB2TDP + lane_off + qh * 64 + c * 16,
+                                  *reinterpret_cast<const uint32_t(*)[16]>(&dk[c * 16]));
         }
-        ptx::tmem_st_32x32b_x32(tmem + kB2TDP + lane_off + qh * 64, dk);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         if (warp == 0 && lane == 0) ATR(8, it);
