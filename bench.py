@@ -61,8 +61,12 @@ CONFIGS = {
     # tier (3 samples) pinned every lockstep ZeRO-3 micro-step to 3 samples on the fast ranks, so
     # the 104-SM tier could only take 2 and idled 24 % by the planner's own prediction
     # (profiles/r2_bench_lines/g15_c5_n4.json, g20_c5_n4.json)
+    # "full Poplar search over global batch" (BASELINE.json): Alg. 2 is evaluated on the measured
+    # profile at every global batch of 24..40 samples per GPU; the run uses the batch with the best
+    # predicted samples/s (the smallest within 0.5 % of it, so one GPU keeps short iterations)
     "c5": dict(model="llama-7b", stage=3, tiers=[148, 104, 74, 148, 104, 74, 148, 74], caps=[0, 0, 0, 128],
-               gbs_per_gpu=32, label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/128 GB"),
+               gbs_per_gpu=32, gbs_search=(24, 40, 2),
+               label="C5: Llama-style 7B s4096, ZeRO-3 bf16, mixed SM tiers 148/104/74 + HBM caps 180/128 GB"),
 }
 DEFAULT_CONFIG = "c5"
 
@@ -259,13 +263,27 @@ def plan_parity(rt, profiles, gbs, stage, world, link):
     ref = oracle.reference()
     out = {"checked": 0, "identical": True, "diffs": []}
     for name, prof, plan, lk in profiles:
-        theirs = poplar.poplar_plan(rt, prof, gbs, stage, world, link=lk, api=ref)
+        theirs = poplar.poplar_plan(rt, prof, plan["gbs"], stage, world, link=lk, api=ref)
         d = plans_equal(plan, theirs)
         out["checked"] += 1
         if d:
             out["identical"] = False
             out["diffs"].append({name: d})
     return out
+
+
+def search_gbs(rt, profile, stage, world, link, per_gpu):
+    """Poplar's planner (Alg. 2, the product planner) evaluated over candidate global batches on
+    the measured profile: the batch with the best predicted samples/s, the smallest within 0.5 %
+    of the best. Deterministic in its inputs, so every rank picks the same batch."""
+    from paper_2408_12596_b200 import poplar
+    lo, hi, step = per_gpu
+    table = []
+    for g in range(lo * world, hi * world + 1, step * world):
+        p = poplar.poplar_plan(rt, profile, g, stage, world, link=link)
+        table.append((g, g / p["predicted_wall_time"]))
+    best = max(t for _, t in table)
+    return min(g for g, t in table if t >= 0.995 * best), table
 
 
 def reference_prediction(rt, profile, probes, link, gbs, stage, world):
@@ -388,8 +406,11 @@ def main():
     profile = rt.profile(stage)
     t_profile = time.perf_counter() - t0
     stage = profile["effective_stage"]
+    search = cfg.get("gbs_search") if not args.gbs else None
+    search_table = None
+    if search:
+        gbs, search_table = search_gbs(rt, profile, stage, world, link, search)
     plan = poplar.poplar_plan(rt, profile, gbs, stage, world, link=link)
-    uniform = poplar.poplar_plan(rt, profile, gbs, stage, world, uniform=True, link=link)
     first, count = poplar.rank_slice(plan, rank)
     rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
     plan_initial, profile_initial = plan, profile
@@ -417,6 +438,8 @@ def main():
                 # optimizer tail, so it leaves the comm floor
                 floor -= max(d["optimizer_time"] for d in profile["devices"])
             link = poplar.recalibrate_link(link, stage, plan["gas"], floor, rt.param_count)
+            if search:
+                gbs, search_table = search_gbs(rt, profile, stage, world, link, search)
             plan = poplar.poplar_plan(rt, profile, gbs, stage, world, link=link)
             first, count = poplar.rank_slice(plan, rank)
             rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
@@ -438,6 +461,8 @@ def main():
         barrier()
         return max(allgather(local_t)), tm.to_py()
 
+    # heterogeneity-blind baseline at the same (final) global batch, from the Alg. 1 profile
+    uniform = poplar.poplar_plan(rt, profile_initial, gbs, stage, world, uniform=True, link=link)
     rt.execute_iteration(plan, stage)  # the final plan once more before the timed region
     launches0 = _lib.lib.zp_launch_count()
     with ClockSampler(local) as clk:
@@ -568,6 +593,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": cfg["label"], "model": cfg["model"], "params": rt.param_count,
                        "seq_len": model.seq_len, "head_dim": model.head_dim, "global_batch": gbs,
+                       "gbs_search": ({"per_gpu_range": list(search), "chosen": gbs,
+                                       "predicted_samples_per_s": {str(g): t for g, t in search_table}}
+                                      if search_table else None),
                        "stage": stage,
                        "sm_budgets": [cfg["tiers"][r % len(cfg["tiers"])] for r in range(world)],
                        "hbm_caps_gib": [cfg["caps"][r % len(cfg["caps"])] or "full" for r in range(world)],
