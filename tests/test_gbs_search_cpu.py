@@ -1,0 +1,44 @@
+"""bench.py's Poplar search over the global batch (C5, BASELINE.json "full Poplar search over
+global batch"): Alg. 2 (the product planner, bit-exact with the reference) evaluated at every
+candidate batch on a profile; the chosen batch is the smallest within 0.5 % of the best predicted
+samples/s, and the choice is deterministic in its inputs (every rank must pick the same batch)."""
+import os
+import sys
+from types import SimpleNamespace
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def _profile(fits, mbs):
+    return {"effective_stage": 3,
+            "devices": [{"device_id": i, "mbs": m, "probes_used": m, "optimizer_time": 0.01,
+                         "samples": [(b, c0 + c1 * b) for b in range(1, m + 1)]}
+                        for i, ((c0, c1), m) in enumerate(zip(fits, mbs))]}
+
+
+def _rt():
+    return SimpleNamespace(model=SimpleNamespace(d_model=4096, n_layer=32), param_count=6738415616)
+
+
+def test_search_picks_the_best_predicted_batch():
+    import bench
+    from paper_2408_12596_b200 import poplar
+    fits = [(0.0001, 0.157), (0.002, 0.176), (0.008, 0.219), (0.005, 0.153)]  # C5 4-GPU measured fits
+    prof = _profile(fits, [8, 8, 8, 5])
+    link = (2.17e12, 24.5e-6)
+    g, table = bench.search_gbs(_rt(), prof, 3, 4, link, (24, 40, 2))
+    assert [t[0] for t in table] == list(range(96, 161, 8))
+    best = max(t for _, t in table)
+    assert dict(table)[g] >= 0.995 * best
+    assert all(t < 0.995 * best for gg, t in table if gg < g)
+    # the table is the planner's own prediction at each batch
+    p = poplar.poplar_plan(_rt(), prof, g, 3, 4, link=link)
+    assert abs(dict(table)[g] - g / p["predicted_wall_time"]) < 1e-12
+    assert bench.search_gbs(_rt(), prof, 3, 4, link, (24, 40, 2)) == (g, table)  # deterministic
+
+
+def test_one_rank_keeps_the_smallest_batch():
+    import bench
+    prof = _profile([(0.005, 0.16)], [3])
+    g, table = bench.search_gbs(_rt(), prof, 3, 1, (float("inf"), 0.0), (24, 40, 2))
+    assert g == 24  # per-sample cost is flat on one rank: the shortest iteration wins the tie
