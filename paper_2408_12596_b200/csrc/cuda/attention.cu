@@ -112,6 +112,9 @@ __device__ __forceinline__ float4 lds_v4(const float* p) {
                : "r"(ptx::smem_u32(p)));
   return v;
 }
+__device__ __forceinline__ void red_add_v2_f32(float* p, float a, float b) {  // p 8-byte aligned
+  asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
@@ -1488,15 +1491,22 @@ __global__ void __launch_bounds__(kB2Threads, 1)
         ptx::tc_fence_before();
         if (warp == 8 && lane == 0) ATR(12, it);
         ptx::mbar_arrive(dq_free);  // the MMA warp may put dP^T(i+1) into these columns
-        // dQ^T: lane = head dim r, column = query; each reduction instruction adds one query row's
-        // 32 consecutive head dims (128 B, coalesced) into fp32 dQ. The reductions need no shared
+        // dQ^T: lane = head dim r, column = query. Lane pairs swap one value per query pair, so each
+        // lane holds two adjacent head dims of one query: a red.v2 instruction adds two query rows'
+        // 32 consecutive head dims (2 x 128 B, coalesced) into fp32 dQ. The reductions need no shared
         // memory, so nothing waits for them to drain.
-        float* dst = dq32 + (int64_t(smp) * seq + int64_t(i) * kT) * h + head * kD2 + r;
         if (!(dbg & 1)) {
+            const bool odd = lane & 1;
+            float* dst = dq32 + (int64_t(smp) * seq + int64_t(i) * kT + (odd ? 1 : 0)) * h + head * kD2 +
+                         q4 * 32 + (lane & ~1);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int j = 0; j < 32; ++j) red_add_f32(dst + int64_t(c * 32 + j) * h, __uint_as_float(v[c][j]));
+              for (int j = 0; j < 32; j += 2) {
+                const float a0 = __uint_as_float(v[c][j]), a1 = __uint_as_float(v[c][j + 1]);
+                const float got = __shfl_xor_sync(0xffffffffu, odd ? a0 : a1, 1);
+                red_add_v2_f32(dst + int64_t(c * 32 + j) * h, odd ? got : a0, odd ? a1 : got);
+              }
         }
         if (warp == 8 && lane == 0) ATR(13, it);
       }
