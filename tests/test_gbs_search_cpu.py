@@ -1,6 +1,6 @@
 """bench.py's Poplar search over the global batch (C5, BASELINE.json "full Poplar search over
 global batch"): Alg. 2 (the product planner, bit-exact with the reference) evaluated at every
-candidate batch on a profile; the chosen batch is the smallest within 0.5 % of the best predicted
+candidate batch on a profile; the chosen batch is the smallest within 0.1 % of the best predicted
 samples/s, and the choice is deterministic in its inputs (every rank must pick the same batch)."""
 import os
 import sys
@@ -29,16 +29,19 @@ def test_search_picks_the_best_predicted_batch():
     g, table = bench.search_gbs(_rt(), prof, 3, 4, link, (24, 40, 2))
     assert [t[0] for t in table] == list(range(96, 161, 8))
     best = max(t for _, t in table)
-    assert dict(table)[g] >= 0.995 * best
-    assert all(t < 0.995 * best for gg, t in table if gg < g)
+    assert dict(table)[g] >= 0.999 * best
+    assert all(t < 0.999 * best for gg, t in table if gg < g)
     # the table is the planner's own prediction at each batch
     p = poplar.poplar_plan(_rt(), prof, g, 3, 4, link=link)
     assert abs(dict(table)[g] - g / p["predicted_wall_time"]) < 1e-12
     assert bench.search_gbs(_rt(), prof, 3, 4, link, (24, 40, 2)) == (g, table)  # deterministic
 
 
-def test_one_rank_keeps_the_smallest_batch():
+def test_one_rank_picks_the_smallest_near_best_batch():
     import bench
     prof = _profile([(0.005, 0.16)], [3])
     g, table = bench.search_gbs(_rt(), prof, 3, 1, (float("inf"), 0.0), (24, 40, 2))
-    assert g == 24  # per-sample cost is flat on one rank: the shortest iteration wins the tie
+    best = max(t for _, t in table)
+    # one rank: the per-sample cost is nearly flat (only the optimizer tail amortises)
+    assert best / min(t for _, t in table) < 1.01
+    assert g == min(gg for gg, t in table if t >= 0.999 * best)
