@@ -461,6 +461,25 @@ def main():
         barrier()
         return max(allgather(local_t)), tm.to_py()
 
+    # The predicted rates of neighbouring batches differ by about the planner's prediction error,
+    # so the final choice is measured: one iteration of the plan at each of the three batches with
+    # the best predicted samples/s (after one untimed iteration each), max over ranks
+    measured_search = None
+    if search_table and world > 1:
+        top = [g for g, _ in sorted(search_table, key=lambda x: -x[1])[:3]]
+        measured_search = {}
+        for g in top:
+            p_g = poplar.poplar_plan(rt, profile, g, stage, world, link=link)
+            f_g, c_g = poplar.rank_slice(p_g, rank)
+            rt.load_tokens(first_sample=f_g, count=max(c_g, 1), iteration=0)
+            rt.execute_iteration(p_g, stage)
+            T_g, _ = timed(1, p_g)
+            measured_search[g] = g / T_g
+        gbs = max(measured_search, key=measured_search.get)
+        plan = poplar.poplar_plan(rt, profile, gbs, stage, world, link=link)
+        first, count = poplar.rank_slice(plan, rank)
+        rt.load_tokens(first_sample=first, count=max(count, 1), iteration=0)
+
     # heterogeneity-blind baseline at the same (final) global batch, from the Alg. 1 profile
     uniform = poplar.poplar_plan(rt, profile_initial, gbs, stage, world, uniform=True, link=link)
     rt.execute_iteration(plan, stage)  # the final plan once more before the timed region
@@ -594,7 +613,9 @@ def main():
             "config": {"workload": cfg["label"], "model": cfg["model"], "params": rt.param_count,
                        "seq_len": model.seq_len, "head_dim": model.head_dim, "global_batch": gbs,
                        "gbs_search": ({"per_gpu_range": list(search), "chosen": gbs,
-                                       "predicted_samples_per_s": {str(g): t for g, t in search_table}}
+                                       "predicted_samples_per_s": {str(g): t for g, t in search_table},
+                                       "measured_top3_samples_per_s": ({str(g): v for g, v in measured_search.items()}
+                                                                       if measured_search else None)}
                                       if search_table else None),
                        "stage": stage,
                        "sm_budgets": [cfg["tiers"][r % len(cfg["tiers"])] for r in range(world)],
